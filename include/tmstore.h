@@ -1,0 +1,145 @@
+/*
+ * tmstore — B200-resident session-history store for the trajectory-manager hot path.
+ *
+ * C ABI (extern "C", plain pointers and sizes, no torch/CUDA types beyond an opaque
+ * `void *stream` that is a cudaStream_t or NULL).  The reference has no FFI: its
+ * boundary is the Python class SessionTrie (/root/reference/pkg/src/rolloutlab/trie.py)
+ * called by TrajectoryManager (trajectory.py).  Each entry point below names the
+ * reference interface it replaces; INTEGRATION.md shows the ctypes binding.
+ *
+ * Model: a store holds many sessions.  Every distinct recorded sequence of a session
+ * is a ROW (global id int64; session-local ordinal int32 in order of first
+ * appearance).  A row stores only its novel suffix [matched, len); its prefix is
+ * inherited from its PARENT row = the earliest-inserted row whose longest common
+ * prefix with it equals `matched` (-1 when matched == 0).  Shared prefixes keep the
+ * metadata of their first writer (trie.py:9-11).
+ *
+ * Status codes: TM_OK, TM_EINVAL (reference: ValueError), TM_ENOENT (KeyError /
+ * UnknownSessionError), TM_ENOMEM / TM_ECUDA (RuntimeError).  tm_last_error()
+ * returns a thread-local message for the last failing call on this thread.
+ *
+ * Memory kinds: TM_MEM_HOST — every array argument is host memory (pageable or
+ * pinned); the call is synchronous.  TM_MEM_DEVICE — token/offset/output arrays are
+ * device pointers on the store's GPU; the call is asynchronous on `stream`.  Device
+ * token buffers must start every sequence at a 128-byte aligned word offset
+ * (tok_off[k] % 32 == 0) and be readable up to the next 128-byte boundary.
+ *
+ * Thread safety: every call locks the store; callers may use any thread.
+ */
+#ifndef TMSTORE_H
+#define TMSTORE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tm_store tm_store;
+
+enum { TM_OK = 0, TM_EINVAL = 1, TM_ENOENT = 2, TM_ENOMEM = 3, TM_ECUDA = 4 };
+enum { TM_MEM_HOST = 0, TM_MEM_DEVICE = 1 };
+enum { TM_ORDER_INSERT = 0, TM_ORDER_LEX = 1 };
+enum { TM_ORIGIN_AGENT_INPUT = 0, TM_ORIGIN_MODEL_OUTPUT = 1 };
+
+typedef struct {
+  int32_t device;           /* CUDA device ordinal */
+  int64_t arena_words;      /* initial token-arena capacity (int32 words); grows x2 */
+  int64_t row_capacity;     /* initial row-table capacity; grows x2 */
+  int64_t run_capacity;     /* initial metadata-run capacity; grows x2 */
+  int64_t session_capacity; /* initial session capacity; grows x2 */
+} tm_config;
+
+/* Thread-local message describing the last error returned on this thread. */
+const char *tm_last_error(void);
+/* Library version string. */
+const char *tm_version(void);
+
+/* Create / destroy a store on one GPU.  cfg may be NULL (defaults).
+ * Replaces: the per-session `SessionTrie(session_id)` objects held in
+ * TrajectoryManager._sessions (trajectory.py:128, 137-145, trie.py:93-99). */
+int tm_store_create(const tm_config *cfg, tm_store **out);
+int tm_store_destroy(tm_store *store);
+
+/* Open a new empty session; returns its dense id.
+ * Replaces: `_Session(trie=SessionTrie(session_id))` (trajectory.py:143). */
+int tm_session_create(tm_store *store, int32_t *out_sid);
+int tm_session_count(tm_store *store, int64_t *out_n);
+
+/* Record a batch of sequences: the batched `SessionTrie.lpm_insert` (trie.py:120-179)
+ * with sequential semantics — entry k sees every earlier entry of the batch.
+ *   sids[n]          session of each sequence
+ *   tokens/tok_off/tok_len   sequence k = tokens[tok_off[k] : tok_off[k] + tok_len[k]]
+ *   run_off[n+1]     metadata runs of sequence k = runs[run_off[k] : run_off[k+1]]
+ *   run_start[]      run start relative to its sequence (first must be 0, ascending)
+ *   run_origin[]     TM_ORIGIN_* ; run_version[] model version
+ * Outputs (any may be NULL), one per entry:
+ *   out_matched      matched_prefix_length           (InsertResult, trie.py:71-75)
+ *   out_row          global row id of the sequence   (node_id)
+ *   out_local        session-local row ordinal
+ *   out_parent       global parent row (-1 if none)
+ *   out_parent_local session-local parent ordinal (-1 if none)
+ *   out_added        added_tokens (= len - matched, 0 for an existing sequence)
+ * mem applies to the token/run/sid inputs; outputs are host arrays (the call is
+ * synchronous, as lpm_insert is).  Errors: empty sequence or non-parallel metadata
+ * -> TM_EINVAL (trie.py:128-131); unknown session -> TM_ENOENT. */
+int tm_record_batch(tm_store *store, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
+                    const int64_t *tok_off, const int64_t *tok_len, const int64_t *run_off,
+                    const int32_t *run_start, const uint8_t *run_origin, const int32_t *run_version,
+                    int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
+                    int32_t *out_parent_local, int64_t *out_added);
+
+/* Read-only longest-prefix match of a batch of queries (no mutation): the LPM walk
+ * of lpm_insert (trie.py:136-158) without the record step.
+ *   out_matched[n]   LCP length with the best stored sequence of the session
+ *   out_parent[n]    global row achieving it (earliest such), -1 if matched == 0
+ *   out_dup[n]       global row equal to the query, -1 if none
+ * TM_MEM_HOST: all arrays host, synchronous.  TM_MEM_DEVICE: all arrays device,
+ * asynchronous on `stream` (NULL = the store's stream).  Unknown/empty -> matched 0. */
+int tm_match_batch(tm_store *store, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
+                   const int64_t *tok_off, const int64_t *tok_len, int64_t *out_matched, int64_t *out_parent,
+                   int64_t *out_dup, void *stream);
+
+/* Total tokens of a list of rows (to size tm_export_rows outputs). */
+int tm_rows_total(tm_store *store, int64_t n, const int64_t *rows, int64_t *out_total);
+
+/* Reconstruct rows into packed token-id batches: path_trajectory / extract /
+ * drain_batch assembly (trie.py:203-224, core.py:88-98, trajectory.py:342-363).
+ *   rows[n]              global row ids (host array)
+ *   out_offsets[n+1]     cu_seqlens-style row offsets (host array, always)
+ *   out_tokens/mask/versions  packed arrays of out_offsets[n] entries; mask is
+ *                        loss_mask (1 = MODEL_OUTPUT); memory kind `mem_out`
+ *   out_resp_start[n]    1 + last position whose mask is 0 (0 if none): where the
+ *                        trailing model response begins (kind `mem_out`, may be NULL)
+ * TM_MEM_DEVICE outputs are written asynchronously on `stream`. */
+int tm_export_rows(tm_store *store, int64_t n, const int64_t *rows, int32_t mem_out, int64_t *out_offsets,
+                   int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
+                   void *stream);
+
+/* StorageStats of a session (trie.py:78-87, 184-185; trajectory.py:369-372). */
+int tm_session_stats(tm_store *store, int32_t sid, int64_t *stored, int64_t *naive, int64_t *nrows);
+
+/* Rows of a session (global ids) in insertion order or in lexicographic sequence
+ * order — the order of SessionTrie.extract (trie.py:189-198, 210-216).
+ * Writes min(cap, nrows) ids; *n_out = nrows. */
+int tm_session_rows(tm_store *store, int32_t sid, int32_t order, int64_t *out_rows, int64_t cap,
+                    int64_t *n_out);
+
+/* Describe one global row. */
+int tm_row_info(tm_store *store, int64_t row, int32_t *sid, int32_t *local, int64_t *parent,
+                int64_t *matched, int64_t *length);
+
+/* Store-wide counters: rows, arena words used, arena capacity, max row-tree depth. */
+int tm_store_stats(tm_store *store, int64_t *rows, int64_t *arena_used, int64_t *arena_cap,
+                   int64_t *max_depth);
+
+/* The store's CUDA stream (cudaStream_t) for callers that want to order work after it. */
+int tm_store_stream(tm_store *store, void **out_stream);
+
+/* Block until all work queued on the store's stream is done. */
+int tm_synchronize(tm_store *store);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,385 @@
+// Kernels of the tmstore (see kernels.cuh for the data layout).
+//
+//  k_plan_lpt      single CTA: longest-first processing order (counting sort on length)
+//  k_walk          K1: longest-prefix-match walk, one CTA per query, vectorised compare
+//  k_commit_plan   single CTA: allocation scan (row ids, arena slots, run slots)
+//  k_commit        K2: append novel suffixes + metadata runs, branch-index insert, stats
+//  k_export        K3: chain walk + gather into packed tokens / loss_mask / versions
+//  k_rehash        branch-index growth
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace tms {
+
+// ----------------------------------------------------------------------------------
+// Longest-first order: bucket = min(NB-1, len >> 8), descending.  One CTA.
+constexpr int kPlanNT = 1024;
+constexpr int kPlanNB = 2048;
+
+__global__ void __launch_bounds__(kPlanNT) k_plan_lpt(Batch b, int64_t *order) {
+  __shared__ int hist[kPlanNB];
+  for (int i = threadIdx.x; i < kPlanNB; i += kPlanNT) hist[i] = 0;
+  __syncthreads();
+  for (int64_t w = threadIdx.x; w < b.n; w += kPlanNT) {
+    int64_t L = b.len[w];
+    int bk = (int)(L >> 8 < kPlanNB - 1 ? L >> 8 : kPlanNB - 1);
+    atomicAdd(&hist[kPlanNB - 1 - bk], 1);  // descending length
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan (2048 entries; negligible)
+    int acc = 0;
+    for (int i = 0; i < kPlanNB; i++) { int c = hist[i]; hist[i] = acc; acc += c; }
+  }
+  __syncthreads();
+  for (int64_t w = threadIdx.x; w < b.n; w += kPlanNT) {
+    int64_t L = b.len[w];
+    int bk = (int)(L >> 8 < kPlanNB - 1 ? L >> 8 : kPlanNB - 1);
+    int pos = atomicAdd(&hist[kPlanNB - 1 - bk], 1);
+    order[pos] = w;
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// K1 walk.  Per query: root lookup (session, q[0]) -> row; compare the row's own
+// segment from the current position; at the first mismatch j look up the child
+// branching at (row, j, q[j]); continue in the child or finish.
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
+  __shared__ int s_red[NT / 32];
+  __shared__ long long s_item;
+  __shared__ long long s_row;
+  __shared__ int s_lo;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(b.work, 1ull);
+    __syncthreads();
+    const int64_t it = s_item;
+    if (it >= b.n) return;
+    const int64_t w = b.order ? b.order[it] : it;
+    const int32_t *q = b.tok + b.off[w];
+    const int L = (int)b.len[w];
+    const int32_t sid = b.sids[w];
+    if (threadIdx.x == 0) {
+      int64_t r = -1;
+      if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+      if (r < 0) {  // nothing shares the first token: matched 0
+        b.o_m[w] = 0;
+        b.o_parent[w] = -1;
+        b.o_dup[w] = -1;
+        if (b.o_tnext) { b.o_tnext[w] = L > 0 ? q[0] : -1; b.o_spar[w] = -1; }
+      }
+      s_row = r;
+      s_lo = 1;
+    }
+    __syncthreads();
+    int64_t r = s_row;
+    int lo = s_lo;
+    __syncthreads();
+    while (r >= 0) {
+      const int Lr = v.row_len[r];
+      const int hi = min(Lr, L);
+      const int32_t *a = v.arena + v.row_vb[r];
+      const int j = block_first_mismatch<NT, U>(q, a, lo, hi, s_red);
+      if (threadIdx.x == 0) {
+        int64_t next = -1;
+        if (j < L) {
+          const int32_t t = q[j];
+          next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
+          if (next < 0) {
+            b.o_m[w] = j;
+            b.o_parent[w] = r;
+            b.o_dup[w] = -1;
+            if (b.o_tnext) { b.o_tnext[w] = t; b.o_spar[w] = j < Lr ? a[j] : -1; }
+          }
+        } else {  // the query ended inside (or at the end of) row r
+          int64_t dup = (L == Lr) ? r : ht_find(v, (uint64_t)r, dt_key(L, 0, true));
+          b.o_m[w] = L;
+          b.o_parent[w] = r;
+          b.o_dup[w] = dup;
+          if (b.o_tnext) { b.o_tnext[w] = -1; b.o_spar[w] = L < Lr ? a[L] : -1; }
+        }
+        s_row = next;
+        s_lo = j + 1;
+      }
+      __syncthreads();
+      r = s_row;
+      lo = s_lo;
+      __syncthreads();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// Commit planner: one CTA scans the batch for new rows and allocates row ids, arena
+// slots (128-byte lines covering [floor32(m), ceil32(L)) ) and metadata-run slots.
+constexpr int kScanNT = 1024;
+
+__device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m) {
+  // index (relative) of the run containing position m (runs start at 0, ascending)
+  int64_t r0 = b.run_off[w], r1 = b.run_off[w + 1];
+  int64_t lo = r0, hi = r1;  // last run with start <= m
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (b.run_start[mid] <= m) lo = mid; else hi = mid;
+  }
+  return (int)(lo - r0);
+}
+
+__global__ void __launch_bounds__(kScanNT) k_commit_plan(DevView v, Batch b) {
+  __shared__ long long s_w[kScanNT / 32], s_r[kScanNT / 32], s_n[kScanNT / 32];
+  __shared__ long long base_w, base_r, base_n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { base_w = v.ctr[0]; base_n = v.ctr[1]; base_r = v.ctr[2]; }
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < b.n; t0 += kScanNT) {
+    const int64_t w = t0 + threadIdx.x;
+    long long words = 0, runs = 0, isnew = 0;
+    int fr = 0;
+    int64_t m = 0, L = 0;
+    if (w < b.n) {
+      m = b.o_m[w];
+      L = b.len[w];
+      if (b.o_dup[w] < 0) {
+        isnew = 1;
+        if (L > m) {
+          words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
+          fr = first_run_at(b, w, m);
+          runs = (b.run_off[w + 1] - b.run_off[w]) - fr;
+        }
+      }
+    }
+    // block exclusive scans of (words, runs, isnew)
+    long long xw = words, xr = runs, xn = isnew;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      long long yw = __shfl_up_sync(0xffffffffu, xw, d);
+      long long yr = __shfl_up_sync(0xffffffffu, xr, d);
+      long long yn = __shfl_up_sync(0xffffffffu, xn, d);
+      if (lane >= d) { xw += yw; xr += yr; xn += yn; }
+    }
+    if (lane == 31) { s_w[warp] = xw; s_r[warp] = xr; s_n[warp] = xn; }
+    __syncthreads();
+    if (warp == 0) {
+      long long a = s_w[lane], c = s_r[lane], e = s_n[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        long long ya = __shfl_up_sync(0xffffffffu, a, d);
+        long long yc = __shfl_up_sync(0xffffffffu, c, d);
+        long long ye = __shfl_up_sync(0xffffffffu, e, d);
+        if (lane >= d) { a += ya; c += yc; e += ye; }
+      }
+      s_w[lane] = a; s_r[lane] = c; s_n[lane] = e;  // inclusive per-warp totals
+    }
+    __syncthreads();
+    const long long pw = (warp ? s_w[warp - 1] : 0) + xw - words;
+    const long long pr = (warp ? s_r[warp - 1] : 0) + xr - runs;
+    const long long pn = (warp ? s_n[warp - 1] : 0) + xn - isnew;
+    if (w < b.n) {
+      if (isnew) {
+        b.c_row[w] = base_n + pn;
+        b.c_vb[w] = base_w + pw - (m / kAlignWords) * kAlignWords;
+        b.c_run0[w] = base_r + pr;
+        b.c_firstrun[w] = fr;
+      } else {
+        b.c_row[w] = b.o_dup[w];
+        b.c_vb[w] = 0;
+        b.c_run0[w] = 0;
+        b.c_firstrun[w] = 0;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      base_w += s_w[kScanNT / 32 - 1];
+      base_r += s_r[kScanNT / 32 - 1];
+      base_n += s_n[kScanNT / 32 - 1];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { v.ctr[0] = base_w; v.ctr[1] = base_n; v.ctr[2] = base_r; }
+}
+
+// ----------------------------------------------------------------------------------
+// K2 commit: one CTA per entry (grid-stride).  At most one entry per session per
+// wave, so session counters need no atomics.
+constexpr int kCommitNT = 256;
+
+__global__ void __launch_bounds__(kCommitNT) k_commit(DevView v, Batch b) {
+  for (int64_t w = blockIdx.x; w < b.n; w += gridDim.x) {
+    const int64_t m = b.o_m[w];
+    const int64_t L = b.len[w];
+    const int32_t sid = b.sids[w];
+    const int64_t row = b.c_row[w];
+    const bool isnew = b.o_dup[w] < 0;
+    if (threadIdx.x == 0) {
+      if (isnew) {
+        const int64_t par = b.o_parent[w];
+        const int32_t local = v.s_nrows[sid];
+        v.s_nrows[sid] = local + 1;
+        v.row_vb[row] = b.c_vb[w];
+        v.row_m[row] = (int32_t)m;
+        v.row_len[row] = (int32_t)L;
+        v.row_parent[row] = par;
+        v.row_sess[row] = sid;
+        v.row_local[row] = local;
+        v.row_depth[row] = par >= 0 ? v.row_depth[par] + 1 : 0;
+        v.row_run0[row] = b.c_run0[w];
+        v.row_nrun[row] = L > m ? (int32_t)(b.run_off[w + 1] - b.run_off[w] - b.c_firstrun[w]) : 0;
+        v.s_stored[sid] += L - m;
+        const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
+        if (L > m) ht_insert(v, owner, dt_key(m, b.tok[b.off[w] + m], false), row);
+        else ht_insert(v, owner, dt_key(m, 0, true), row);
+        b.c_local[w] = local;
+      } else {
+        b.c_local[w] = v.row_local[row];
+      }
+      v.s_naive[sid] += L;
+    }
+    if (!isnew || L <= m) continue;
+    // novel suffix: int4 copy of [m, L) (congruent mod 4 words; edges land in padding)
+    const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[w]);
+    int4 *dst = reinterpret_cast<int4 *>(v.arena + b.c_vb[w]);
+    for (int64_t i = (m >> 2) + threadIdx.x; i < ((L + 3) >> 2); i += kCommitNT) dst[i] = ldg_stream(src + i);
+    // metadata runs overlapping [m, L), first one clamped to m
+    const int64_t r0 = b.run_off[w] + b.c_firstrun[w];
+    const int64_t nr = b.run_off[w + 1] - r0;
+    for (int64_t k = threadIdx.x; k < nr; k += kCommitNT) {
+      const int64_t d = b.c_run0[w] + k;
+      const int32_t st = b.run_start[r0 + k];
+      v.run_start[d] = (int32_t)(st > m ? (int64_t)st : m);
+      v.run_origin[d] = b.run_origin[r0 + k];
+      v.run_version[d] = b.run_version[r0 + k];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// K3 export: one CTA per (row, 4096-position tile).  Walk the parent chain from the
+// row; each ancestor owns positions [m_x, upper); copy tokens and expand runs.
+constexpr int kExportNT = 256;
+constexpr int kExportTile = 4096;
+
+struct ExportArgs {
+  int64_t n;
+  const int64_t *rows;
+  const int64_t *out_off;   // n+1
+  const int64_t *tile_off;  // n+1
+  int64_t ntiles;
+  int32_t *tokens;
+  uint8_t *mask;
+  int32_t *versions;
+  unsigned long long *resp;  // n (atomicMax), may be null
+};
+
+__global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
+  for (int64_t t = blockIdx.x; t < e.ntiles; t += gridDim.x) {
+    int64_t lo = 0, hi = e.n;  // largest i with tile_off[i] <= t
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (e.tile_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int64_t i = lo;
+    const int64_t row = e.rows[i];
+    const int64_t a = (t - e.tile_off[i]) * kExportTile;
+    const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
+    const int64_t o = e.out_off[i];
+    int64_t cur = row, upper = v.row_len[row];
+    long long respmax = 0;
+    while (cur >= 0 && upper > a) {
+      const int64_t mx = v.row_m[cur];
+      const int64_t pa = max(mx, a), pb = min(upper, b);
+      if (pa < pb) {
+        const int32_t *src = v.arena + v.row_vb[cur];
+        for (int64_t p = pa + threadIdx.x; p < pb; p += kExportNT) e.tokens[o + p] = src[p];
+        const int64_t r0 = v.row_run0[cur];
+        const int nr = v.row_nrun[cur];
+        const int64_t lenx = v.row_len[cur];
+        int lo2 = 0, hi2 = nr;  // last run with start <= pa
+        while (hi2 - lo2 > 1) {
+          int mid = (lo2 + hi2) >> 1;
+          if (v.run_start[r0 + mid] <= pa) lo2 = mid; else hi2 = mid;
+        }
+        for (int k = lo2; k < nr; k++) {
+          const int64_t rs = v.run_start[r0 + k];
+          if (rs >= pb) break;
+          const int64_t re = (k + 1 < nr) ? v.run_start[r0 + k + 1] : lenx;
+          const int64_t xa = max(rs, pa), xb = min(re, pb);
+          const uint8_t org = v.run_origin[r0 + k];
+          const int32_t ver = v.run_version[r0 + k];
+          for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) {
+            e.mask[o + p] = org;
+            e.versions[o + p] = ver;
+          }
+          if (org == 0 && xb > respmax) respmax = xb;
+        }
+      }
+      upper = mx;
+      cur = v.row_parent[cur];
+    }
+    if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[i], (unsigned long long)respmax);
+  }
+}
+
+// ----------------------------------------------------------------------------------
+__global__ void k_rehash(DevView v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval, int64_t ocap) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < ocap; s += (int64_t)gridDim.x * blockDim.x) {
+    if (ok0[s] != kEmpty) ht_insert(v, ok0[s], ok1[s], oval[s]);
+  }
+}
+
+__global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t val) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) p[s] = val;
+}
+
+// ----------------------------------------------------------------------------------
+// launchers
+constexpr int kWalkNT = 256;
+constexpr int kWalkU = 4;
+
+cudaError_t launch_plan_lpt(const Batch &b, int64_t *order, cudaStream_t s) {
+  k_plan_lpt<<<1, kPlanNT, 0, s>>>(b, order);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<kWalkNT, kWalkU>, kWalkNT, 0);
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)num_sms * occ;
+  if (grid > b.n) grid = b.n;
+  if (grid < 1) grid = 1;
+  k_walk<kWalkNT, kWalkU><<<(int)grid, kWalkNT, 0, s>>>(v, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+  k_commit_plan<<<1, kScanNT, 0, s>>>(v, b);
+  int64_t grid = b.n < (int64_t)num_sms * 8 ? b.n : (int64_t)num_sms * 8;
+  if (grid < 1) grid = 1;
+  k_commit<<<(int)grid, kCommitNT, 0, s>>>(v, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {
+  ExportArgs e{h.n, h.rows, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions,
+               (unsigned long long *)h.resp};
+  int64_t grid = h.ntiles < (int64_t)num_sms * 8 ? h.ntiles : (int64_t)num_sms * 8;
+  if (grid < 1) return cudaSuccess;
+  k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
+                          int64_t ocap, cudaStream_t s) {
+  k_rehash<<<1024, 256, 0, s>>>(v, ok0, ok1, oval, ocap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s) {
+  k_fill_u64<<<1024, 256, 0, s>>>(p, n, val);
+  return cudaGetLastError();
+}
+
+int export_tile_tokens() { return kExportTile; }
+
+}  // namespace tms

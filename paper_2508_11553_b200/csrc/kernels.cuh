@@ -1,0 +1,184 @@
+// Device side of the tmstore: session-history arena, branch index, and the three
+// hot kernels (K1 prefix-match walk, K2 record/commit, K3 trajectory assembly).
+// sm_100a; integer and HBM-bound — no tensor cores.  See DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tms {
+
+constexpr int kAlignWords = 32;  // 128-byte lines: sequence positions are stored congruent mod 32
+constexpr uint64_t kEmpty = ~0ull;
+constexpr uint64_t kRootTag = 1ull << 62;
+
+// Device view of the store (passed by value to every kernel).
+struct DevView {
+  int32_t *arena;  // token arena; row r's position p lives at arena[row_vb[r] + p]
+  // row table (global row id)
+  int64_t *row_vb;     // virtual base, multiple of 32 words
+  int32_t *row_m;      // matched length = first own position
+  int32_t *row_len;    // sequence length
+  int64_t *row_parent; // -1 for none
+  int32_t *row_sess;
+  int32_t *row_local;
+  int32_t *row_depth;
+  int64_t *row_run0;   // first metadata run
+  int32_t *row_nrun;
+  // metadata runs (absolute start positions within the row's sequence)
+  int32_t *run_start;
+  int32_t *run_version;
+  uint8_t *run_origin;
+  // branch index: open addressing, key (owner, depth|term|token) -> child row
+  uint64_t *hk0;
+  uint64_t *hk1;
+  int64_t *hval;
+  uint64_t ht_mask;
+  // sessions
+  int32_t *s_nrows;
+  int64_t *s_stored;
+  int64_t *s_naive;
+  // allocation counters (device-resident, advanced by the commit planner)
+  int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=error flags
+};
+
+// one batch of sequences resident on the device
+struct Batch {
+  int64_t n;
+  const int32_t *sids;
+  const int32_t *tok;     // tokens; sequence w starts at tok + off[w] (multiple of 32)
+  const int64_t *off;
+  const int64_t *len;
+  const int64_t *order;   // optional processing order (longest first)
+  unsigned long long *work;  // work counter (zeroed before launch)
+  // walk outputs
+  int64_t *o_m;
+  int64_t *o_parent;
+  int64_t *o_dup;
+  int32_t *o_tnext;  // query token at the mismatch (-1 if the query ended)
+  int32_t *o_spar;   // parent's token at the mismatch (-1 if the parent ended)
+  // metadata runs (record only)
+  const int64_t *run_off;
+  const int32_t *run_start;
+  const uint8_t *run_origin;
+  const int32_t *run_version;
+  // commit plan outputs (record only)
+  int64_t *c_row;
+  int64_t *c_vb;
+  int64_t *c_run0;
+  int32_t *c_firstrun;
+  int32_t *c_local;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t dt_key(int64_t depth, int32_t token, bool term) {
+  return ((uint64_t)depth << 33) | ((uint64_t)(term ? 1 : 0) << 32) | (uint64_t)(uint32_t)token;
+}
+
+__device__ __forceinline__ uint64_t slot_of(uint64_t owner, uint64_t dt, uint64_t mask) {
+  return mix64(owner * 0x9e3779b97f4a7c15ull ^ mix64(dt + 0x632be59bd9b4e019ull)) & mask;
+}
+
+__device__ __forceinline__ int64_t ht_find(const DevView &v, uint64_t owner, uint64_t dt) {
+  uint64_t s = slot_of(owner, dt, v.ht_mask);
+  for (;;) {
+    uint64_t k0 = v.hk0[s];
+    if (k0 == kEmpty) return -1;
+    if (k0 == owner && v.hk1[s] == dt) return v.hval[s];
+    s = (s + 1) & v.ht_mask;
+  }
+}
+
+__device__ __forceinline__ void ht_insert(const DevView &v, uint64_t owner, uint64_t dt, int64_t val) {
+  uint64_t s = slot_of(owner, dt, v.ht_mask);
+  for (;;) {
+    unsigned long long prev = atomicCAS((unsigned long long *)&v.hk0[s], (unsigned long long)kEmpty,
+                                        (unsigned long long)owner);
+    if (prev == kEmpty) {
+      v.hk1[s] = dt;
+      v.hval[s] = val;
+      return;
+    }
+    s = (s + 1) & v.ht_mask;
+  }
+}
+
+__device__ __forceinline__ int4 ldg_stream(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// First mismatch position in [lo, hi) between q[] and a[] (both indexed by absolute
+// position, 16-byte congruent), or hi.  Whole-block call; all threads get the result.
+// Each warp owns 32*U consecutive int4 per chunk; the next chunk is prefetched into
+// registers while the current one is checked; __syncthreads_or gates early exit.
+template <int NT, int U>
+__device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
+                                                    int lo, int hi, int *s_red) {
+  if (lo >= hi) return hi;
+  const int4 *q4 = reinterpret_cast<const int4 *>(q);
+  const int4 *a4 = reinterpret_cast<const int4 *>(a);
+  const int v0 = lo >> 2, v1 = (hi + 3) >> 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CH = NT * U;
+  const int tb = warp * (32 * U) + lane;
+  int4 qa[U], aa[U], qb[U], ab[U];
+  int base = v0;
+#pragma unroll
+  for (int k = 0; k < U; k++) {
+    int idx = base + tb + k * 32;
+    if (idx < v1) { qa[k] = ldg_stream(q4 + idx); aa[k] = ldg_stream(a4 + idx); }
+    else { qa[k] = make_int4(0, 0, 0, 0); aa[k] = qa[k]; }
+  }
+  for (;;) {
+    const int nb = base + CH;
+    const bool more = nb < v1;
+    if (more) {
+#pragma unroll
+      for (int k = 0; k < U; k++) {
+        int idx = nb + tb + k * 32;
+        if (idx < v1) { qb[k] = ldg_stream(q4 + idx); ab[k] = ldg_stream(a4 + idx); }
+        else { qb[k] = make_int4(0, 0, 0, 0); ab[k] = qb[k]; }
+      }
+    }
+    int first = 0x7fffffff;
+#pragma unroll
+    for (int k = U - 1; k >= 0; k--) {
+      int p = (base + tb + k * 32) * 4;
+      unsigned ne = (qa[k].x != aa[k].x ? 1u : 0u) | (qa[k].y != aa[k].y ? 2u : 0u) |
+                    (qa[k].z != aa[k].z ? 4u : 0u) | (qa[k].w != aa[k].w ? 8u : 0u);
+      // mask positions outside [lo, hi)
+      unsigned valid = 0xfu;
+      if (p < lo) valid &= (0xfu << (lo - p)) & 0xfu;
+      if (p + 4 > hi) valid &= (hi - p) <= 0 ? 0u : (0xfu >> (4 - (hi - p)));
+      ne &= valid;
+      if (ne) first = p + __ffs(ne) - 1;
+    }
+    if (__syncthreads_or(first != 0x7fffffff)) {
+      unsigned wmin = __reduce_min_sync(0xffffffffu, (unsigned)first);
+      if (lane == 0) s_red[warp] = (int)wmin;
+      __syncthreads();
+      int r = 0x7fffffff;
+#pragma unroll
+      for (int w = 0; w < NT / 32; w++) r = min(r, s_red[w]);
+      __syncthreads();
+      return r;
+    }
+    if (!more) return hi;
+    base = nb;
+#pragma unroll
+    for (int k = 0; k < U; k++) { qa[k] = qb[k]; aa[k] = ab[k]; }
+  }
+}
+
+}  // namespace tms

@@ -1,0 +1,30 @@
+// Host-visible launchers for the tmstore kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tms {
+struct DevView;
+struct Batch;
+
+struct ExportArgsHost {
+  int64_t n;
+  const int64_t *rows;
+  const int64_t *out_off;
+  const int64_t *tile_off;
+  int64_t ntiles;
+  int32_t *tokens;
+  uint8_t *mask;
+  int32_t *versions;
+  int64_t *resp;
+};
+
+cudaError_t launch_plan_lpt(const Batch &b, int64_t *order, cudaStream_t s);
+cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
+cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
+cudaError_t launch_export(const DevView &v, const ExportArgsHost &e, int num_sms, cudaStream_t s);
+cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
+                          int64_t ocap, cudaStream_t s);
+cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
+int export_tile_tokens();
+}  // namespace tms

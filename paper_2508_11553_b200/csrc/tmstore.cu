@@ -1,0 +1,744 @@
+// tmstore host runtime + C ABI (include/tmstore.h).
+//
+// One store per GPU: device arena / row table / metadata runs / branch index /
+// session counters, a host mirror of the row table (ids, lengths, parents, branch
+// tokens) used for planning, lexicographic ordering and export sizing, pinned
+// staging for host-memory calls, and one CUDA stream.  Every entry point locks the
+// store mutex; ctypes callers release the GIL around the call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tmstore.h"
+#include "kernels.cuh"
+#include "launch.h"
+
+using tms::DevView;
+using tms::Batch;
+
+static thread_local std::string g_err;
+
+namespace {
+
+struct TmError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string &msg) { throw TmError{code, msg}; }
+
+void ck(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) {
+    fail(e == cudaErrorMemoryAllocation ? TM_ENOMEM : TM_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+template <class T>
+void dev_grow(T *&p, int64_t old_n, int64_t new_n, cudaStream_t s) {
+  T *q = nullptr;
+  ck(cudaMalloc((void **)&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1)), "cudaMalloc(grow)");
+  if (p && old_n > 0) ck(cudaMemcpyAsync(q, p, sizeof(T) * (size_t)old_n, cudaMemcpyDeviceToDevice, s), "grow copy");
+  ck(cudaStreamSynchronize(s), "grow sync");
+  if (p) cudaFree(p);
+  p = q;
+}
+
+// growable byte buffers (device scratch / pinned staging)
+struct DevBytes {
+  void *p = nullptr;
+  size_t cap = 0;
+  void *need(size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      size_t c = std::max<size_t>(n, cap * 2);
+      ck(cudaMalloc(&p, c), "cudaMalloc(scratch)");
+      cap = c;
+    }
+    return p;
+  }
+  ~DevBytes() { if (p) cudaFree(p); }
+};
+
+struct PinBytes {
+  void *p = nullptr;
+  size_t cap = 0;
+  void *need(size_t n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      size_t c = std::max<size_t>(n, cap * 2);
+      ck(cudaHostAlloc(&p, c, cudaHostAllocDefault), "cudaHostAlloc(staging)");
+      cap = c;
+    }
+    return p;
+  }
+  ~PinBytes() { if (p) cudaFreeHost(p); }
+};
+
+// lay out several arrays in one buffer
+struct Layout {
+  size_t bytes = 0;
+  size_t add(size_t n) {
+    size_t o = bytes;
+    bytes += (n + 255) / 256 * 256;
+    return o;
+  }
+};
+
+struct RowHost {
+  int32_t sid, local;
+  int64_t parent;
+  int32_t m, len, depth;
+  int32_t tnext, spar;
+};
+
+}  // namespace
+
+struct tm_store {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t last = nullptr;
+  std::mutex mu;
+  DevView v{};
+  int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
+  int64_t arena_used = 0, n_runs = 0, n_sess = 0;
+  std::vector<RowHost> rows;
+  std::vector<std::vector<int64_t>> sess_rows;
+  std::vector<int64_t> sess_stored, sess_naive;
+  int64_t max_depth = 0;
+  DevBytes scratch, dtok;
+  PinBytes pin, ptok;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void ensure_rows(tm_store *s, int64_t need) {
+  if (need <= s->row_cap) return;
+  int64_t nc = std::max<int64_t>(need, s->row_cap * 2);
+  int64_t n = (int64_t)s->rows.size();
+  dev_grow(s->v.row_vb, n, nc, s->stream);
+  dev_grow(s->v.row_m, n, nc, s->stream);
+  dev_grow(s->v.row_len, n, nc, s->stream);
+  dev_grow(s->v.row_parent, n, nc, s->stream);
+  dev_grow(s->v.row_sess, n, nc, s->stream);
+  dev_grow(s->v.row_local, n, nc, s->stream);
+  dev_grow(s->v.row_depth, n, nc, s->stream);
+  dev_grow(s->v.row_run0, n, nc, s->stream);
+  dev_grow(s->v.row_nrun, n, nc, s->stream);
+  s->row_cap = nc;
+}
+
+void ensure_runs(tm_store *s, int64_t need) {
+  if (need <= s->run_cap) return;
+  int64_t nc = std::max<int64_t>(need, s->run_cap * 2);
+  dev_grow(s->v.run_start, s->n_runs, nc, s->stream);
+  dev_grow(s->v.run_version, s->n_runs, nc, s->stream);
+  dev_grow(s->v.run_origin, s->n_runs, nc, s->stream);
+  s->run_cap = nc;
+}
+
+void ensure_arena(tm_store *s, int64_t need) {
+  if (need <= s->arena_cap) return;
+  int64_t nc = std::max<int64_t>(round_up(need, 1 << 20), s->arena_cap * 2);
+  dev_grow(s->v.arena, s->arena_used, nc, s->stream);
+  s->arena_cap = nc;
+}
+
+void ensure_sessions(tm_store *s, int64_t need) {
+  if (need <= s->sess_cap) return;
+  int64_t nc = std::max<int64_t>(need, s->sess_cap * 2);
+  int64_t n = s->n_sess;
+  dev_grow(s->v.s_nrows, n, nc, s->stream);
+  dev_grow(s->v.s_stored, n, nc, s->stream);
+  dev_grow(s->v.s_naive, n, nc, s->stream);
+  ck(cudaMemsetAsync(s->v.s_nrows + n, 0, sizeof(int32_t) * (nc - n), s->stream), "memset");
+  ck(cudaMemsetAsync(s->v.s_stored + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
+  ck(cudaMemsetAsync(s->v.s_naive + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
+  s->sess_cap = nc;
+}
+
+void alloc_table(tm_store *s, int64_t cap) {
+  ck(cudaMalloc((void **)&s->v.hk0, sizeof(uint64_t) * cap), "cudaMalloc(ht)");
+  ck(cudaMalloc((void **)&s->v.hk1, sizeof(uint64_t) * cap), "cudaMalloc(ht)");
+  ck(cudaMalloc((void **)&s->v.hval, sizeof(int64_t) * cap), "cudaMalloc(ht)");
+  ck(tms::launch_fill_u64(s->v.hk0, cap, tms::kEmpty, s->stream), "ht fill");
+  s->ht_cap = cap;
+  s->v.ht_mask = (uint64_t)cap - 1;
+}
+
+// keep the branch index at load <= 1/2
+void ensure_table(tm_store *s, int64_t entries) {
+  if (entries * 2 <= s->ht_cap) return;
+  int64_t nc = s->ht_cap;
+  while (entries * 2 > nc) nc *= 2;
+  uint64_t *o0 = s->v.hk0, *o1 = s->v.hk1;
+  int64_t *ov = s->v.hval;
+  int64_t oc = s->ht_cap;
+  alloc_table(s, nc);
+  ck(tms::launch_rehash(s->v, o0, o1, ov, oc, s->stream), "rehash");
+  ck(cudaStreamSynchronize(s->stream), "rehash sync");
+  cudaFree(o0);
+  cudaFree(o1);
+  cudaFree(ov);
+}
+
+void wait_prev(tm_store *s, cudaStream_t st) {
+  ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
+}
+
+void mark_done(tm_store *s, cudaStream_t st) { ck(cudaEventRecord(s->last, st), "cudaEventRecord"); }
+
+template <class F>
+int guarded(tm_store *s, F &&f) {
+  if (!s) {
+    g_err = "null store";
+    return TM_EINVAL;
+  }
+  try {
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard dg(s->device);
+    f();
+    return TM_OK;
+  } catch (const TmError &e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc &) {
+    g_err = "host allocation failed";
+    return TM_ENOMEM;
+  }
+}
+
+// Stage host sequences into the pinned buffer with 128-byte aligned starts and copy
+// them to the device token scratch.  Returns device offsets (host vector).
+void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off, const int64_t *tok_len,
+                  std::vector<int64_t> &doff, const std::vector<int64_t> *perm) {
+  doff.resize(n);
+  int64_t total = 0;
+  for (int64_t k = 0; k < n; k++) {
+    int64_t e = perm ? (*perm)[k] : k;
+    doff[k] = total;
+    total += round_up(std::max<int64_t>(tok_len[e], 1), tms::kAlignWords);
+  }
+  int32_t *h = (int32_t *)s->ptok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
+  for (int64_t k = 0; k < n; k++) {
+    int64_t e = perm ? (*perm)[k] : k;
+    int64_t L = tok_len[e];
+    memcpy(h + doff[k], tokens + tok_off[e], sizeof(int32_t) * (size_t)L);
+    int64_t pad = round_up(std::max<int64_t>(L, 1), tms::kAlignWords) - L;
+    memset(h + doff[k] + L, 0, sizeof(int32_t) * (size_t)pad);
+  }
+  void *d = s->dtok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
+  if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, s->stream), "H2D tokens");
+}
+
+void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, int64_t r, std::vector<int64_t> &out) {
+  // kids[local] = children of that row sorted by (m, prefix-first, tnext).  Order of
+  // the subtree of r:
+  //   for each branch depth d < len(r), ascending: [prefix row at d] + [children whose
+  //   token at d is below r's token at d] ... then r itself, then its extensions,
+  //   then, deepest depth first, the children whose token at d is above r's.
+  const RowHost &R = s->rows[r];
+  const auto &ch = kids[R.local];
+  std::vector<int64_t> hi_list;
+  std::vector<size_t> hi_mark;
+  size_t i = 0;
+  while (i < ch.size() && s->rows[ch[i]].m < R.len) {
+    const int32_t d = s->rows[ch[i]].m;
+    hi_mark.push_back(hi_list.size());
+    for (; i < ch.size() && s->rows[ch[i]].m == d; i++) {
+      const RowHost &C = s->rows[ch[i]];
+      if (C.len == C.m) out.push_back(ch[i]);
+      else if (C.tnext < C.spar) lex_emit(s, kids, ch[i], out);
+      else hi_list.push_back(ch[i]);
+    }
+  }
+  out.push_back(r);
+  for (; i < ch.size(); i++) lex_emit(s, kids, ch[i], out);
+  for (size_t g = hi_mark.size(); g-- > 0;) {
+    const size_t a = hi_mark[g], b = (g + 1 < hi_mark.size()) ? hi_mark[g + 1] : hi_list.size();
+    for (size_t k = a; k < b; k++) lex_emit(s, kids, hi_list[k], out);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tm_last_error(void) { return g_err.c_str(); }
+const char *tm_version(void) { return "tmstore 0.1.0 (sm_100a)"; }
+
+int tm_store_create(const tm_config *cfg, tm_store **out) {
+  if (!out) {
+    g_err = "null out";
+    return TM_EINVAL;
+  }
+  tm_config c{0, 1 << 22, 1 << 12, 1 << 14, 1 << 10};
+  if (cfg) c = *cfg;
+  tm_store *s = new tm_store();
+  s->device = c.device;
+  int rc = guarded(s, [&] {
+    ck(cudaSetDevice(c.device), "cudaSetDevice");
+    ck(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, c.device), "attr");
+    ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&s->last, cudaEventDisableTiming), "event");
+    ck(cudaMalloc((void **)&s->v.ctr, sizeof(int64_t) * 4), "ctr");
+    ck(cudaMemsetAsync(s->v.ctr, 0, sizeof(int64_t) * 4, s->stream), "ctr");
+    ensure_arena(s, std::max<int64_t>(c.arena_words, 1 << 16));
+    ensure_rows(s, std::max<int64_t>(c.row_capacity, 64));
+    ensure_runs(s, std::max<int64_t>(c.run_capacity, 64));
+    ensure_sessions(s, std::max<int64_t>(c.session_capacity, 16));
+    int64_t ht = 1024;
+    while (ht < 2 * s->row_cap) ht *= 2;
+    alloc_table(s, ht);
+    mark_done(s, s->stream);
+    ck(cudaStreamSynchronize(s->stream), "create sync");
+  });
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return TM_OK;
+}
+
+int tm_store_destroy(tm_store *s) {
+  if (!s) return TM_OK;
+  {
+    DeviceGuard dg(s->device);
+    cudaStreamSynchronize(s->stream);
+    void *ptrs[] = {s->v.arena, s->v.row_vb, s->v.row_m, s->v.row_len, s->v.row_parent, s->v.row_sess,
+                    s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.run_start,
+                    s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
+                    s->v.s_stored, s->v.s_naive, s->v.ctr};
+    for (void *p : ptrs)
+      if (p) cudaFree(p);
+    s->scratch.~DevBytes();
+    new (&s->scratch) DevBytes();
+    s->dtok.~DevBytes();
+    new (&s->dtok) DevBytes();
+    cudaEventDestroy(s->last);
+    cudaStreamDestroy(s->stream);
+  }
+  delete s;
+  return TM_OK;
+}
+
+int tm_session_create(tm_store *s, int32_t *out_sid) {
+  return guarded(s, [&] {
+    if (s->n_sess >= INT32_MAX) fail(TM_ENOMEM, "too many sessions");
+    ensure_sessions(s, s->n_sess + 1);
+    s->sess_rows.emplace_back();
+    s->sess_stored.push_back(0);
+    s->sess_naive.push_back(0);
+    *out_sid = (int32_t)s->n_sess++;
+  });
+}
+
+int tm_session_count(tm_store *s, int64_t *out_n) {
+  return guarded(s, [&] { *out_n = s->n_sess; });
+}
+
+int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
+                    const int64_t *tok_off, const int64_t *tok_len, const int64_t *run_off,
+                    const int32_t *run_start, const uint8_t *run_origin, const int32_t *run_version,
+                    int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
+                    int32_t *out_parent_local, int64_t *out_added) {
+  return guarded(s, [&] {
+    if (n < 0) fail(TM_EINVAL, "negative batch size");
+    if (n == 0) return;
+    if (mem != TM_MEM_HOST) fail(TM_EINVAL, "tm_record_batch: only TM_MEM_HOST inputs are supported");
+    // ---- validate (trie.py:128-131) and build waves: entry k of a session goes to
+    // wave (number of earlier entries of that session in the batch)
+    std::vector<int32_t> occ(s->n_sess, 0);
+    std::vector<int32_t> wave(n);
+    int32_t nwaves = 0;
+    int64_t total_runs = 0, words_upper = 0;
+    for (int64_t k = 0; k < n; k++) {
+      int32_t sid = sids[k];
+      if (sid < 0 || sid >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sid));
+      int64_t L = tok_len[k];
+      if (L <= 0) fail(TM_EINVAL, "cannot insert an empty sequence");
+      if (L >= (int64_t)INT32_MAX - 64) fail(TM_EINVAL, "sequence too long");
+      int64_t r0 = run_off[k], r1 = run_off[k + 1];
+      if (r1 <= r0 || run_start[r0] != 0) fail(TM_EINVAL, "tokens, origins, versions must be parallel");
+      for (int64_t r = r0 + 1; r < r1; r++)
+        if (run_start[r] <= run_start[r - 1] || run_start[r] >= L)
+          fail(TM_EINVAL, "tokens, origins, versions must be parallel");
+      for (int64_t r = r0; r < r1; r++)
+        if (run_origin[r] > 1) fail(TM_EINVAL, "bad origin");
+      wave[k] = occ[sid]++;
+      nwaves = std::max(nwaves, wave[k] + 1);
+      total_runs += r1 - r0;
+      words_upper += round_up(L, tms::kAlignWords) + tms::kAlignWords;
+    }
+    // stable order by wave
+    std::vector<int64_t> perm(n);
+    {
+      std::vector<int64_t> cnt(nwaves + 1, 0);
+      for (int64_t k = 0; k < n; k++) cnt[wave[k] + 1]++;
+      for (int32_t w = 0; w < nwaves; w++) cnt[w + 1] += cnt[w];
+      std::vector<int64_t> wbeg(cnt.begin(), cnt.end());
+      for (int64_t k = 0; k < n; k++) perm[cnt[wave[k]]++] = k;
+      cnt.assign(wbeg.begin(), wbeg.end());
+      // capacity (upper bounds)
+      ensure_arena(s, s->arena_used + words_upper);
+      ensure_rows(s, (int64_t)s->rows.size() + n);
+      ensure_runs(s, s->n_runs + total_runs);
+      ensure_table(s, (int64_t)s->rows.size() + n);
+      wait_prev(s, s->stream);
+      // ---- stage tokens and per-entry arrays
+      std::vector<int64_t> doff;
+      stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
+      Layout lay;
+      size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
+             o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs);
+      size_t in_bytes = lay.bytes;
+      size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
+             o_sp = lay.add(4 * n), o_crow = lay.add(8 * n), o_cloc = lay.add(4 * n);
+      size_t out_end = lay.bytes;
+      size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n), o_ord = lay.add(8 * n),
+             o_work = lay.add(8 * (size_t)nwaves);
+      char *h = (char *)s->pin.need(lay.bytes);
+      char *d = (char *)s->scratch.need(lay.bytes);
+      int32_t *h_sid = (int32_t *)(h + o_sid);
+      int64_t *h_off = (int64_t *)(h + o_off), *h_len = (int64_t *)(h + o_len), *h_roff = (int64_t *)(h + o_roff);
+      int32_t *h_rs = (int32_t *)(h + o_rs), *h_rv = (int32_t *)(h + o_rv);
+      uint8_t *h_ro = (uint8_t *)(h + o_ro);
+      int64_t rr = 0;
+      for (int64_t k = 0; k < n; k++) {
+        int64_t e = perm[k];
+        h_sid[k] = sids[e];
+        h_off[k] = doff[k];
+        h_len[k] = tok_len[e];
+        h_roff[k] = rr;
+        int64_t r0 = run_off[e], r1 = run_off[e + 1];
+        memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
+        memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
+        memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
+        rr += r1 - r0;
+      }
+      h_roff[n] = rr;
+      ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
+      ck(cudaMemsetAsync(d + o_work, 0, 8 * (size_t)nwaves, s->stream), "memset work");
+      // ---- waves: walk (K1) then commit (K2)
+      for (int32_t w = 0; w < nwaves; w++) {
+        int64_t b0 = wbeg[w], b1 = wbeg[w + 1];
+        Batch b{};
+        b.n = b1 - b0;
+        b.sids = (const int32_t *)(d + o_sid) + b0;
+        b.tok = (const int32_t *)s->dtok.p;
+        b.off = (const int64_t *)(d + o_off) + b0;
+        b.len = (const int64_t *)(d + o_len) + b0;
+        b.order = nullptr;
+        b.work = (unsigned long long *)(d + o_work) + w;
+        b.o_m = (int64_t *)(d + o_m) + b0;
+        b.o_parent = (int64_t *)(d + o_par) + b0;
+        b.o_dup = (int64_t *)(d + o_dup) + b0;
+        b.o_tnext = (int32_t *)(d + o_tn) + b0;
+        b.o_spar = (int32_t *)(d + o_sp) + b0;
+        b.run_off = (const int64_t *)(d + o_roff) + b0;
+        b.run_start = (const int32_t *)(d + o_rs);
+        b.run_origin = (const uint8_t *)(d + o_ro);
+        b.run_version = (const int32_t *)(d + o_rv);
+        b.c_row = (int64_t *)(d + o_crow) + b0;
+        b.c_vb = (int64_t *)(d + o_cvb) + b0;
+        b.c_run0 = (int64_t *)(d + o_cr0) + b0;
+        b.c_firstrun = (int32_t *)(d + o_cfr) + b0;
+        b.c_local = (int32_t *)(d + o_cloc) + b0;
+        if (b.n >= 512) {
+          int64_t *ord = (int64_t *)(d + o_ord) + b0;
+          ck(tms::launch_plan_lpt(b, ord, s->stream), "plan");
+          b.order = ord;
+        }
+        ck(tms::launch_walk(s->v, b, s->num_sms, s->stream), "walk");
+        ck(tms::launch_commit(s->v, b, s->num_sms, s->stream), "commit");
+      }
+      // ---- results back
+      char *hout = h + o_m;
+      ck(cudaMemcpyAsync(hout, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, s->stream), "D2H results");
+      int64_t ctr[4];
+      ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
+      mark_done(s, s->stream);
+      ck(cudaStreamSynchronize(s->stream), "record sync");
+      const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
+                    *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
+      const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
+                    *r_loc = (const int32_t *)(h + o_cloc);
+      for (int64_t k = 0; k < n; k++) {
+        int64_t e = perm[k];
+        int32_t sid = sids[e];
+        int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
+        if (r_dup[k] < 0) {
+          if (row != (int64_t)s->rows.size()) fail(TM_ECUDA, "row numbering out of sync");
+          RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
+          rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
+          s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
+          s->rows.push_back(rh);
+          s->sess_rows[sid].push_back(row);
+          s->sess_stored[sid] += L - m;
+        }
+        s->sess_naive[sid] += L;
+        if (out_matched) out_matched[e] = m;
+        if (out_row) out_row[e] = row;
+        if (out_local) out_local[e] = r_loc[k];
+        if (out_parent) out_parent[e] = par;
+        if (out_parent_local) out_parent_local[e] = par >= 0 ? s->rows[par].local : -1;
+        if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
+      }
+      s->arena_used = ctr[0];
+      s->n_runs = ctr[2];
+      if (ctr[1] != (int64_t)s->rows.size()) fail(TM_ECUDA, "row counter out of sync");
+    }
+  });
+}
+
+int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
+                   const int64_t *tok_off, const int64_t *tok_len, int64_t *out_matched, int64_t *out_parent,
+                   int64_t *out_dup, void *stream) {
+  return guarded(s, [&] {
+    if (n < 0) fail(TM_EINVAL, "negative batch size");
+    if (n == 0) return;
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    wait_prev(s, st);
+    Layout lay;
+    size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n);
+    size_t in_bytes = lay.bytes;
+    size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n);
+    size_t out_end = lay.bytes;
+    size_t o_ord = lay.add(8 * n), o_work = lay.add(8);
+    char *d = (char *)s->scratch.need(lay.bytes);
+    Batch b{};
+    b.n = n;
+    b.work = (unsigned long long *)(d + o_work);
+    if (mem == TM_MEM_HOST) {
+      for (int64_t k = 0; k < n; k++)
+        if (sids[k] < 0 || sids[k] >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sids[k]));
+      std::vector<int64_t> doff;
+      // stage on the chosen stream
+      cudaStream_t keep = s->stream;
+      s->stream = st;
+      stage_tokens(s, n, tokens, tok_off, tok_len, doff, nullptr);
+      s->stream = keep;
+      char *h = (char *)s->pin.need(lay.bytes);
+      memcpy(h + o_sid, sids, 4 * n);
+      memcpy(h + o_off, doff.data(), 8 * n);
+      memcpy(h + o_len, tok_len, 8 * n);
+      ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D batch");
+      b.sids = (const int32_t *)(d + o_sid);
+      b.tok = (const int32_t *)s->dtok.p;
+      b.off = (const int64_t *)(d + o_off);
+      b.len = (const int64_t *)(d + o_len);
+      b.o_m = (int64_t *)(d + o_m);
+      b.o_parent = (int64_t *)(d + o_par);
+      b.o_dup = (int64_t *)(d + o_dup);
+    } else if (mem == TM_MEM_DEVICE) {
+      b.sids = sids;
+      b.tok = tokens;
+      b.off = tok_off;
+      b.len = tok_len;
+      b.o_m = out_matched;
+      b.o_parent = out_parent;
+      b.o_dup = out_dup;
+    } else {
+      fail(TM_EINVAL, "bad memory kind");
+    }
+    ck(cudaMemsetAsync(b.work, 0, 8, st), "memset work");
+    if (n >= 512) {
+      ck(tms::launch_plan_lpt(b, (int64_t *)(d + o_ord), st), "plan");
+      b.order = (const int64_t *)(d + o_ord);
+    }
+    ck(tms::launch_walk(s->v, b, s->num_sms, st), "walk");
+    if (mem == TM_MEM_HOST) {
+      char *h = (char *)s->pin.need(lay.bytes);
+      ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, st), "D2H");
+      mark_done(s, st);
+      ck(cudaStreamSynchronize(st), "match sync");
+      memcpy(out_matched, h + o_m, 8 * n);
+      if (out_parent) memcpy(out_parent, h + o_par, 8 * n);
+      if (out_dup) memcpy(out_dup, h + o_dup, 8 * n);
+    } else {
+      mark_done(s, st);
+    }
+  });
+}
+
+int tm_rows_total(tm_store *s, int64_t n, const int64_t *rows, int64_t *out_total) {
+  return guarded(s, [&] {
+    int64_t t = 0;
+    for (int64_t k = 0; k < n; k++) {
+      if (rows[k] < 0 || rows[k] >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
+      t += s->rows[rows[k]].len;
+    }
+    *out_total = t;
+  });
+}
+
+int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out, int64_t *out_offsets,
+                   int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
+                   void *stream) {
+  return guarded(s, [&] {
+    if (n < 0) fail(TM_EINVAL, "negative batch size");
+    if (mem_out != TM_MEM_HOST && mem_out != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
+    out_offsets[0] = 0;
+    if (n == 0) return;
+    const int64_t T = tms::export_tile_tokens();
+    std::vector<int64_t> tile(n + 1);
+    tile[0] = 0;
+    for (int64_t k = 0; k < n; k++) {
+      if (rows[k] < 0 || rows[k] >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
+      int64_t L = s->rows[rows[k]].len;
+      out_offsets[k + 1] = out_offsets[k] + L;
+      tile[k + 1] = tile[k] + (L + T - 1) / T;
+    }
+    const int64_t total = out_offsets[n];
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    wait_prev(s, st);
+    Layout lay;
+    size_t o_rows = lay.add(8 * n), o_off = lay.add(8 * (n + 1)), o_tile = lay.add(8 * (n + 1));
+    size_t in_bytes = lay.bytes;
+    size_t o_tok = 0, o_msk = 0, o_ver = 0, o_resp = 0;
+    if (mem_out == TM_MEM_HOST) {
+      o_tok = lay.add(4 * total);
+      o_msk = lay.add(total);
+      o_ver = lay.add(4 * total);
+      o_resp = lay.add(8 * n);
+    }
+    char *d = (char *)s->scratch.need(lay.bytes);
+    char *h = (char *)s->pin.need(in_bytes);
+    memcpy(h + o_rows, rows, 8 * n);
+    memcpy(h + o_off, out_offsets, 8 * (n + 1));
+    memcpy(h + o_tile, tile.data(), 8 * (n + 1));
+    ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D export plan");
+    tms::ExportArgsHost e{};
+    e.n = n;
+    e.rows = (const int64_t *)(d + o_rows);
+    e.out_off = (const int64_t *)(d + o_off);
+    e.tile_off = (const int64_t *)(d + o_tile);
+    e.ntiles = tile[n];
+    if (mem_out == TM_MEM_HOST) {
+      e.tokens = (int32_t *)(d + o_tok);
+      e.mask = (uint8_t *)(d + o_msk);
+      e.versions = (int32_t *)(d + o_ver);
+      e.resp = (int64_t *)(d + o_resp);
+    } else {
+      e.tokens = out_tokens;
+      e.mask = out_mask;
+      e.versions = out_versions;
+      e.resp = out_resp_start;
+    }
+    if (e.resp) ck(cudaMemsetAsync(e.resp, 0, 8 * n, st), "memset resp");
+    ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
+    if (mem_out == TM_MEM_HOST) {
+      if (out_tokens) ck(cudaMemcpyAsync(out_tokens, e.tokens, 4 * total, cudaMemcpyDeviceToHost, st), "D2H tokens");
+      if (out_mask) ck(cudaMemcpyAsync(out_mask, e.mask, total, cudaMemcpyDeviceToHost, st), "D2H mask");
+      if (out_versions) ck(cudaMemcpyAsync(out_versions, e.versions, 4 * total, cudaMemcpyDeviceToHost, st), "D2H versions");
+      if (out_resp_start) ck(cudaMemcpyAsync(out_resp_start, e.resp, 8 * n, cudaMemcpyDeviceToHost, st), "D2H resp");
+      mark_done(s, st);
+      ck(cudaStreamSynchronize(st), "export sync");
+    } else {
+      mark_done(s, st);
+    }
+  });
+}
+
+int tm_session_stats(tm_store *s, int32_t sid, int64_t *stored, int64_t *naive, int64_t *nrows) {
+  return guarded(s, [&] {
+    if (sid < 0 || sid >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sid));
+    if (stored) *stored = s->sess_stored[sid];
+    if (naive) *naive = s->sess_naive[sid];
+    if (nrows) *nrows = (int64_t)s->sess_rows[sid].size();
+  });
+}
+
+int tm_session_rows(tm_store *s, int32_t sid, int32_t order, int64_t *out_rows, int64_t cap, int64_t *n_out) {
+  return guarded(s, [&] {
+    if (sid < 0 || sid >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sid));
+    const auto &rs = s->sess_rows[sid];
+    *n_out = (int64_t)rs.size();
+    if (order == TM_ORDER_INSERT) {
+      for (int64_t k = 0; k < (int64_t)rs.size() && k < cap; k++) out_rows[k] = rs[k];
+      return;
+    }
+    if (order != TM_ORDER_LEX) fail(TM_EINVAL, "bad order");
+    // children lists indexed by session-local ordinal; root rows hang off a virtual root
+    const int64_t nr = (int64_t)rs.size();
+    std::vector<std::vector<int64_t>> kids_local(nr);
+    std::vector<int64_t> roots;
+    for (int64_t k = 0; k < nr; k++) {
+      const RowHost &R = s->rows[rs[k]];
+      if (R.parent < 0) roots.push_back(rs[k]);
+      else kids_local[s->rows[R.parent].local].push_back(rs[k]);
+    }
+    auto cmp = [&](int64_t a, int64_t b) {
+      const RowHost &A = s->rows[a], &B = s->rows[b];
+      if (A.m != B.m) return A.m < B.m;
+      bool pa = A.len == A.m, pb = B.len == B.m;
+      if (pa != pb) return pa;
+      return A.tnext < B.tnext;
+    };
+    for (auto &v : kids_local) std::sort(v.begin(), v.end(), cmp);
+    std::sort(roots.begin(), roots.end(), [&](int64_t a, int64_t b) { return s->rows[a].tnext < s->rows[b].tnext; });
+    std::vector<int64_t> out;
+    out.reserve(nr);
+    for (int64_t r : roots) lex_emit(s, kids_local, r, out);
+    for (int64_t k = 0; k < (int64_t)out.size() && k < cap; k++) out_rows[k] = out[k];
+  });
+}
+
+int tm_row_info(tm_store *s, int64_t row, int32_t *sid, int32_t *local, int64_t *parent, int64_t *matched,
+                int64_t *length) {
+  return guarded(s, [&] {
+    if (row < 0 || row >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(row) + " not in store");
+    const RowHost &R = s->rows[row];
+    if (sid) *sid = R.sid;
+    if (local) *local = R.local;
+    if (parent) *parent = R.parent;
+    if (matched) *matched = R.m;
+    if (length) *length = R.len;
+  });
+}
+
+int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *arena_cap, int64_t *max_depth) {
+  return guarded(s, [&] {
+    if (rows) *rows = (int64_t)s->rows.size();
+    if (arena_used) *arena_used = s->arena_used;
+    if (arena_cap) *arena_cap = s->arena_cap;
+    if (max_depth) *max_depth = s->max_depth;
+  });
+}
+
+int tm_store_stream(tm_store *s, void **out_stream) {
+  return guarded(s, [&] { *out_stream = (void *)s->stream; });
+}
+
+int tm_synchronize(tm_store *s) {
+  return guarded(s, [&] {
+    ck(cudaStreamSynchronize(s->stream), "sync");
+    ck(cudaEventSynchronize(s->last), "sync");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+"""Batched Python front end of the B200 session-history store (libtmstore.so).
+
+``DeviceStore`` owns one tm_store on one GPU.  Host-array calls are synchronous
+(they are what the drop-in SessionTrie / TrajectoryManager use); the ``*_device``
+variants take CUDA tensors and enqueue on a stream (trainer handoff, benchmarks).
+PyTorch is used only to hand device memory and streams across; all compute is in
+the CUDA kernels behind the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import TM_MEM_DEVICE, TM_MEM_HOST, TM_ORDER_INSERT, TM_ORDER_LEX, check
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _tptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def runs_from_per_token(origins: np.ndarray, versions: np.ndarray):
+    """Per-token (origin code, version) -> run starts / origins / versions."""
+    n = len(origins)
+    if n == 0:
+        return np.zeros(0, np.int32), np.zeros(0, np.uint8), np.zeros(0, np.int32)
+    o = np.asarray(origins, dtype=np.int64)
+    v = np.asarray(versions, dtype=np.int64)
+    cut = np.flatnonzero((o[1:] != o[:-1]) | (v[1:] != v[:-1])) + 1
+    starts = np.concatenate(([0], cut))
+    return starts.astype(np.int32), o[starts].astype(np.uint8), v[starts].astype(np.int32)
+
+
+@dataclass
+class RecordResult:
+    """Per-entry outputs of a record batch (numpy arrays, batch order)."""
+
+    matched: np.ndarray   # int64, InsertResult.matched_prefix_length
+    row: np.ndarray       # int64 global row id
+    local: np.ndarray     # int32 session-local ordinal (node_id of the drop-in API)
+    parent: np.ndarray    # int64 global parent row, -1 if none
+    parent_local: np.ndarray  # int32
+    added: np.ndarray     # int64, InsertResult.added_tokens
+
+
+@dataclass
+class Packed:
+    """cu_seqlens-style packed trajectories."""
+
+    offsets: np.ndarray  # int64 [n+1]
+    tokens: object       # int32 [total]  (numpy on host, torch tensor on device)
+    loss_mask: object    # uint8 [total]
+    versions: object     # int32 [total]
+    resp_start: object   # int64 [n]: where the trailing model response starts
+
+
+class DeviceStore:
+    """A GPU-resident store of many sessions (one per device per process)."""
+
+    def __init__(self, device: int = 0, *, arena_words: int = 1 << 22, row_capacity: int = 1 << 12,
+                 run_capacity: int = 1 << 14, session_capacity: int = 1 << 10):
+        self.lib = _lib.load()
+        cfg = _lib.TmConfig(device, arena_words, row_capacity, run_capacity, session_capacity)
+        h = C.c_void_p()
+        check(self.lib.tm_store_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tm_store_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sessions ----------------------------------------------------------------
+    def new_session(self) -> int:
+        sid = C.c_int32()
+        check(self.lib.tm_session_create(self.h, C.byref(sid)))
+        return sid.value
+
+    def session_stats(self, sid: int) -> tuple[int, int, int]:
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(self.lib.tm_session_stats(self.h, sid, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def session_rows(self, sid: int, order: str = "insert") -> np.ndarray:
+        _, _, n = self.session_stats(sid)
+        out = np.empty(max(n, 1), np.int64)
+        got = C.c_int64()
+        code = TM_ORDER_LEX if order == "lex" else TM_ORDER_INSERT
+        check(self.lib.tm_session_rows(self.h, sid, code, _ptr(out), n, C.byref(got)))
+        return out[: got.value]
+
+    def row_info(self, row: int):
+        sid, loc = C.c_int32(), C.c_int32()
+        par, m, L = C.c_int64(), C.c_int64(), C.c_int64()
+        check(self.lib.tm_row_info(self.h, row, C.byref(sid), C.byref(loc), C.byref(par), C.byref(m), C.byref(L)))
+        return dict(session=sid.value, local=loc.value, parent=par.value, matched=m.value, length=L.value)
+
+    def stats(self) -> dict:
+        r, u, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        check(self.lib.tm_store_stats(self.h, C.byref(r), C.byref(u), C.byref(c), C.byref(d)))
+        return dict(rows=r.value, arena_used=u.value, arena_cap=c.value, max_depth=d.value)
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(self.lib.tm_store_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        check(self.lib.tm_synchronize(self.h))
+
+    # -- record (batched lpm_insert) ------------------------------------------------
+    def record_packed(self, sids, tokens, tok_off, tok_len, run_off, run_start, run_origin, run_version) -> RecordResult:
+        sids = np.ascontiguousarray(sids, np.int32)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        tok_off = np.ascontiguousarray(tok_off, np.int64)
+        tok_len = np.ascontiguousarray(tok_len, np.int64)
+        run_off = np.ascontiguousarray(run_off, np.int64)
+        run_start = np.ascontiguousarray(run_start, np.int32)
+        run_origin = np.ascontiguousarray(run_origin, np.uint8)
+        run_version = np.ascontiguousarray(run_version, np.int32)
+        n = len(sids)
+        if not (len(tok_off) >= n and len(tok_len) == n and len(run_off) == n + 1):
+            raise ValueError("inconsistent batch arrays")
+        r = RecordResult(np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.int32),
+                         np.empty(n, np.int64), np.empty(n, np.int32), np.empty(n, np.int64))
+        check(self.lib.tm_record_batch(
+            self.h, n, TM_MEM_HOST, _ptr(sids), _ptr(tokens), _ptr(tok_off), _ptr(tok_len), _ptr(run_off),
+            _ptr(run_start), _ptr(run_origin), _ptr(run_version), _ptr(r.matched), _ptr(r.row), _ptr(r.local),
+            _ptr(r.parent), _ptr(r.parent_local), _ptr(r.added)))
+        return r
+
+    def record(self, sids, seqs, runs) -> RecordResult:
+        """seqs: list of int sequences; runs: list of (starts, origins, versions)."""
+        lens = np.fromiter((len(s) for s in seqs), np.int64, len(seqs))
+        off = np.zeros(len(seqs) + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        tokens = np.concatenate([np.asarray(s, np.int64) for s in seqs]) if seqs else np.zeros(0, np.int64)
+        if tokens.size and (tokens.min() < -(2**31) or tokens.max() >= 2**31):
+            raise ValueError("token ids must fit in int32")
+        rc = np.fromiter((len(r[0]) for r in runs), np.int64, len(runs))
+        roff = np.zeros(len(runs) + 1, np.int64)
+        np.cumsum(rc, out=roff[1:])
+        cat = lambda i, dt: np.concatenate([np.asarray(r[i], dt) for r in runs]) if runs else np.zeros(0, dt)  # noqa: E731
+        return self.record_packed(sids, tokens, off[:-1], lens, roff, cat(0, np.int32), cat(1, np.uint8), cat(2, np.int32))
+
+    # -- read-only match --------------------------------------------------------------
+    def match(self, sids, tokens, tok_off, tok_len):
+        sids = np.ascontiguousarray(sids, np.int32)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        tok_off = np.ascontiguousarray(tok_off, np.int64)
+        tok_len = np.ascontiguousarray(tok_len, np.int64)
+        n = len(sids)
+        m = np.empty(n, np.int64)
+        p = np.empty(n, np.int64)
+        d = np.empty(n, np.int64)
+        check(self.lib.tm_match_batch(self.h, n, TM_MEM_HOST, _ptr(sids), _ptr(tokens), _ptr(tok_off), _ptr(tok_len),
+                                      _ptr(m), _ptr(p), _ptr(d), None))
+        return m, p, d
+
+    def match_device(self, sids, tokens, tok_off, tok_len, out_matched, out_parent, out_dup, stream=None):
+        """All CUDA tensors on this store's device; tok_off multiples of 32; enqueued on
+        ``stream`` (a cudaStream_t int, default: torch's current stream)."""
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(self.lib.tm_match_batch(self.h, sids.numel(), TM_MEM_DEVICE, _tptr(sids), _tptr(tokens), _tptr(tok_off),
+                                      _tptr(tok_len), _tptr(out_matched), _tptr(out_parent), _tptr(out_dup),
+                                      C.c_void_p(stream)))
+
+    # -- export (trajectory assembly) ---------------------------------------------------
+    def rows_total(self, rows) -> int:
+        rows = np.ascontiguousarray(rows, np.int64)
+        t = C.c_int64()
+        check(self.lib.tm_rows_total(self.h, len(rows), _ptr(rows), C.byref(t)))
+        return t.value
+
+    def export(self, rows) -> Packed:
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = len(rows)
+        total = self.rows_total(rows) if n else 0
+        off = np.zeros(n + 1, np.int64)
+        tok = np.empty(total, np.int32)
+        msk = np.empty(total, np.uint8)
+        ver = np.empty(total, np.int32)
+        resp = np.empty(n, np.int64)
+        check(self.lib.tm_export_rows(self.h, n, _ptr(rows), TM_MEM_HOST, _ptr(off), _ptr(tok), _ptr(msk), _ptr(ver),
+                                      _ptr(resp), None))
+        return Packed(off, tok, msk, ver, resp)
+
+    def export_device(self, rows, stream=None) -> Packed:
+        """Packed trajectories left on the GPU as torch tensors (trainer handoff)."""
+        import torch
+
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = len(rows)
+        total = self.rows_total(rows) if n else 0
+        dev = torch.device("cuda", self.device)
+        tok = torch.empty(total, dtype=torch.int32, device=dev)
+        msk = torch.empty(total, dtype=torch.uint8, device=dev)
+        ver = torch.empty(total, dtype=torch.int32, device=dev)
+        resp = torch.empty(n, dtype=torch.int64, device=dev)
+        off = np.zeros(n + 1, np.int64)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(self.lib.tm_export_rows(self.h, n, _ptr(rows), TM_MEM_DEVICE, _ptr(off), _tptr(tok), _tptr(msk), _tptr(ver),
+                                      _tptr(resp), C.c_void_p(stream)))
+        return Packed(off, tok, msk, ver, resp)
+
+
+_default: dict[int, DeviceStore] = {}
+
+
+def default_store(device: int = 0) -> DeviceStore:
+    """Process-wide store for stand-alone SessionTrie objects."""
+    st = _default.get(device)
+    if st is None:
+        st = _default[device] = DeviceStore(device)
+    return st

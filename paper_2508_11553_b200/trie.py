@@ -1,0 +1,268 @@
+"""Drop-in ``SessionTrie`` (reference: rolloutlab/trie.py:90-255) backed by the B200 store.
+
+A session's recorded sequences live in the GPU arena as rows (novel suffix + parent
+pointer); matching, recording and reconstruction run in CUDA kernels.  This class
+keeps the reference's public surface:
+
+* ``lpm_insert(tokens, origins, versions, completion_id=None) -> InsertResult``
+* ``stats() -> StorageStats``; ``total_stored_tokens`` / ``total_naive_tokens``
+* ``extract() -> [(node_id, Trajectory)]`` in lexicographic order (marked rows)
+* ``path_trajectory(node_id)``, ``mark``, ``marked_nodes``, ``check_well_formed``
+* ``root`` / ``nodes``: a radix-tree VIEW materialised from the rows on demand
+  (debug and API fidelity only; never on the hot path).
+
+``node_id`` is the session-local row ordinal: identical sequences get the same id,
+extensions a new one, and ids survive later branching.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from .core import ORIGIN_CODE, ModelVersion, SpanOrigin, TokenId, Trajectory
+from .store import DeviceStore, default_store, runs_from_per_token
+
+MetaRun = tuple[int, SpanOrigin, ModelVersion]
+
+
+@dataclass
+class InsertResult:
+    matched_prefix_length: int
+    node_id: int
+    added_tokens: int
+
+
+@dataclass
+class StorageStats:
+    stored_tokens: int
+    naive_tokens: int
+
+    @property
+    def dedup_ratio(self) -> float:
+        if self.naive_tokens == 0:
+            return 1.0
+        return self.stored_tokens / self.naive_tokens
+
+
+@dataclass
+class TrieNode:
+    """Node of the materialised radix view (same fields as trie.py:58-68)."""
+
+    node_id: int
+    tokens: list[TokenId]
+    runs: list[MetaRun]
+    children: dict[TokenId, "TrieNode"] = field(default_factory=dict)
+    leaf_marks: set[str] = field(default_factory=set)
+
+    @property
+    def is_marked(self) -> bool:
+        return bool(self.leaf_marks)
+
+
+def _origins_to_codes(origins: Sequence[SpanOrigin]) -> np.ndarray:
+    if isinstance(origins, np.ndarray):
+        return origins.astype(np.int64)
+    try:
+        return np.fromiter((ORIGIN_CODE[o] for o in origins), np.int64, len(origins))
+    except KeyError:
+        return np.fromiter((1 if o in (1, True, "model_output") else 0 for o in origins), np.int64, len(origins))
+
+
+class SessionTrie:
+    """One session of the B200 store, with the reference SessionTrie API."""
+
+    def __init__(self, session_id: str, *, store: DeviceStore | None = None):
+        self.session_id = session_id
+        self.store = store if store is not None else default_store()
+        self.sid = self.store.new_session()
+        self._marks: dict[int, set[str]] = {}
+        self._rows: list[int] = []  # local ordinal -> global row
+
+    # -- record -------------------------------------------------------------------
+    def lpm_insert(self, tokens: Sequence[TokenId], origins: Sequence[SpanOrigin], versions: Sequence[ModelVersion],
+                   completion_id: str | None = None) -> InsertResult:
+        """Insert one recorded sequence, merging with stored content by LPM (trie.py:120-179)."""
+        if len(tokens) == 0:
+            raise ValueError("cannot insert an empty sequence")
+        if not (len(tokens) == len(origins) == len(versions)):
+            raise ValueError("tokens, origins, versions must be parallel")
+        runs = runs_from_per_token(_origins_to_codes(origins), np.asarray(versions, np.int64))
+        return self.insert_runs(tokens, runs, completion_id)
+
+    def insert_runs(self, tokens, runs, completion_id: str | None = None) -> InsertResult:
+        """lpm_insert with metadata already as (starts, origins 0/1, versions) runs."""
+        r = self.store.record([self.sid], [tokens], [runs])
+        return self._absorb(r, 0, completion_id)
+
+    def _absorb(self, r, k: int, completion_id):
+        local = int(r.local[k])
+        if local == len(self._rows):
+            self._rows.append(int(r.row[k]))
+        if completion_id is not None:
+            self._marks.setdefault(local, set()).add(completion_id)
+        return InsertResult(int(r.matched[k]), local, int(r.added[k]))
+
+    def mark(self, node_id: int, completion_id: str) -> None:
+        self._global(node_id)
+        self._marks.setdefault(node_id, set()).add(completion_id)
+
+    # -- accounting -----------------------------------------------------------------
+    def stats(self) -> StorageStats:
+        stored, naive, _ = self.store.session_stats(self.sid)
+        return StorageStats(stored, naive)
+
+    @property
+    def total_stored_tokens(self) -> int:
+        return self.store.session_stats(self.sid)[0]
+
+    @property
+    def total_naive_tokens(self) -> int:
+        return self.store.session_stats(self.sid)[1]
+
+    # -- reconstruction ----------------------------------------------------------------
+    def _global(self, node_id: int) -> int:
+        if not (0 <= node_id < len(self._rows)):
+            raise KeyError(f"node {node_id} not in trie")
+        return self._rows[node_id]
+
+    def row_of(self, node_id: int) -> int:
+        """Global store row of a node id."""
+        return self._global(node_id)
+
+    def path_trajectory(self, node_id: int) -> Trajectory:
+        """Rebuild the trajectory for the root->node path (trie.py:203-208)."""
+        p = self.store.export([self._global(node_id)])
+        return Trajectory.from_packed(self.session_id, p.tokens, p.loss_mask, p.versions)
+
+    def lex_node_ids(self) -> list[int]:
+        """All node ids of the session in lexicographic sequence order."""
+        base = {g: k for k, g in enumerate(self._rows)}
+        return [base[int(g)] for g in self.store.session_rows(self.sid, "lex")]
+
+    def marked_nodes(self) -> list[int]:
+        return [k for k in self.lex_node_ids() if self._marks.get(k)]
+
+    def extract(self) -> list[tuple[int, Trajectory]]:
+        """One trajectory per marked node, in lexicographic order (trie.py:210-216)."""
+        ids = self.marked_nodes()
+        if not ids:
+            return []
+        p = self.store.export([self._rows[k] for k in ids])
+        out = []
+        for i, k in enumerate(ids):
+            a, b = p.offsets[i], p.offsets[i + 1]
+            out.append((k, Trajectory.from_packed(self.session_id, p.tokens[a:b], p.loss_mask[a:b], p.versions[a:b])))
+        return out
+
+    # -- radix view (debug / API fidelity) ----------------------------------------------
+    def _materialise(self):
+        """Build the reference-shaped radix tree from the rows (insertion order)."""
+        root = TrieNode(node_id=-1, tokens=[], runs=[])
+        nodes = {root.node_id: root}
+        if not self._rows:
+            return root, nodes
+        p = self.store.export(self._rows)
+        next_interior = [-2]
+
+        def new_interior(tokens, runs):
+            n = TrieNode(node_id=next_interior[0], tokens=tokens, runs=runs)
+            next_interior[0] -= 1
+            nodes[n.node_id] = n
+            return n
+
+        def runs_of(a, b):
+            mk, vs = p.loss_mask[a:b], p.versions[a:b]
+            out = []
+            for m, v in zip(mk.tolist(), vs.tolist()):
+                o = SpanOrigin.MODEL_OUTPUT if m else SpanOrigin.AGENT_INPUT
+                if out and out[-1][1] is o and out[-1][2] == v:
+                    out[-1] = (out[-1][0] + 1, o, v)
+                else:
+                    out.append((1, o, v))
+            return out
+
+        for local, _ in enumerate(self._rows):
+            a, b = int(p.offsets[local]), int(p.offsets[local + 1])
+            toks = p.tokens[a:b].tolist()
+            node, i = root, 0
+            while True:
+                if i == len(toks):
+                    end = node
+                    break
+                child = node.children.get(toks[i])
+                if child is None:
+                    end = TrieNode(node_id=local, tokens=toks[i:], runs=runs_of(a + i, b))
+                    nodes[local] = end
+                    node.children[toks[i]] = end
+                    break
+                c = 0
+                lim = min(len(child.tokens), len(toks) - i)
+                while c < lim and child.tokens[c] == toks[i + c]:
+                    c += 1
+                if c == len(child.tokens):
+                    node, i = child, i + c
+                    continue
+                head_runs, tail_runs, seen = [], [], 0
+                for ln, o, v in child.runs:
+                    if seen + ln <= c:
+                        head_runs.append((ln, o, v))
+                    elif seen >= c:
+                        tail_runs.append((ln, o, v))
+                    else:
+                        head_runs.append((c - seen, o, v))
+                        tail_runs.append((ln - (c - seen), o, v))
+                    seen += ln
+                head = new_interior(child.tokens[:c], head_runs)
+                node.children[head.tokens[0]] = head
+                child.tokens, child.runs = child.tokens[c:], tail_runs
+                head.children = {child.tokens[0]: child}
+                i += c
+                if i == len(toks):
+                    end = head
+                    break
+                end = TrieNode(node_id=local, tokens=toks[i:], runs=runs_of(a + i, b))
+                nodes[local] = end
+                head.children[toks[i]] = end
+                break
+            if end.node_id != local:  # the sequence ends on an interior node: it becomes the row's node
+                del nodes[end.node_id]
+                end.node_id = local
+                nodes[local] = end
+            end.leaf_marks = set(self._marks.get(local, set()))
+        return root, nodes
+
+    @property
+    def root(self) -> TrieNode:
+        return self._materialise()[0]
+
+    @property
+    def nodes(self) -> dict[int, TrieNode]:
+        return self._materialise()[1]
+
+    def check_well_formed(self) -> list[str]:
+        """Structural invariants of the materialised view + store accounting (trie.py:228-255)."""
+        root, _ = self._materialise()
+        problems: list[str] = []
+        seen = 0
+        stack = [root]
+        while stack:
+            node = stack.pop()
+            if node is not root:
+                if not node.tokens:
+                    problems.append(f"node {node.node_id} has empty span")
+                seen += len(node.tokens)
+                if sum(r[0] for r in node.runs) != len(node.tokens):
+                    problems.append(f"node {node.node_id} runs do not cover its tokens")
+            for key, child in node.children.items():
+                if not child.tokens or child.tokens[0] != key:
+                    problems.append(f"child of node {node.node_id} keyed {key} but starts with {child.tokens[:1]}")
+                stack.append(child)
+        st = self.stats()
+        if seen != st.stored_tokens:
+            problems.append(f"stored-token accounting off: counted {seen}, recorded {st.stored_tokens}")
+        if st.stored_tokens > st.naive_tokens:
+            problems.append("stored exceeds naive total")
+        return problems

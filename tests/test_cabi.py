@@ -1,0 +1,62 @@
+"""CPU-side checks of the C ABI boundary: the shared library loads and exports every
+symbol include/tmstore.h declares (no compute calls — there is no GPU here)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tmstore.h")
+LIB = os.path.join(ROOT, "paper_2508_11553_b200", "libtmstore.so")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tm_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+
+        __graft_entry__.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_header_declares_expected_api():
+    syms = declared_symbols()
+    for s in ["tm_store_create", "tm_record_batch", "tm_match_batch", "tm_export_rows", "tm_session_stats",
+              "tm_session_rows", "tm_last_error"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert missing == []
+
+
+def test_python_binding_covers_header():
+    from paper_2508_11553_b200._lib import SIGNATURES
+
+    assert sorted(SIGNATURES) == declared_symbols()
+
+
+def test_version_string(lib):
+    lib.tm_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.tm_version()
+
+
+def test_store_create_fails_loudly_without_gpu(lib):
+    """No CPU fallback: creating a store with no usable GPU returns an error code."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    rc = lib.tm_store_create(None, ctypes.byref(h))
+    assert rc != 0
+    lib.tm_last_error.restype = ctypes.c_char_p
+    assert lib.tm_last_error()

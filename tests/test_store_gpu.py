@@ -1,0 +1,189 @@
+"""GPU parity: the B200 store against the reference golden vectors and the C oracle.
+
+Everything here calls through the C ABI (libtmstore.so) on cuda:0.  Integer work, so
+the bar is bit-exact: matched length, row (node id), chosen parent row, added tokens,
+storage stats, export order and every token / loss-mask / version value.
+"""
+
+import numpy as np
+import pytest
+
+from oracle.cport import CRadixStore
+from workloads import pack_records
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def store():
+    from paper_2508_11553_b200 import DeviceStore
+
+    s = DeviceStore(0)
+    yield s
+    s.close()
+
+
+def _origins(codes):
+    from paper_2508_11553_b200 import SpanOrigin
+
+    return [SpanOrigin.MODEL_OUTPUT if c else SpanOrigin.AGENT_INPUT for c in codes]
+
+
+def test_golden_cases_through_session_trie(store, trie_cases):
+    """Every golden stream through the drop-in SessionTrie, insert by insert."""
+    from paper_2508_11553_b200 import SessionTrie, trajectory_to_line
+
+    for case in trie_cases:
+        trie = SessionTrie(case["session_id"], store=store)
+        for ins, exp in zip(case["inserts"], case["results"]):
+            r = trie.lpm_insert(ins["tokens"], _origins(ins["origins"]), ins["versions"], ins["completion_id"])
+            assert (r.matched_prefix_length, r.node_id, r.added_tokens) == (exp["matched"], exp["row"], exp["added"]), case["name"]
+            st = trie.stats()
+            assert (st.stored_tokens, st.naive_tokens) == (exp["stored"], exp["naive"]), case["name"]
+        assert trie.stats().dedup_ratio == case["dedup_ratio"]
+        ext = trie.extract()
+        assert [k for k, _ in ext] == [e["row"] for e in case["extract"]], case["name"]
+        for (_, t), e in zip(ext, case["extract"]):
+            assert trajectory_to_line(t) == e["line"]
+        for row, p in case["paths"].items():
+            t = trie.path_trajectory(int(row))
+            assert t.tokens == p["tokens"]
+            assert [int(m) for m in t.loss_mask] == p["loss_mask"] and t.version_tags == p["versions"]
+        assert trie.check_well_formed() == []
+
+
+def test_golden_cases_as_one_batch(store, trie_cases):
+    """All golden streams in ONE record batch (sequential semantics across waves),
+    including the parent rows the reference does not report."""
+    sids, seqs, origins, versions = [], [], [], []
+    base = [store.new_session() for _ in trie_cases]
+    for s, case in zip(base, trie_cases):
+        for ins in case["inserts"]:
+            sids.append(s)
+            seqs.append(ins["tokens"])
+            origins.append(ins["origins"])
+            versions.append(ins["versions"])
+    sid_a, tok, off, roff, rs, ro, rv = pack_records(sids, seqs, origins, versions)
+    res = store.record_packed(sid_a, tok, off[:-1], np.diff(off), roff, rs, ro, rv)
+    k = 0
+    for s, case in zip(base, trie_cases):
+        for exp in case["results"]:
+            assert (res.matched[k], res.local[k], res.parent_local[k], res.added[k]) == (
+                exp["matched"], exp["row"], exp["parent"], exp["added"]), case["name"]
+            k += 1
+        stored, naive, _ = store.session_stats(s)
+        assert (stored, naive) == (case["stored"], case["naive"])
+
+
+def _random_sessions(rng, n_sess, n_ins, vocab, max_new):
+    sids, seqs, origins, versions = [], [], [], []
+    ctx = {s: [[]] for s in range(n_sess)}
+    for _ in range(n_ins):
+        s = int(rng.integers(n_sess))
+        base = ctx[s][int(rng.integers(len(ctx[s])))]
+        r = rng.random()
+        if r < 0.1 and len(base) > 1:
+            seq = base[: int(rng.integers(1, len(base)))]          # strict prefix
+        elif r < 0.2 and len(base) > 0:
+            seq = list(base)                                        # duplicate
+        elif r < 0.35 and len(base) > 2:                            # branch inside
+            cut = int(rng.integers(1, len(base)))
+            seq = base[:cut] + rng.integers(0, vocab, int(rng.integers(1, max_new))).tolist()
+        else:
+            seq = base + rng.integers(0, vocab, int(rng.integers(1, max_new))).tolist()
+        org = (rng.random(len(seq)) < 0.5).astype(int).tolist()
+        ver = np.sort(rng.integers(0, 3, len(seq))).tolist()
+        sids.append(s)
+        seqs.append(seq)
+        origins.append(org)
+        versions.append(ver)
+        ctx[s].append(seq)
+    return sids, seqs, origins, versions
+
+
+@pytest.mark.parametrize("vocab,max_new,n_sess,n_ins", [(4, 12, 30, 600), (151936, 700, 50, 800), (3, 200, 5, 300)])
+def test_random_batches_vs_c_oracle(store, vocab, max_new, n_sess, n_ins):
+    rng = np.random.default_rng(vocab * 7 + n_ins)
+    sids, seqs, origins, versions = _random_sessions(rng, n_sess, n_ins, vocab, max_new)
+    ora = CRadixStore()
+    rec = pack_records(sids, seqs, origins, versions)
+    om, orow, opar, oadd = ora.insert_batch(*rec, nthreads=2)
+    gsid = [store.new_session() for _ in range(n_sess)]
+    g_sids = np.array([gsid[s] for s in sids], np.int32)
+    # split into 3 record calls to exercise cross-call state
+    cuts = [0, n_ins // 3, 2 * n_ins // 3, n_ins]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sub = pack_records(g_sids[a:b], seqs[a:b], origins[a:b], versions[a:b])
+        r = store.record_packed(sub[0], sub[1], sub[2][:-1], np.diff(sub[2]), *sub[3:])
+        assert np.array_equal(r.matched, om[a:b])
+        assert np.array_equal(r.local, orow[a:b])
+        assert np.array_equal(r.parent_local, opar[a:b])
+        assert np.array_equal(r.added, oadd[a:b])
+    for s in range(n_sess):
+        stored, naive, nrows = store.session_stats(gsid[s])
+        assert (stored, naive, nrows) == ora.stats(s)
+        lex_local = [store.row_info(int(g))["local"] for g in store.session_rows(gsid[s], "lex")]
+        assert lex_local == ora.lex_rows(s).tolist()
+        rows = store.session_rows(gsid[s], "insert")
+        p = store.export(rows)
+        for k in range(nrows):
+            t, m, v = ora.export_row(s, k)
+            a, b = p.offsets[k], p.offsets[k + 1]
+            assert np.array_equal(p.tokens[a:b], t)
+            assert np.array_equal(p.loss_mask[a:b], m)
+            assert np.array_equal(p.versions[a:b], v)
+            zeros = np.flatnonzero(m == 0)
+            assert p.resp_start[k] == (zeros[-1] + 1 if len(zeros) else 0)
+    # read-only matches of fresh queries (host path)
+    q = _random_sessions(rng, n_sess, 300, vocab, max_new)
+    qsid = np.array([gsid[s] for s in q[0]], np.int32)
+    qp = pack_records(q[0], q[1], q[2], q[3])
+    m_o, p_o, d_o = ora.match_batch(qp[0], qp[1], qp[2])
+    qg = pack_records(qsid, q[1], q[2], q[3])
+    m_g, p_g, d_g = store.match(qg[0], qg[1], qg[2][:-1], np.diff(qg[2]))
+    assert np.array_equal(m_g, m_o)
+    par_local = np.array([store.row_info(int(x))["local"] if x >= 0 else -1 for x in p_g])
+    assert np.array_equal(par_local, p_o)
+    dup_local = np.array([store.row_info(int(x))["local"] if x >= 0 else -1 for x in d_g])
+    assert np.array_equal(dup_local, d_o)
+
+
+def test_device_match_path_and_alignment(store):
+    """TM_MEM_DEVICE match on torch tensors equals the host-path result."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    sid = store.new_session()
+    hist = rng.integers(0, 151936, 5000).tolist()
+    store.record([sid], [hist], [(np.array([0]), np.array([1], np.uint8), np.array([0]))])
+    queries = [hist + [1, 2, 3], hist[:1234] + [int(hist[1234]) + 1], hist[:77], hist, [int(hist[0]) + 1]]
+    qp = pack_records([sid] * len(queries), queries, [[0] * len(x) for x in queries], [[0] * len(x) for x in queries], align=32)
+    m_h, p_h, d_h = store.match(qp[0], qp[1], qp[2][:-1], np.array([len(x) for x in queries]))
+    dev = torch.device("cuda", 0)
+    t_sid = torch.from_numpy(qp[0]).to(dev)
+    t_tok = torch.from_numpy(qp[1]).to(dev)
+    t_off = torch.from_numpy(qp[2][:-1].copy()).to(dev)
+    t_len = torch.tensor([len(x) for x in queries], dtype=torch.int64, device=dev)
+    om = torch.empty(len(queries), dtype=torch.int64, device=dev)
+    op = torch.empty_like(om)
+    od = torch.empty_like(om)
+    store.match_device(t_sid, t_tok, t_off, t_len, om, op, od)
+    torch.cuda.synchronize()
+    assert om.cpu().tolist() == m_h.tolist() == [5000, 1234, 77, 5000, 0]
+    assert op.cpu().tolist() == p_h.tolist()
+    assert od.cpu().tolist() == d_h.tolist()
+    assert d_h[3] >= 0 and d_h[0] == -1
+
+
+def test_errors_map_to_reference_exceptions(store):
+    from paper_2508_11553_b200 import SessionTrie
+
+    trie = SessionTrie("err", store=store)
+    with pytest.raises(ValueError):
+        trie.lpm_insert([], [], [])
+    with pytest.raises(ValueError):
+        trie.lpm_insert([1, 2], [], [0, 0])
+    with pytest.raises(KeyError):
+        trie.path_trajectory(5)
+    with pytest.raises(KeyError):
+        store.session_stats(10**6)
