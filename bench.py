@@ -1,0 +1,307 @@
+"""Benchmark: prefix-match queries/s and tokens compared/s (HBM GB/s vs peak) on B200.
+
+Workload (BASELINE.json configs[3]): per GPU, 10,000 sessions
+each holding one 32,768-token history (8 turns of input/output metadata runs), and
+batches of 4,096 read-only longest-prefix-match queries — 75% full history + 256 new
+tokens, 25% branches at a uniform depth with a forced mismatch.  One step = one
+batch through the K1 match kernel.
+
+  value      queries/s with queries resident in HBM (device-timed, CUDA events on the
+             launching stream, max over ranks)
+  e2e        the same through the C-ABI host-buffer call (pinned H2D of the query
+             tokens + D2H of the results inside the timed region)
+  roofline   K1 algorithmic bytes (8 B per compared token, c_q = min(m+1,|q|,|parent|))
+             / K1 device time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C restatement of the reference radix tree (oracle/, "port"),
+             timed on this box's host cores over the same batch
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling — every rank owns its own
+session shard and matches its own batch; no collective on the data path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefix-match queries/s (c4: 10k sessions x 32k-token histories, 4096-query batches)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--sessions", type=int, default=10_000)
+    ap.add_argument("--hist", type=int, default=32_768)
+    ap.add_argument("--queries", type=int, default=4096)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            time.sleep(0.15)
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=5)
+            self.rows = [r.split(", ") for r in out.strip().splitlines() if r.strip()]
+        else:
+            self.rows = []
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for n, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from workloads import MatchWorkload
+
+    wl = MatchWorkload(args.sessions, args.hist, args.queries)
+    cores = os.cpu_count() or 1
+    times = []
+    cpu_port_bench_reuse(wl, cores)  # warm: build the C store + one pass
+    for _ in range(max(1, args.steps)):
+        _, dt, _ = cpu_port_bench_reuse(wl, cores)
+        times.append(dt)
+    total = sum(times)
+    v = wl.n_queries * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "c4", "sessions": args.sessions, "history_tokens": args.hist, "batch_queries": args.queries},
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                         "sample": f"full c4 batch ({wl.n_queries} queries) per step, C radix-tree restatement (oracle/radix_oracle.c), {cores} threads"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+_cpu_store = {}
+
+
+def cpu_port_bench_reuse(wl, nthreads):
+    from oracle.cport import CRadixStore
+
+    st = _cpu_store.get("st")
+    if st is None:
+        st = CRadixStore()
+        ns = wl.n_sessions
+        toks = np.concatenate([wl.hist_tokens[wl.hist_off[s]: wl.hist_off[s] + wl.hist_len[s]] for s in range(ns)])
+        off = np.zeros(ns + 1, np.int64)
+        np.cumsum(wl.hist_len, out=off[1:])
+        st.insert_batch(np.arange(ns, dtype=np.int32), toks, off, wl.run_off, wl.run_start, wl.run_origin,
+                        wl.run_version, nthreads=nthreads)
+        n = wl.n_queries
+        qt = np.concatenate([wl.q_tokens[wl.q_off[i]: wl.q_off[i] + wl.q_len[i]] for i in range(n)])
+        qo = np.zeros(n + 1, np.int64)
+        np.cumsum(wl.q_len, out=qo[1:])
+        _cpu_store.update(st=st, qt=qt, qo=qo)
+    t0 = time.perf_counter()
+    res = st.match_batch(wl.q_sess, _cpu_store["qt"], _cpu_store["qo"], nthreads=nthreads)
+    return wl.n_queries, time.perf_counter() - t0, res
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2508_11553_b200 import DeviceStore
+    from workloads import SEED0, MatchWorkload
+
+    wl = MatchWorkload(args.sessions, args.hist, args.queries, seed=SEED0 + 4 + 1000 * rank)
+    store = DeviceStore(local, arena_words=int(wl.hist_off[-1]) + (1 << 20), row_capacity=args.sessions + 64,
+                        run_capacity=len(wl.run_start) + 64, session_capacity=args.sessions + 16)
+    sids = [store.new_session() for _ in range(args.sessions)]
+    assert sids[0] == 0 and sids[-1] == args.sessions - 1
+    rec = store.record_packed(np.arange(args.sessions, dtype=np.int32), wl.hist_tokens, wl.hist_off[:-1].copy(),
+                              wl.hist_len, wl.run_off, wl.run_start, wl.run_origin, wl.run_version)
+    assert np.all(rec.matched == 0) and np.all(rec.added == wl.hist_len)
+    row_len = wl.hist_len  # row id == session id here (one row per session, recorded in order)
+
+    # device-resident batch
+    t_sid = torch.from_numpy(wl.q_sess).to(dev)
+    t_tok = torch.from_numpy(wl.q_tokens).to(dev)
+    t_off = torch.from_numpy(wl.q_off[:-1].copy()).to(dev)
+    t_len = torch.from_numpy(wl.q_len).to(dev)
+    om = torch.empty(wl.n_queries, dtype=torch.int64, device=dev)
+    op = torch.empty_like(om)
+    od = torch.empty_like(om)
+    stream = torch.cuda.Stream(dev)  # one explicit stream: kernels and timing events share it
+    torch.cuda.set_stream(stream)
+
+    def step():
+        store.match_device(t_sid, t_tok, t_off, t_len, om, op, od, stream=stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # correctness of the benchmarked batch (size-independent properties)
+    m = om.cpu().numpy()
+    par = op.cpu().numpy()
+    assert np.array_equal(m, wl.q_depth), "matched length != constructed depth"
+    assert np.all((par == wl.q_sess) | (m == 0)), "parent row != query session's row"
+    plen = np.where(par >= 0, row_len[np.maximum(par, 0)], 0)
+    cq = wl.compared_tokens(m, plen)
+    alg_bytes = 8.0 * float(cq.sum())
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    store.profile_begin()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        time.sleep(0.3)  # let the sampler start before the timed region
+        t_wall = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        walk_ms, walk_n = store.profile_end("walk")
+        # short regions: keep the identical load running so the sampler sees >= 1 s of it
+        while time.perf_counter() - t_wall < 1.0:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = world * wl.n_queries * args.steps / elapsed
+    toks_per_s = world * float(cq.sum()) * args.steps / elapsed
+
+    # e2e: the public host-buffer API, pinned inputs, copies inside the timed region
+    pin_tok = torch.from_numpy(wl.q_tokens).pin_memory()
+    pin_np = pin_tok.numpy()
+    q_off = wl.q_off[:-1].copy()
+    store.match(wl.q_sess, pin_np, q_off, wl.q_len)  # warm
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        mh, ph, dh = store.match(wl.q_sess, pin_np, q_off, wl.q_len)
+    e2e_elapsed = time.perf_counter() - t0
+    assert np.array_equal(mh, wl.q_depth)
+    if world > 1:
+        t = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_elapsed = float(t.item())
+    e2e_value = world * wl.n_queries * args.e2e_steps / e2e_elapsed
+    h2d = int(wl.q_off[-2] + wl.q_len[-1]) * 4 + wl.n_queries * (4 + 8 + 8)
+    d2h = wl.n_queries * 24
+
+    peak, peak_kind = peaks()
+    k_avg = walk_ms / max(walk_n, 1) / 1e3
+    achieved = alg_bytes / k_avg / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "c4", "sessions": args.sessions, "history_tokens": args.hist,
+                   "batch_queries": args.queries, "ext_frac": 0.75, "parallelism": f"session-shard x{world}",
+                   "l2": "inputs larger than L2 (arena %.2f GB + queries %.2f GB per rank)" % (
+                       wl.hist_off[-1] * 4 / 1e9, wl.q_off[-1] * 4 / 1e9)},
+        "tokens_compared_per_s": toks_per_s,
+        "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
+        "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0,
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": None},
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps * 2,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        n, dt, res = cpu_port_bench_reuse(wl, cores)
+        n, dt2, res = cpu_port_bench_reuse(wl, cores)
+        dt = min(dt, dt2)
+        assert np.array_equal(res[0], m), "CPU port disagrees with the GPU"
+        line["cpu_baseline"] = {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+                                "sample": f"full c4 batch ({n} queries), best of 2, C radix-tree restatement "
+                                          f"(oracle/radix_oracle.c), {cores} threads"}
+    if rank == 0:
+        print(json.dumps(line))
+    store.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

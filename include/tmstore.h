@@ -136,6 +136,13 @@ int tm_store_stats(tm_store *store, int64_t *rows, int64_t *arena_used, int64_t 
 /* The store's CUDA stream (cudaStream_t) for callers that want to order work after it. */
 int tm_store_stream(tm_store *store, void **out_stream);
 
+/* Per-kernel CUDA-event timing for benchmarks.  tm_profile_begin starts recording an
+ * event pair around every launch; tm_profile_end(kind) waits for them and returns the
+ * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */
+enum { TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3 };
+int tm_profile_begin(tm_store *store);
+int tm_profile_end(tm_store *store, int32_t kind, double *total_ms, int64_t *launches);
+
 /* Block until all work queued on the store's stream is done. */
 int tm_synchronize(tm_store *store);
 

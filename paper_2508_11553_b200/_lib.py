@@ -41,6 +41,8 @@ SIGNATURES = {
     "tm_store_stats": (C.c_int, [_P, _P, _P, _P, _P]),
     "tm_store_stream": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
+    "tm_profile_begin": (C.c_int, [_P]),
+    "tm_profile_end": (C.c_int, [_P, _I32, _P, _P]),
 }
 
 

@@ -9,6 +9,9 @@
 #include "kernels.cuh"
 #include "launch.h"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace tms {
 
 // ----------------------------------------------------------------------------------
@@ -16,12 +19,14 @@ namespace tms {
 constexpr int kPlanNT = 1024;
 constexpr int kPlanNB = 2048;
 
-__global__ void __launch_bounds__(kPlanNT) k_plan_lpt(Batch b, int64_t *order) {
+__global__ void __launch_bounds__(kPlanNT) k_plan_lpt(DevView v, Batch b, int64_t *order, int64_t *root) {
   __shared__ int hist[kPlanNB];
   for (int i = threadIdx.x; i < kPlanNB; i += kPlanNT) hist[i] = 0;
   __syncthreads();
   for (int64_t w = threadIdx.x; w < b.n; w += kPlanNT) {
     int64_t L = b.len[w];
+    // resolve the root row here so the walk starts streaming immediately
+    root[w] = L > 0 ? ht_find(v, kRootTag | (uint64_t)(uint32_t)b.sids[w], dt_key(0, b.tok[b.off[w]], false)) : -1;
     int bk = (int)(L >> 8 < kPlanNB - 1 ? L >> 8 : kPlanNB - 1);
     atomicAdd(&hist[kPlanNB - 1 - bk], 1);  // descending length
   }
@@ -60,7 +65,8 @@ __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
     const int32_t sid = b.sids[w];
     if (threadIdx.x == 0) {
       int64_t r = -1;
-      if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+      if (b.root) r = b.root[w];
+      else if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
       if (r < 0) {  // nothing shares the first token: matched 0
         b.o_m[w] = 0;
         b.o_parent[w] = -1;
@@ -334,22 +340,45 @@ __global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t val) {
 constexpr int kWalkNT = 256;
 constexpr int kWalkU = 4;
 
-cudaError_t launch_plan_lpt(const Batch &b, int64_t *order, cudaStream_t s) {
-  k_plan_lpt<<<1, kPlanNT, 0, s>>>(b, order);
+cudaError_t launch_plan_lpt(const DevView &v, const Batch &b, int64_t *order, int64_t *root, cudaStream_t s) {
+  k_plan_lpt<<<1, kPlanNT, 0, s>>>(v, b, order, root);
   return cudaGetLastError();
 }
 
-cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+template <int NT, int U>
+static cudaError_t walk_variant(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<kWalkNT, kWalkU>, kWalkNT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<NT, U>, NT, 0);
     if (occ < 1) occ = 1;
   }
   int64_t grid = (int64_t)num_sms * occ;
   if (grid > b.n) grid = b.n;
   if (grid < 1) grid = 1;
-  k_walk<kWalkNT, kWalkU><<<(int)grid, kWalkNT, 0, s>>>(v, b);
+  k_walk<NT, U><<<(int)grid, NT, 0, s>>>(v, b);
   return cudaGetLastError();
+}
+
+// TM_WALK_VARIANT (tuning only): "256x4" (default), "256x2", "512x2", "128x4", "512x1"
+cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+  static int variant = -1;
+  if (variant < 0) {
+    const char *e = getenv("TM_WALK_VARIANT");
+    variant = 0;
+    if (e) {
+      if (!strcmp(e, "256x2")) variant = 1;
+      else if (!strcmp(e, "512x2")) variant = 2;
+      else if (!strcmp(e, "128x4")) variant = 3;
+      else if (!strcmp(e, "512x1")) variant = 4;
+    }
+  }
+  switch (variant) {
+    case 1: return walk_variant<256, 2>(v, b, num_sms, s);
+    case 2: return walk_variant<512, 2>(v, b, num_sms, s);
+    case 3: return walk_variant<128, 4>(v, b, num_sms, s);
+    case 4: return walk_variant<512, 1>(v, b, num_sms, s);
+    default: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
+  }
 }
 
 cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {

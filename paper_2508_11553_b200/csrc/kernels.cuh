@@ -49,6 +49,7 @@ struct Batch {
   const int64_t *off;
   const int64_t *len;
   const int64_t *order;   // optional processing order (longest first)
+  const int64_t *root;    // optional pre-resolved root row per entry (-1: none)
   unsigned long long *work;  // work counter (zeroed before launch)
   // walk outputs
   int64_t *o_m;

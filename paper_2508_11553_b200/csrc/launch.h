@@ -19,7 +19,7 @@ struct ExportArgsHost {
   int64_t *resp;
 };
 
-cudaError_t launch_plan_lpt(const Batch &b, int64_t *order, cudaStream_t s);
+cudaError_t launch_plan_lpt(const DevView &v, const Batch &b, int64_t *order, int64_t *root, cudaStream_t s);
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &e, int num_sms, cudaStream_t s);

@@ -118,6 +118,10 @@ struct tm_store {
   int64_t max_depth = 0;
   DevBytes scratch, dtok;
   PinBytes pin, ptok;
+  // optional per-kernel CUDA-event timing (tm_profile_*): pairs recorded around launches
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
+  size_t ev_used[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -205,6 +209,29 @@ void ensure_table(tm_store *s, int64_t entries) {
   cudaFree(ov);
 }
 
+// Bracket a launch with events when profiling (kind: 0 walk, 1 commit, 2 export, 3 plan).
+struct ProfScope {
+  tm_store *s;
+  int kind;
+  cudaStream_t st;
+  ProfScope(tm_store *s_, int k, cudaStream_t st_) : s(s_), kind(k), st(st_) {
+    if (!s->profile) return;
+    auto &v = s->ev[kind];
+    if (s->ev_used[kind] == v.size()) {
+      cudaEvent_t a, b;
+      ck(cudaEventCreate(&a), "event");
+      ck(cudaEventCreate(&b), "event");
+      v.push_back({a, b});
+    }
+    ck(cudaEventRecord(v[s->ev_used[kind]].first, st), "event");
+  }
+  ~ProfScope() {
+    if (!s->profile) return;
+    cudaEventRecord(s->ev[kind][s->ev_used[kind]].second, st);
+    s->ev_used[kind]++;
+  }
+};
+
 void wait_prev(tm_store *s, cudaStream_t st) {
   ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
 }
@@ -236,6 +263,21 @@ int guarded(tm_store *s, F &&f) {
 void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off, const int64_t *tok_len,
                   std::vector<int64_t> &doff, const std::vector<int64_t> *perm) {
   doff.resize(n);
+  // Fast path: every sequence already starts on a 128-byte boundary -> one direct
+  // H2D copy of the caller's buffer (pinned buffers go at full PCIe rate).  Padding
+  // words after a sequence are never compared (positions >= len are masked).
+  bool aligned = true;
+  int64_t end = 0;
+  for (int64_t k = 0; k < n; k++) {
+    aligned &= (tok_off[k] % tms::kAlignWords) == 0 && tok_off[k] >= 0;
+    end = std::max<int64_t>(end, tok_off[k] + tok_len[k]);
+  }
+  if (aligned) {
+    for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm ? (*perm)[k] : k];
+    void *d = s->dtok.need(sizeof(int32_t) * (size_t)(round_up(std::max<int64_t>(end, 1), tms::kAlignWords) + tms::kAlignWords));
+    if (end > 0) ck(cudaMemcpyAsync(d, tokens, sizeof(int32_t) * end, cudaMemcpyHostToDevice, s->stream), "H2D tokens");
+    return;
+  }
   int64_t total = 0;
   for (int64_t k = 0; k < n; k++) {
     int64_t e = perm ? (*perm)[k] : k;
@@ -420,6 +462,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
              o_sp = lay.add(4 * n), o_crow = lay.add(8 * n), o_cloc = lay.add(4 * n);
       size_t out_end = lay.bytes;
       size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n), o_ord = lay.add(8 * n),
+             o_root = lay.add(8 * n),
              o_work = lay.add(8 * (size_t)nwaves);
       char *h = (char *)s->pin.need(lay.bytes);
       char *d = (char *)s->scratch.need(lay.bytes);
@@ -470,11 +513,20 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         b.c_local = (int32_t *)(d + o_cloc) + b0;
         if (b.n >= 512) {
           int64_t *ord = (int64_t *)(d + o_ord) + b0;
-          ck(tms::launch_plan_lpt(b, ord, s->stream), "plan");
+          ProfScope ps(s, 3, s->stream);
+          int64_t *rt = (int64_t *)(d + o_root) + b0;
+          ck(tms::launch_plan_lpt(s->v, b, ord, rt, s->stream), "plan");
           b.order = ord;
+          b.root = rt;
         }
-        ck(tms::launch_walk(s->v, b, s->num_sms, s->stream), "walk");
-        ck(tms::launch_commit(s->v, b, s->num_sms, s->stream), "commit");
+        {
+          ProfScope ps(s, 0, s->stream);
+          ck(tms::launch_walk(s->v, b, s->num_sms, s->stream), "walk");
+        }
+        {
+          ProfScope ps(s, 1, s->stream);
+          ck(tms::launch_commit(s->v, b, s->num_sms, s->stream), "commit");
+        }
       }
       // ---- results back
       char *hout = h + o_m;
@@ -528,7 +580,7 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n);
     size_t out_end = lay.bytes;
-    size_t o_ord = lay.add(8 * n), o_work = lay.add(8);
+    size_t o_ord = lay.add(8 * n), o_root = lay.add(8 * n), o_work = lay.add(8);
     char *d = (char *)s->scratch.need(lay.bytes);
     Batch b{};
     b.n = n;
@@ -567,10 +619,15 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     }
     ck(cudaMemsetAsync(b.work, 0, 8, st), "memset work");
     if (n >= 512) {
-      ck(tms::launch_plan_lpt(b, (int64_t *)(d + o_ord), st), "plan");
+      ProfScope ps(s, 3, st);
+      ck(tms::launch_plan_lpt(s->v, b, (int64_t *)(d + o_ord), (int64_t *)(d + o_root), st), "plan");
       b.order = (const int64_t *)(d + o_ord);
+      b.root = (const int64_t *)(d + o_root);
     }
-    ck(tms::launch_walk(s->v, b, s->num_sms, st), "walk");
+    {
+      ProfScope ps(s, 0, st);
+      ck(tms::launch_walk(s->v, b, s->num_sms, st), "walk");
+    }
     if (mem == TM_MEM_HOST) {
       char *h = (char *)s->pin.need(lay.bytes);
       ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, st), "D2H");
@@ -650,7 +707,10 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       e.resp = out_resp_start;
     }
     if (e.resp) ck(cudaMemsetAsync(e.resp, 0, 8 * n, st), "memset resp");
-    ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
+    {
+      ProfScope ps(s, 2, st);
+      ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
+    }
     if (mem_out == TM_MEM_HOST) {
       if (out_tokens) ck(cudaMemcpyAsync(out_tokens, e.tokens, 4 * total, cudaMemcpyDeviceToHost, st), "D2H tokens");
       if (out_mask) ck(cudaMemcpyAsync(out_mask, e.mask, total, cudaMemcpyDeviceToHost, st), "D2H mask");
@@ -732,6 +792,29 @@ int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *are
 
 int tm_store_stream(tm_store *s, void **out_stream) {
   return guarded(s, [&] { *out_stream = (void *)s->stream; });
+}
+
+int tm_profile_begin(tm_store *s) {
+  return guarded(s, [&] {
+    s->profile = true;
+    for (int k = 0; k < 4; k++) s->ev_used[k] = 0;
+  });
+}
+
+int tm_profile_end(tm_store *s, int32_t kind, double *total_ms, int64_t *launches) {
+  return guarded(s, [&] {
+    if (kind < 0 || kind > 3) fail(TM_EINVAL, "bad kernel kind");
+    double t = 0;
+    for (size_t i = 0; i < s->ev_used[kind]; i++) {
+      ck(cudaEventSynchronize(s->ev[kind][i].second), "event sync");
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, s->ev[kind][i].first, s->ev[kind][i].second), "elapsed");
+      t += ms;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = (int64_t)s->ev_used[kind];
+    s->profile = false;
+  });
 }
 
 int tm_synchronize(tm_store *s) {

@@ -119,6 +119,18 @@ class DeviceStore:
         check(self.lib.tm_store_stream(self.h, C.byref(s)))
         return s.value or 0
 
+    KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3}
+
+    def profile_begin(self):
+        """Start recording CUDA events around every kernel launch of this store."""
+        check(self.lib.tm_profile_begin(self.h))
+
+    def profile_end(self, kernel: str = "walk") -> tuple[float, int]:
+        """(summed device ms, launches) of one kernel kind since profile_begin."""
+        ms, n = C.c_double(), C.c_int64()
+        check(self.lib.tm_profile_end(self.h, self.KERNELS[kernel], C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def synchronize(self):
         check(self.lib.tm_synchronize(self.h))
 
@@ -171,6 +183,12 @@ class DeviceStore:
                                       _ptr(m), _ptr(p), _ptr(d), None))
         return m, p, d
 
+    @staticmethod
+    def _stream_arg(stream):
+        # torch reports the legacy default stream as 0; the C ABI reads NULL as "the
+        # store's own stream", so pass cudaStreamLegacy (0x1) explicitly
+        return C.c_void_p(1 if stream == 0 else stream)
+
     def match_device(self, sids, tokens, tok_off, tok_len, out_matched, out_parent, out_dup, stream=None):
         """All CUDA tensors on this store's device; tok_off multiples of 32; enqueued on
         ``stream`` (a cudaStream_t int, default: torch's current stream)."""
@@ -180,7 +198,7 @@ class DeviceStore:
             stream = torch.cuda.current_stream(self.device).cuda_stream
         check(self.lib.tm_match_batch(self.h, sids.numel(), TM_MEM_DEVICE, _tptr(sids), _tptr(tokens), _tptr(tok_off),
                                       _tptr(tok_len), _tptr(out_matched), _tptr(out_parent), _tptr(out_dup),
-                                      C.c_void_p(stream)))
+                                      self._stream_arg(stream)))
 
     # -- export (trajectory assembly) ---------------------------------------------------
     def rows_total(self, rows) -> int:
@@ -218,7 +236,7 @@ class DeviceStore:
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
         check(self.lib.tm_export_rows(self.h, n, _ptr(rows), TM_MEM_DEVICE, _ptr(off), _tptr(tok), _tptr(msk), _tptr(ver),
-                                      _tptr(resp), C.c_void_p(stream)))
+                                      _tptr(resp), self._stream_arg(stream)))
         return Packed(off, tok, msk, ver, resp)
 
 

@@ -59,3 +59,78 @@ def pack_records(sids, seqs, origins, versions, align=1):
         cat(ro, np.uint8),
         cat(rv, np.int32),
     )
+
+
+# ----------------------------------------------------------------------------- configs
+
+
+def turn_runs(hist_len: int, turns: int, in_frac: float = 0.125, bump_at: int = 5):
+    """Meta runs of an agent history: per turn an AGENT_INPUT run then a MODEL_OUTPUT
+    run; versions bumped from turn ``bump_at`` on (a policy update mid-session)."""
+    per = hist_len // turns
+    n_in = max(1, int(per * in_frac))
+    starts, origins, versions = [], [], []
+    for t in range(turns):
+        v = 0 if t < bump_at else 1
+        starts += [t * per, t * per + n_in]
+        origins += [0, 1]
+        versions += [v, v]
+    return np.asarray(starts, np.int32), np.asarray(origins, np.uint8), np.asarray(versions, np.int32)
+
+
+class MatchWorkload:
+    """Config 4 (and the per-shard slice of config 5): sessions with one stored history
+    each, and batches of read-only match queries — 75% full history + 256 new tokens
+    (matched = history length), 25% branches at d ~ U[0, len) with a forced mismatch."""
+
+    def __init__(self, n_sessions=10_000, hist_len=32_768, n_queries=4096, ext_frac=0.75, new_tokens=256,
+                 seed=SEED0 + 4, mixed=None):
+        rng = np.random.default_rng(seed)
+        self.n_sessions = n_sessions
+        if mixed is None:
+            lens = np.full(n_sessions, hist_len, np.int64)
+        else:  # log-uniform lengths in [lo, hi] (config 5)
+            lo, hi = mixed
+            lens = np.exp(rng.uniform(np.log(lo), np.log(hi), n_sessions)).astype(np.int64)
+        self.hist_len = lens
+        padded = (lens + ALIGN - 1) // ALIGN * ALIGN
+        self.hist_off = np.zeros(n_sessions + 1, np.int64)
+        np.cumsum(padded, out=self.hist_off[1:])
+        self.hist_tokens = np.zeros(int(self.hist_off[-1]), np.int32)
+        for s in range(n_sessions):  # chunked generation keeps peak memory low
+            self.hist_tokens[self.hist_off[s]: self.hist_off[s] + lens[s]] = rng.integers(0, VOCAB, int(lens[s]), dtype=np.int32)
+        runs = [turn_runs(int(L), 8) if L >= 64 else (np.array([0], np.int32), np.array([1], np.uint8), np.array([0], np.int32)) for L in lens]
+        self.run_off = np.zeros(n_sessions + 1, np.int64)
+        np.cumsum([len(r[0]) for r in runs], out=self.run_off[1:])
+        self.run_start = np.concatenate([r[0] for r in runs])
+        self.run_origin = np.concatenate([r[1] for r in runs])
+        self.run_version = np.concatenate([r[2] for r in runs])
+        # queries
+        qs = rng.integers(0, n_sessions, n_queries)
+        ext = rng.random(n_queries) < ext_frac
+        qlen = np.empty(n_queries, np.int64)
+        depth = np.empty(n_queries, np.int64)
+        for i in range(n_queries):
+            L = lens[qs[i]]
+            depth[i] = L if ext[i] else rng.integers(0, L)
+            qlen[i] = depth[i] + new_tokens
+        qpad = (qlen + ALIGN - 1) // ALIGN * ALIGN
+        self.q_off = np.zeros(n_queries + 1, np.int64)
+        np.cumsum(qpad, out=self.q_off[1:])
+        self.q_tokens = np.zeros(int(self.q_off[-1]), np.int32)
+        for i in range(n_queries):
+            s, d, o = qs[i], int(depth[i]), int(self.q_off[i])
+            h = self.hist_tokens[self.hist_off[s]: self.hist_off[s] + lens[s]]
+            self.q_tokens[o: o + d] = h[:d]
+            tail = rng.integers(0, VOCAB, new_tokens, dtype=np.int32)
+            if d < lens[s]:  # forced mismatch at d
+                tail[0] = (int(h[d]) + 1 + int(rng.integers(0, VOCAB - 1))) % VOCAB
+            self.q_tokens[o + d: o + d + new_tokens] = tail
+        self.q_sess = qs.astype(np.int32)
+        self.q_len = qlen
+        self.q_depth = depth  # expected matched length
+        self.n_queries = n_queries
+
+    def compared_tokens(self, matched, parent_len):
+        """c_q = min(m+1, |q|, |parent|) per query."""
+        return np.minimum(np.minimum(matched + 1, self.q_len), parent_len)
