@@ -234,6 +234,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
+        plan_ms, plan_n = store.profile_end("plan")
         # short regions: keep the identical load running so the sampler sees >= 1 s of it
         while time.perf_counter() - t_wall < 1.0:
             for _ in range(50):
@@ -282,7 +283,8 @@ def main():
         "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
         "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0,
-                     "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": None},
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": None,
+                     "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": args.steps * 2,
         "clocks": clk.summary(),

@@ -15,33 +15,36 @@
 namespace tms {
 
 // ----------------------------------------------------------------------------------
-// Longest-first order: bucket = min(NB-1, len >> 8), descending.  One CTA.
-constexpr int kPlanNT = 1024;
-constexpr int kPlanNB = 2048;
+// Planner (one grid-wide pass, one thread per entry): resolve each entry's root row
+// (session, first token) in the branch index, and drop the entry into one of kPlanNB
+// length buckets (longest first, 1024-token granularity).  The walk grabs items by
+// rank and maps rank -> (bucket, slot) with a 128-entry scan in shared memory, so the
+// tail of the grid is left with the shortest items (longest-processing-time order).
+constexpr int kPlanNT = 256;
+constexpr int kPlanNB = 128;
 
-__global__ void __launch_bounds__(kPlanNT) k_plan_lpt(DevView v, Batch b, int64_t *order, int64_t *root) {
-  __shared__ int hist[kPlanNB];
-  for (int i = threadIdx.x; i < kPlanNB; i += kPlanNT) hist[i] = 0;
-  __syncthreads();
-  for (int64_t w = threadIdx.x; w < b.n; w += kPlanNT) {
-    int64_t L = b.len[w];
-    // resolve the root row here so the walk starts streaming immediately
-    root[w] = L > 0 ? ht_find(v, kRootTag | (uint64_t)(uint32_t)b.sids[w], dt_key(0, b.tok[b.off[w]], false)) : -1;
-    int bk = (int)(L >> 8 < kPlanNB - 1 ? L >> 8 : kPlanNB - 1);
-    atomicAdd(&hist[kPlanNB - 1 - bk], 1);  // descending length
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive scan (2048 entries; negligible)
-    int acc = 0;
-    for (int i = 0; i < kPlanNB; i++) { int c = hist[i]; hist[i] = acc; acc += c; }
-  }
-  __syncthreads();
-  for (int64_t w = threadIdx.x; w < b.n; w += kPlanNT) {
-    int64_t L = b.len[w];
-    int bk = (int)(L >> 8 < kPlanNB - 1 ? L >> 8 : kPlanNB - 1);
-    int pos = atomicAdd(&hist[kPlanNB - 1 - bk], 1);
-    order[pos] = w;
-  }
+__device__ __forceinline__ int len_bucket(int64_t L) {
+  const int64_t k = L >> 10;
+  return kPlanNB - 1 - (int)(k < kPlanNB - 1 ? k : kPlanNB - 1);
+}
+
+__global__ void __launch_bounds__(kPlanNT) k_plan(DevView v, Batch b, int64_t *root, int *count, int *items) {
+  const int64_t w = blockIdx.x * (int64_t)kPlanNT + threadIdx.x;
+  if (w >= b.n) return;
+  const int64_t L = b.len[w];
+  root[w] = L > 0 ? ht_find(v, kRootTag | (uint64_t)(uint32_t)b.sids[w], dt_key(0, b.tok[b.off[w]], false)) : -1;
+  // warp-aggregated slot allocation: most entries of a batch share a few buckets, and
+  // per-thread atomics on one address serialise (measured 10+ us for 4096 entries)
+  const int bk = len_bucket(L);
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, bk);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&count[bk], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  items[(int64_t)bk * b.n + base + rank] = (int)w;
 }
 
 // ----------------------------------------------------------------------------------
@@ -54,12 +57,31 @@ __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
   __shared__ long long s_item;
   __shared__ long long s_row;
   __shared__ int s_lo;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = (long long)atomicAdd(b.work, 1ull);
+  __shared__ int s_base[kPlanNB + 1];
+  if (b.bucket_count) {  // exclusive scan of the planner's bucket sizes
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int i = 0; i < kPlanNB; i++) { s_base[i] = acc; acc += b.bucket_count[i]; }
+      s_base[kPlanNB] = acc;
+    }
     __syncthreads();
-    const int64_t it = s_item;
-    if (it >= b.n) return;
-    const int64_t w = b.order ? b.order[it] : it;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) {
+      long long it = (long long)atomicAdd(b.work, 1ull);
+      if (b.bucket_count && it < b.n) {
+        int lo = 0, hi = kPlanNB;  // last bucket with base <= it
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (s_base[mid] <= it) lo = mid; else hi = mid;
+        }
+        it = b.bucket_items[(int64_t)lo * b.n + (it - s_base[lo])];
+      }
+      s_item = it;
+    }
+    __syncthreads();
+    const int64_t w = s_item;
+    if (w >= b.n) return;
     const int32_t *q = b.tok + b.off[w];
     const int L = (int)b.len[w];
     const int32_t sid = b.sids[w];
@@ -337,11 +359,23 @@ __global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t val) {
 
 // ----------------------------------------------------------------------------------
 // launchers
-constexpr int kWalkNT = 256;
-constexpr int kWalkU = 4;
+constexpr int kWalkNT = 64;
+constexpr int kWalkU = 8;
 
-cudaError_t launch_plan_lpt(const DevView &v, const Batch &b, int64_t *order, int64_t *root, cudaStream_t s) {
-  k_plan_lpt<<<1, kPlanNT, 0, s>>>(v, b, order, root);
+// scratch layout (ints): [0, kPlanNB) bucket counts, [kPlanNB, kPlanNB+2) the walk's u64
+// work counter — zeroed together by one memset — then kPlanNB * n bucket slots.
+int64_t plan_scratch_ints(int64_t n) { return kPlanNB + 2 + (int64_t)kPlanNB * n; }
+unsigned long long *plan_work_counter(int *scratch) { return reinterpret_cast<unsigned long long *>(scratch + kPlanNB); }
+
+cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *scratch, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int) * (kPlanNB + 2), s);
+  if (e != cudaSuccess) return e;
+  b.bucket_count = scratch;
+  b.bucket_items = scratch + kPlanNB + 2;
+  b.work = plan_work_counter(scratch);
+  b.root = root;
+  const int grid = (int)((b.n + kPlanNT - 1) / kPlanNT);
+  k_plan<<<grid, kPlanNT, 0, s>>>(v, b, root, b.bucket_count, b.bucket_items);
   return cudaGetLastError();
 }
 
@@ -370,6 +404,10 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
       else if (!strcmp(e, "512x2")) variant = 2;
       else if (!strcmp(e, "128x4")) variant = 3;
       else if (!strcmp(e, "512x1")) variant = 4;
+      else if (!strcmp(e, "128x2")) variant = 5;
+      else if (!strcmp(e, "128x8")) variant = 6;
+      else if (!strcmp(e, "64x8")) variant = 7;
+      else if (!strcmp(e, "256x4")) variant = 8;
     }
   }
   switch (variant) {
@@ -377,6 +415,10 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
     case 2: return walk_variant<512, 2>(v, b, num_sms, s);
     case 3: return walk_variant<128, 4>(v, b, num_sms, s);
     case 4: return walk_variant<512, 1>(v, b, num_sms, s);
+    case 5: return walk_variant<128, 2>(v, b, num_sms, s);
+    case 6: return walk_variant<128, 8>(v, b, num_sms, s);
+    case 7: return walk_variant<64, 8>(v, b, num_sms, s);
+    case 8: return walk_variant<256, 4>(v, b, num_sms, s);
     default: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
   }
 }

@@ -48,8 +48,9 @@ struct Batch {
   const int32_t *tok;     // tokens; sequence w starts at tok + off[w] (multiple of 32)
   const int64_t *off;
   const int64_t *len;
-  const int64_t *order;   // optional processing order (longest first)
   const int64_t *root;    // optional pre-resolved root row per entry (-1: none)
+  int *bucket_count;      // optional planner output: entries per length bucket (longest first)
+  int *bucket_items;      //   and the entries of each bucket (stride n)
   unsigned long long *work;  // work counter (zeroed before launch)
   // walk outputs
   int64_t *o_m;

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -119,6 +120,10 @@ struct tm_store {
   DevBytes scratch, dtok;
   PinBytes pin, ptok;
   // optional per-kernel CUDA-event timing (tm_profile_*): pairs recorded around launches
+  // batches at least this large get the longest-first planner.  Off by default: on the
+  // c4 workload in-kernel root lookups are hidden by occupancy and the planner's ~10 us
+  // costs more than the tail it removes (TM_PLAN_MIN at store creation overrides).
+  int64_t plan_min = int64_t(1) << 62;
   bool profile = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
   size_t ev_used[4] = {0, 0, 0, 0};
@@ -341,6 +346,7 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
   if (cfg) c = *cfg;
   tm_store *s = new tm_store();
   s->device = c.device;
+  if (const char *e = getenv("TM_PLAN_MIN")) s->plan_min = atoll(e);
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
     ck(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, c.device), "attr");
@@ -461,8 +467,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
              o_sp = lay.add(4 * n), o_crow = lay.add(8 * n), o_cloc = lay.add(4 * n);
       size_t out_end = lay.bytes;
-      size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n), o_ord = lay.add(8 * n),
-             o_root = lay.add(8 * n),
+      size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n),
+             o_root = lay.add(8 * n), o_plan = lay.add(4 * (size_t)tms::plan_scratch_ints(n)),
              o_work = lay.add(8 * (size_t)nwaves);
       char *h = (char *)s->pin.need(lay.bytes);
       char *d = (char *)s->scratch.need(lay.bytes);
@@ -495,7 +501,6 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         b.tok = (const int32_t *)s->dtok.p;
         b.off = (const int64_t *)(d + o_off) + b0;
         b.len = (const int64_t *)(d + o_len) + b0;
-        b.order = nullptr;
         b.work = (unsigned long long *)(d + o_work) + w;
         b.o_m = (int64_t *)(d + o_m) + b0;
         b.o_parent = (int64_t *)(d + o_par) + b0;
@@ -511,13 +516,9 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         b.c_run0 = (int64_t *)(d + o_cr0) + b0;
         b.c_firstrun = (int32_t *)(d + o_cfr) + b0;
         b.c_local = (int32_t *)(d + o_cloc) + b0;
-        if (b.n >= 512) {
-          int64_t *ord = (int64_t *)(d + o_ord) + b0;
+        if (b.n >= s->plan_min) {
           ProfScope ps(s, 3, s->stream);
-          int64_t *rt = (int64_t *)(d + o_root) + b0;
-          ck(tms::launch_plan_lpt(s->v, b, ord, rt, s->stream), "plan");
-          b.order = ord;
-          b.root = rt;
+          ck(tms::launch_plan(s->v, b, (int64_t *)(d + o_root) + b0, (int *)(d + o_plan), s->stream), "plan");
         }
         {
           ProfScope ps(s, 0, s->stream);
@@ -580,7 +581,7 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n);
     size_t out_end = lay.bytes;
-    size_t o_ord = lay.add(8 * n), o_root = lay.add(8 * n), o_work = lay.add(8);
+    size_t o_root = lay.add(8 * n), o_work = lay.add(8), o_plan = lay.add(4 * (size_t)tms::plan_scratch_ints(n));
     char *d = (char *)s->scratch.need(lay.bytes);
     Batch b{};
     b.n = n;
@@ -617,12 +618,11 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     } else {
       fail(TM_EINVAL, "bad memory kind");
     }
-    ck(cudaMemsetAsync(b.work, 0, 8, st), "memset work");
-    if (n >= 512) {
+    if (n >= s->plan_min) {
       ProfScope ps(s, 3, st);
-      ck(tms::launch_plan_lpt(s->v, b, (int64_t *)(d + o_ord), (int64_t *)(d + o_root), st), "plan");
-      b.order = (const int64_t *)(d + o_ord);
-      b.root = (const int64_t *)(d + o_root);
+      ck(tms::launch_plan(s->v, b, (int64_t *)(d + o_root), (int *)(d + o_plan), st), "plan");
+    } else {
+      ck(cudaMemsetAsync(b.work, 0, 8, st), "memset work");
     }
     {
       ProfScope ps(s, 0, st);

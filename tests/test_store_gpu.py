@@ -14,11 +14,23 @@ from workloads import pack_records
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def store():
+@pytest.fixture(scope="module", params=["default", "planner"])
+def store(request):
+    """Every test runs twice: default path, and with the longest-first planner forced on."""
+    import os
+
     from paper_2508_11553_b200 import DeviceStore
 
-    s = DeviceStore(0)
+    old = os.environ.get("TM_PLAN_MIN")
+    if request.param == "planner":
+        os.environ["TM_PLAN_MIN"] = "1"
+    try:
+        s = DeviceStore(0)
+    finally:
+        if old is None:
+            os.environ.pop("TM_PLAN_MIN", None)
+        else:
+            os.environ["TM_PLAN_MIN"] = old
     yield s
     s.close()
 
