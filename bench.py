@@ -269,6 +269,14 @@ def main():
     d2h = wl.n_queries * 24
 
     peak, peak_kind = peaks()
+    traffic = None
+    try:  # DRAM bytes per k_walk launch from the committed ncu --set full capture of this workload
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get("k_walk:c4")
+        if tr and args.sessions == 10_000 and args.hist == 32_768 and args.queries == 4096:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     k_avg = walk_ms / max(walk_n, 1) / 1e3
     achieved = alg_bytes / k_avg / 1e9
     line = {
@@ -283,7 +291,7 @@ def main():
         "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
         "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0,
-                     "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": None,
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": traffic,
                      "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": args.steps * 2,
