@@ -134,3 +134,88 @@ class MatchWorkload:
     def compared_tokens(self, matched, parent_len):
         """c_q = min(m+1, |q|, |parent|) per query."""
         return np.minimum(np.minimum(matched + 1, self.q_len), parent_len)
+
+
+class RecordWorkload:
+    """Record streams for configs 1-3 as flat batches (sids, sequences, meta runs) in
+    recording order, ready for pack_records / DeviceStore.record / the C oracle.
+
+    c1: 1 session, 8 turns x (128 user + 384 output) -> 4,096 tokens; each turn's
+        input = the previous full sequence + user tokens; version bumped from turn 5.
+    c2: sessions x 16 branches: shared prefix P=6,144 (input), per-branch S=2,048
+        (512 user + 1,536 output), pairwise-distinct first suffix tokens.
+    c3: sessions x 2 turns: turn 1 = 1,024 in + 1,024 out @v0; turn 2 = turn 1 + 512
+        user @v0 (context version) + 1,536 out split at k ~ U[1, 1535]: leg 1 @v0,
+        leg 2 @v1 (a weight switch mid-turn: the partial-rollout stitch).
+    """
+
+    def __init__(self, config: int, n_sessions: int | None = None, seed: int | None = None):
+        rng = np.random.default_rng(SEED0 + config if seed is None else seed)
+        self.sids, self.seqs, self.runs = [], [], []
+        self.config = config
+        if config == 1:
+            n_sessions = n_sessions or 1
+            for s in range(n_sessions):
+                ctx = np.zeros(0, np.int32)
+                runs_s, runs_o, runs_v = [], [], []
+                for t in range(8):
+                    v = 0 if t < 5 else 1
+                    user = rng.integers(0, VOCAB, 128, dtype=np.int32)
+                    out = rng.integers(0, VOCAB, 384, dtype=np.int32)
+                    # the recorded sequence is input ++ output; input runs are re-tagged
+                    # with the current version (trajectory.py:226-230)
+                    seq = np.concatenate([ctx, user, out])
+                    n_in = len(ctx) + 128
+                    self._add(s, seq, [0, n_in], [0, 1], [v, v])
+                    ctx = seq
+        elif config == 2:
+            n_sessions = n_sessions or 1000
+            P, S, K = 6144, 2048, 16
+            for s in range(n_sessions):
+                prefix = rng.integers(0, VOCAB, P, dtype=np.int32)
+                firsts = rng.choice(VOCAB, size=K, replace=False).astype(np.int32)
+                for k in range(K):
+                    suf = rng.integers(0, VOCAB, S, dtype=np.int32)
+                    suf[0] = firsts[k]
+                    self._add(s, np.concatenate([prefix, suf]), [0, P + 512], [0, 1], [0, 0])
+        elif config == 3:
+            n_sessions = n_sessions or 4000
+            self.split = []
+            for s in range(n_sessions):
+                t1 = rng.integers(0, VOCAB, 2048, dtype=np.int32)
+                self._add(s, t1, [0, 1024], [0, 1], [0, 0])
+                user = rng.integers(0, VOCAB, 512, dtype=np.int32)
+                out = rng.integers(0, VOCAB, 1536, dtype=np.int32)
+                k = int(rng.integers(1, 1536))
+                self.split.append(k)
+                n_in = 2048 + 512
+                self._add(s, np.concatenate([t1, user, out]), [0, n_in, n_in + k], [0, 1, 1], [0, 0, 1])
+        else:
+            raise ValueError(config)
+        self.n_sessions = n_sessions
+
+    def _add(self, s, seq, starts, origins, versions):
+        self.sids.append(s)
+        self.seqs.append(np.asarray(seq, np.int32))
+        self.runs.append((np.asarray(starts, np.int32), np.asarray(origins, np.uint8), np.asarray(versions, np.int32)))
+
+    def packed(self, sid_map=None):
+        """(sids, tokens, tok_off[n+1], run_off[n+1], run_start, run_origin, run_version)."""
+        sids = np.asarray(self.sids if sid_map is None else [sid_map[s] for s in self.sids], np.int32)
+        lens = np.array([len(x) for x in self.seqs], np.int64)
+        off = np.zeros(len(lens) + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        rc = np.array([len(r[0]) for r in self.runs], np.int64)
+        roff = np.zeros(len(rc) + 1, np.int64)
+        np.cumsum(rc, out=roff[1:])
+        return (sids, np.concatenate(self.seqs), off, roff, np.concatenate([r[0] for r in self.runs]),
+                np.concatenate([r[1] for r in self.runs]), np.concatenate([r[2] for r in self.runs]))
+
+    def per_token_meta(self, k):
+        """Own (mask, versions) of record k over its full length."""
+        st, org, ver = self.runs[k]
+        L = len(self.seqs[k])
+        ends = np.append(st[1:], L)
+        mask = np.repeat(org, ends - st)
+        vers = np.repeat(ver, ends - st)
+        return mask, vers
