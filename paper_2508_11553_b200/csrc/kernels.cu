@@ -21,7 +21,6 @@ namespace tms {
 // rank and maps rank -> (bucket, slot) with a 128-entry scan in shared memory, so the
 // tail of the grid is left with the shortest items (longest-processing-time order).
 constexpr int kPlanNT = 256;
-constexpr int kPlanNB = 128;
 
 __device__ __forceinline__ int len_bucket(int64_t L) {
   const int64_t k = L >> 10;
@@ -32,9 +31,9 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(DevView v, Batch b, int64_t *r
   const int64_t w = blockIdx.x * (int64_t)kPlanNT + threadIdx.x;
   if (w >= b.n) return;
   const int64_t L = b.len[w];
-  root[w] = L > 0 ? ht_find(v, kRootTag | (uint64_t)(uint32_t)b.sids[w], dt_key(0, b.tok[b.off[w]], false)) : -1;
+  if (root) root[w] = L > 0 ? ht_find(v, kRootTag | (uint64_t)(uint32_t)b.sids[w], dt_key(0, b.tok[b.off[w]], false)) : -1;
   // warp-aggregated slot allocation: most entries of a batch share a few buckets, and
-  // per-thread atomics on one address serialise (measured 10+ us for 4096 entries)
+  // per-thread atomics on one address serialise
   const int bk = len_bucket(L);
   const unsigned act = __activemask();
   const unsigned peers = __match_any_sync(act, bk);
@@ -58,18 +57,18 @@ __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
   __shared__ long long s_row;
   __shared__ int s_lo;
   __shared__ int s_base[kPlanNB + 1];
-  if (b.bucket_count) {  // exclusive scan of the planner's bucket sizes
+  if (b.bucket_items) {  // exclusive scan of the planner's bucket sizes
     if (threadIdx.x == 0) {
       int acc = 0;
-      for (int i = 0; i < kPlanNB; i++) { s_base[i] = acc; acc += b.bucket_count[i]; }
+      for (int i = 0; i < kPlanNB; i++) { s_base[i] = acc; acc += b.sched->count[i]; }
       s_base[kPlanNB] = acc;
     }
     __syncthreads();
   }
   for (;;) {
     if (threadIdx.x == 0) {
-      long long it = (long long)atomicAdd(b.work, 1ull);
-      if (b.bucket_count && it < b.n) {
+      long long it = (long long)atomicAdd(&b.sched->work, 1ull);
+      if (b.bucket_items && it < b.n) {
         int lo = 0, hi = kPlanNB;  // last bucket with base <= it
         while (hi - lo > 1) {
           int mid = (lo + hi) >> 1;
@@ -81,7 +80,20 @@ __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
     }
     __syncthreads();
     const int64_t w = s_item;
-    if (w >= b.n) return;
+    if (w >= b.n) {
+      // the last CTA out leaves the scheduler block zeroed for the next launch, so a
+      // steady stream of batches needs no memset
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&b.sched->exit, 1u) == gridDim.x - 1) {
+          for (int i = 0; i < kPlanNB; i++) b.sched->count[i] = 0;
+          b.sched->work = 0;
+          b.sched->exit = 0;
+          __threadfence();
+        }
+      }
+      return;
+    }
     const int32_t *q = b.tok + b.off[w];
     const int L = (int)b.len[w];
     const int32_t sid = b.sids[w];
@@ -362,20 +374,13 @@ __global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t val) {
 constexpr int kWalkNT = 64;
 constexpr int kWalkU = 8;
 
-// scratch layout (ints): [0, kPlanNB) bucket counts, [kPlanNB, kPlanNB+2) the walk's u64
-// work counter — zeroed together by one memset — then kPlanNB * n bucket slots.
-int64_t plan_scratch_ints(int64_t n) { return kPlanNB + 2 + (int64_t)kPlanNB * n; }
-unsigned long long *plan_work_counter(int *scratch) { return reinterpret_cast<unsigned long long *>(scratch + kPlanNB); }
+int64_t plan_items_ints(int64_t n) { return (int64_t)kPlanNB * n; }
 
-cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *scratch, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int) * (kPlanNB + 2), s);
-  if (e != cudaSuccess) return e;
-  b.bucket_count = scratch;
-  b.bucket_items = scratch + kPlanNB + 2;
-  b.work = plan_work_counter(scratch);
+cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *items, cudaStream_t s) {
+  b.bucket_items = items;
   b.root = root;
   const int grid = (int)((b.n + kPlanNT - 1) / kPlanNT);
-  k_plan<<<grid, kPlanNT, 0, s>>>(v, b, root, b.bucket_count, b.bucket_items);
+  k_plan<<<grid, kPlanNT, 0, s>>>(v, b, root, b.sched->count, items);
   return cudaGetLastError();
 }
 

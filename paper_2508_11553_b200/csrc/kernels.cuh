@@ -41,6 +41,15 @@ struct DevView {
   int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=error flags
 };
 
+// Walk scheduler block (one per store, zeroed once at creation): planner bucket counts,
+// the walk's work counter and an exit counter; the last walk CTA re-zeroes it.
+constexpr int kPlanNB = 128;
+struct Sched {
+  int count[kPlanNB];
+  unsigned long long work;
+  unsigned int exit;
+};
+
 // one batch of sequences resident on the device
 struct Batch {
   int64_t n;
@@ -49,9 +58,9 @@ struct Batch {
   const int64_t *off;
   const int64_t *len;
   const int64_t *root;    // optional pre-resolved root row per entry (-1: none)
-  int *bucket_count;      // optional planner output: entries per length bucket (longest first)
-  int *bucket_items;      //   and the entries of each bucket (stride n)
-  unsigned long long *work;  // work counter (zeroed before launch)
+  int *bucket_items;      // optional planner output: entries of each length bucket (stride n;
+                          // counts in sched->count), longest first
+  Sched *sched;           // scheduler block (clean on entry, left clean on exit)
   // walk outputs
   int64_t *o_m;
   int64_t *o_parent;

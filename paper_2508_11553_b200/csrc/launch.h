@@ -19,9 +19,9 @@ struct ExportArgsHost {
   int64_t *resp;
 };
 
-// fills b.root / b.bucket_count / b.bucket_items / b.work (scratch: plan_scratch_ints(n) ints)
-cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *scratch, cudaStream_t s);
-int64_t plan_scratch_ints(int64_t n);
+// fills b.root (if root != null) and b.bucket_items (plan_items_ints(n) ints); counts go to b.sched
+cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *items, cudaStream_t s);
+int64_t plan_items_ints(int64_t n);
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &e, int num_sms, cudaStream_t s);

@@ -119,11 +119,25 @@ struct tm_store {
   int64_t max_depth = 0;
   DevBytes scratch, dtok;
   PinBytes pin, ptok;
+  // Device-memory match batches are read-only: they may overlap each other (a batch's
+  // planner and grid ramp-up hide under the previous batch's tail) but not a mutation.
+  // Each in-flight batch uses one slot (scratch + scheduler block + completion event).
+  struct MatchSlot {
+    cudaEvent_t done = nullptr;
+    bool used = false;
+    DevBytes scratch;
+    tms::Sched *sched = nullptr;
+  };
+  static constexpr int kSlots = 4;
+  MatchSlot slots[kSlots];
+  int next_slot = 0;
   // optional per-kernel CUDA-event timing (tm_profile_*): pairs recorded around launches
   // batches at least this large get the longest-first planner.  Off by default: on the
   // c4 workload in-kernel root lookups are hidden by occupancy and the planner's ~10 us
   // costs more than the tail it removes (TM_PLAN_MIN at store creation overrides).
   int64_t plan_min = int64_t(1) << 62;
+  int plan_roots = 0;           // planner also resolves root rows (TM_PLAN_ROOTS=1)
+  tms::Sched *sched = nullptr;  // walk scheduler block (self-cleaning)
   bool profile = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
   size_t ev_used[4] = {0, 0, 0, 0};
@@ -237,8 +251,11 @@ struct ProfScope {
   }
 };
 
+// exclusive operations (record, export, host-buffer match) wait for everything before them
 void wait_prev(tm_store *s, cudaStream_t st) {
   ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
+  for (auto &sl : s->slots)
+    if (sl.used) ck(cudaStreamWaitEvent(st, sl.done, 0), "cudaStreamWaitEvent");
 }
 
 void mark_done(tm_store *s, cudaStream_t st) { ck(cudaEventRecord(s->last, st), "cudaEventRecord"); }
@@ -347,12 +364,20 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
   tm_store *s = new tm_store();
   s->device = c.device;
   if (const char *e = getenv("TM_PLAN_MIN")) s->plan_min = atoll(e);
+  if (const char *e = getenv("TM_PLAN_ROOTS")) s->plan_roots = atoi(e);
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
     ck(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, c.device), "attr");
     ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&s->last, cudaEventDisableTiming), "event");
     ck(cudaMalloc((void **)&s->v.ctr, sizeof(int64_t) * 4), "ctr");
+    ck(cudaMalloc((void **)&s->sched, sizeof(tms::Sched)), "sched");
+    ck(cudaMemsetAsync(s->sched, 0, sizeof(tms::Sched), s->stream), "sched");
+    for (auto &sl : s->slots) {
+      ck(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming), "event");
+      ck(cudaMalloc((void **)&sl.sched, sizeof(tms::Sched)), "sched");
+      ck(cudaMemsetAsync(sl.sched, 0, sizeof(tms::Sched), s->stream), "sched");
+    }
     ck(cudaMemsetAsync(s->v.ctr, 0, sizeof(int64_t) * 4, s->stream), "ctr");
     ensure_arena(s, std::max<int64_t>(c.arena_words, 1 << 16));
     ensure_rows(s, std::max<int64_t>(c.row_capacity, 64));
@@ -380,13 +405,19 @@ int tm_store_destroy(tm_store *s) {
     void *ptrs[] = {s->v.arena, s->v.row_vb, s->v.row_m, s->v.row_len, s->v.row_parent, s->v.row_sess,
                     s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.run_start,
                     s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
-                    s->v.s_stored, s->v.s_naive, s->v.ctr};
+                    s->v.s_stored, s->v.s_naive, s->v.ctr, s->sched};
     for (void *p : ptrs)
       if (p) cudaFree(p);
     s->scratch.~DevBytes();
     new (&s->scratch) DevBytes();
     s->dtok.~DevBytes();
     new (&s->dtok) DevBytes();
+    for (auto &sl : s->slots) {
+      cudaEventDestroy(sl.done);
+      if (sl.sched) cudaFree(sl.sched);
+      sl.scratch.~DevBytes();
+      new (&sl.scratch) DevBytes();
+    }
     cudaEventDestroy(s->last);
     cudaStreamDestroy(s->stream);
   }
@@ -468,8 +499,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
              o_sp = lay.add(4 * n), o_crow = lay.add(8 * n), o_cloc = lay.add(4 * n);
       size_t out_end = lay.bytes;
       size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n),
-             o_root = lay.add(8 * n), o_plan = lay.add(4 * (size_t)tms::plan_scratch_ints(n)),
-             o_work = lay.add(8 * (size_t)nwaves);
+             o_root = lay.add(8 * n), o_plan = lay.add(4 * (size_t)tms::plan_items_ints(n));
       char *h = (char *)s->pin.need(lay.bytes);
       char *d = (char *)s->scratch.need(lay.bytes);
       int32_t *h_sid = (int32_t *)(h + o_sid);
@@ -491,7 +521,6 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       }
       h_roff[n] = rr;
       ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
-      ck(cudaMemsetAsync(d + o_work, 0, 8 * (size_t)nwaves, s->stream), "memset work");
       // ---- waves: walk (K1) then commit (K2)
       for (int32_t w = 0; w < nwaves; w++) {
         int64_t b0 = wbeg[w], b1 = wbeg[w + 1];
@@ -501,7 +530,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         b.tok = (const int32_t *)s->dtok.p;
         b.off = (const int64_t *)(d + o_off) + b0;
         b.len = (const int64_t *)(d + o_len) + b0;
-        b.work = (unsigned long long *)(d + o_work) + w;
+        b.sched = s->sched;
         b.o_m = (int64_t *)(d + o_m) + b0;
         b.o_parent = (int64_t *)(d + o_par) + b0;
         b.o_dup = (int64_t *)(d + o_dup) + b0;
@@ -518,7 +547,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         b.c_local = (int32_t *)(d + o_cloc) + b0;
         if (b.n >= s->plan_min) {
           ProfScope ps(s, 3, s->stream);
-          ck(tms::launch_plan(s->v, b, (int64_t *)(d + o_root) + b0, (int *)(d + o_plan), s->stream), "plan");
+          ck(tms::launch_plan(s->v, b, s->plan_roots ? (int64_t *)(d + o_root) + b0 : nullptr, (int *)(d + o_plan),
+                              s->stream), "plan");
         }
         {
           ProfScope ps(s, 0, s->stream);
@@ -575,17 +605,25 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
-    wait_prev(s, st);
+    const bool dev = mem == TM_MEM_DEVICE;
+    tm_store::MatchSlot *slot = nullptr;
+    if (dev) {  // read-only, device buffers: may overlap other device matches, not mutations
+      slot = &s->slots[s->next_slot++ % tm_store::kSlots];
+      ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
+      if (slot->used) ck(cudaStreamWaitEvent(st, slot->done, 0), "cudaStreamWaitEvent");
+    } else {
+      wait_prev(s, st);
+    }
     Layout lay;
     size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n);
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n);
     size_t out_end = lay.bytes;
-    size_t o_root = lay.add(8 * n), o_work = lay.add(8), o_plan = lay.add(4 * (size_t)tms::plan_scratch_ints(n));
-    char *d = (char *)s->scratch.need(lay.bytes);
+    size_t o_root = lay.add(8 * n), o_plan = lay.add(4 * (size_t)tms::plan_items_ints(n));
+    char *d = (char *)(dev ? slot->scratch : s->scratch).need(lay.bytes);
     Batch b{};
     b.n = n;
-    b.work = (unsigned long long *)(d + o_work);
+    b.sched = dev ? slot->sched : s->sched;
     if (mem == TM_MEM_HOST) {
       for (int64_t k = 0; k < n; k++)
         if (sids[k] < 0 || sids[k] >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sids[k]));
@@ -620,9 +658,8 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     }
     if (n >= s->plan_min) {
       ProfScope ps(s, 3, st);
-      ck(tms::launch_plan(s->v, b, (int64_t *)(d + o_root), (int *)(d + o_plan), st), "plan");
-    } else {
-      ck(cudaMemsetAsync(b.work, 0, 8, st), "memset work");
+      ck(tms::launch_plan(s->v, b, s->plan_roots ? (int64_t *)(d + o_root) : nullptr, (int *)(d + o_plan), st),
+         "plan");
     }
     {
       ProfScope ps(s, 0, st);
@@ -637,7 +674,8 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
       if (out_parent) memcpy(out_parent, h + o_par, 8 * n);
       if (out_dup) memcpy(out_dup, h + o_dup, 8 * n);
     } else {
-      mark_done(s, st);
+      ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
+      slot->used = true;
     }
   });
 }
@@ -821,6 +859,8 @@ int tm_synchronize(tm_store *s) {
   return guarded(s, [&] {
     ck(cudaStreamSynchronize(s->stream), "sync");
     ck(cudaEventSynchronize(s->last), "sync");
+    for (auto &sl : s->slots)
+      if (sl.used) ck(cudaEventSynchronize(sl.done), "sync");
   });
 }
 

@@ -14,23 +14,26 @@ from workloads import pack_records
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["default", "planner"])
+@pytest.fixture(scope="module", params=["default", "planner", "planner+roots"])
 def store(request):
-    """Every test runs twice: default path, and with the longest-first planner forced on."""
+    """Every test runs on each walk schedule: the store default, the longest-first
+    planner forced on, and the planner also resolving root rows."""
     import os
 
     from paper_2508_11553_b200 import DeviceStore
 
-    old = os.environ.get("TM_PLAN_MIN")
-    if request.param == "planner":
-        os.environ["TM_PLAN_MIN"] = "1"
+    env = {"default": {}, "planner": {"TM_PLAN_MIN": "1", "TM_PLAN_ROOTS": "0"},
+           "planner+roots": {"TM_PLAN_MIN": "1", "TM_PLAN_ROOTS": "1"}}[request.param]
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         s = DeviceStore(0)
     finally:
-        if old is None:
-            os.environ.pop("TM_PLAN_MIN", None)
-        else:
-            os.environ["TM_PLAN_MIN"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     yield s
     s.close()
 

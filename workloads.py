@@ -105,31 +105,34 @@ class MatchWorkload:
         self.run_start = np.concatenate([r[0] for r in runs])
         self.run_origin = np.concatenate([r[1] for r in runs])
         self.run_version = np.concatenate([r[2] for r in runs])
-        # queries
-        qs = rng.integers(0, n_sessions, n_queries)
-        ext = rng.random(n_queries) < ext_frac
-        qlen = np.empty(n_queries, np.int64)
-        depth = np.empty(n_queries, np.int64)
-        for i in range(n_queries):
-            L = lens[qs[i]]
-            depth[i] = L if ext[i] else rng.integers(0, L)
-            qlen[i] = depth[i] + new_tokens
+        self.n_queries = n_queries
+        self.ext_frac, self.new_tokens = ext_frac, new_tokens
+        self.set_queries(self.make_queries(rng))
+
+    def make_queries(self, rng):
+        """One batch: 75% full history + new tokens, 25% branches with a forced mismatch."""
+        n, lens, new_tokens = self.n_queries, self.hist_len, self.new_tokens
+        qs = rng.integers(0, self.n_sessions, n)
+        ext = rng.random(n) < self.ext_frac
+        depth = np.where(ext, lens[qs], (rng.random(n) * lens[qs]).astype(np.int64))
+        qlen = depth + new_tokens
         qpad = (qlen + ALIGN - 1) // ALIGN * ALIGN
-        self.q_off = np.zeros(n_queries + 1, np.int64)
-        np.cumsum(qpad, out=self.q_off[1:])
-        self.q_tokens = np.zeros(int(self.q_off[-1]), np.int32)
-        for i in range(n_queries):
-            s, d, o = qs[i], int(depth[i]), int(self.q_off[i])
+        q_off = np.zeros(n + 1, np.int64)
+        np.cumsum(qpad, out=q_off[1:])
+        q_tokens = np.zeros(int(q_off[-1]), np.int32)
+        for i in range(n):
+            s, d, o = qs[i], int(depth[i]), int(q_off[i])
             h = self.hist_tokens[self.hist_off[s]: self.hist_off[s] + lens[s]]
-            self.q_tokens[o: o + d] = h[:d]
+            q_tokens[o: o + d] = h[:d]
             tail = rng.integers(0, VOCAB, new_tokens, dtype=np.int32)
             if d < lens[s]:  # forced mismatch at d
                 tail[0] = (int(h[d]) + 1 + int(rng.integers(0, VOCAB - 1))) % VOCAB
-            self.q_tokens[o + d: o + d + new_tokens] = tail
-        self.q_sess = qs.astype(np.int32)
-        self.q_len = qlen
-        self.q_depth = depth  # expected matched length
-        self.n_queries = n_queries
+            q_tokens[o + d: o + d + new_tokens] = tail
+        return dict(q_sess=qs.astype(np.int32), q_len=qlen, q_depth=depth, q_off=q_off, q_tokens=q_tokens)
+
+    def set_queries(self, q):
+        self.q_sess, self.q_len, self.q_depth = q["q_sess"], q["q_len"], q["q_depth"]
+        self.q_off, self.q_tokens = q["q_off"], q["q_tokens"]
 
     def compared_tokens(self, matched, parent_len):
         """c_q = min(m+1, |q|, |parent|) per query."""
