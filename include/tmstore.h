@@ -80,14 +80,16 @@ int tm_session_count(tm_store *store, int64_t *out_n);
  *   out_parent       global parent row (-1 if none)
  *   out_parent_local session-local parent ordinal (-1 if none)
  *   out_added        added_tokens (= len - matched, 0 for an existing sequence)
- * mem applies to the token/run/sid inputs; outputs are host arrays (the call is
- * synchronous, as lpm_insert is).  Errors: empty sequence or non-parallel metadata
+ * mem applies to `tokens` only (TM_MEM_DEVICE: a device buffer with 128-byte aligned
+ * sequence starts, e.g. tokens produced on the GPU); every other array is host memory
+ * and the call is synchronous, as lpm_insert is.  With TM_MEM_DEVICE the tokens are
+ * read after all work already queued on `stream` (their producer; NULL = none).  Errors: empty sequence or non-parallel metadata
  * -> TM_EINVAL (trie.py:128-131); unknown session -> TM_ENOENT. */
 int tm_record_batch(tm_store *store, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
                     const int64_t *tok_off, const int64_t *tok_len, const int64_t *run_off,
                     const int32_t *run_start, const uint8_t *run_origin, const int32_t *run_version,
                     int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
-                    int32_t *out_parent_local, int64_t *out_added);
+                    int32_t *out_parent_local, int64_t *out_added, void *stream);
 
 /* Read-only longest-prefix match of a batch of queries (no mutation): the LPM walk
  * of lpm_insert (trie.py:136-158) without the record step.
@@ -135,6 +137,31 @@ int tm_store_stats(tm_store *store, int64_t *rows, int64_t *arena_used, int64_t 
 
 /* The store's CUDA stream (cudaStream_t) for callers that want to order work after it. */
 int tm_store_stream(tm_store *store, void **out_stream);
+
+/* ---- Cross-GPU routing on one node (session-hash sharding, config 5) ----------------
+ * Every rank publishes its query batch in a shared device region laid out as
+ *   [RouteDesc header | int64 gsid[n] | int64 tok_off[n] | int64 len[n] | int32 tokens |
+ *    int32 idx[n] | int64 out_matched[n] | int64 out_parent[n] | int64 out_dup[n]]
+ * (offsets[8] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup).
+ * tm_route_prepare writes the header and buckets the batch by owner rank
+ * (owner = splitmix64(gsid) mod nranks).  After a cross-rank barrier (e.g. a tiny NCCL
+ * all-reduce on the same stream) every owner calls tm_match_routed, whose kernel reads
+ * its queries directly from the requesters' regions over NVLink and writes results
+ * back into them (P2P), then a second barrier publishes the results.
+ * Regions come from tm_shared_alloc (whole cudaMalloc allocations, IPC-exportable);
+ * peers map them with tm_ipc_handle (64-byte cudaIpcMemHandle) / tm_ipc_open. */
+int tm_route_desc_bytes(int64_t *out_bytes); /* size of the RouteDesc header */
+int tm_shared_alloc(tm_store *store, int64_t bytes, void **out_ptr);
+int tm_shared_free(tm_store *store, void *ptr);
+int tm_ipc_handle(tm_store *store, void *ptr, void *out_handle64);
+int tm_ipc_open(tm_store *store, const void *handle64, void **out_ptr);
+int tm_ipc_close(tm_store *store, void *ptr);
+int tm_route_prepare(tm_store *store, void *region, int64_t n, const int64_t *offsets, int32_t nranks,
+                     void *stream);
+/* g2l: device int32[global sessions] -> this store's session id (-1 if not owned).
+ * peer_regions: host array of nranks device pointers (this rank's own region at [rank]). */
+int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                    void *stream);
 
 /* Per-kernel CUDA-event timing for benchmarks.  tm_profile_begin starts recording an
  * event pair around every launch; tm_profile_end(kind) waits for them and returns the

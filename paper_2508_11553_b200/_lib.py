@@ -31,7 +31,7 @@ SIGNATURES = {
     "tm_store_destroy": (C.c_int, [_P]),
     "tm_session_create": (C.c_int, [_P, _P]),
     "tm_session_count": (C.c_int, [_P, _P]),
-    "tm_record_batch": (C.c_int, [_P, _I64, _I32] + [_P] * 14),
+    "tm_record_batch": (C.c_int, [_P, _I64, _I32] + [_P] * 15),
     "tm_match_batch": (C.c_int, [_P, _I64, _I32] + [_P] * 8),
     "tm_rows_total": (C.c_int, [_P, _I64, _P, _P]),
     "tm_export_rows": (C.c_int, [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P]),
@@ -42,6 +42,14 @@ SIGNATURES = {
     "tm_store_stream": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
+    "tm_route_desc_bytes": (C.c_int, [_P]),
+    "tm_shared_alloc": (C.c_int, [_P, _I64, _P]),
+    "tm_shared_free": (C.c_int, [_P, _P]),
+    "tm_ipc_handle": (C.c_int, [_P, _P, _P]),
+    "tm_ipc_open": (C.c_int, [_P, _P, _P]),
+    "tm_ipc_close": (C.c_int, [_P, _P]),
+    "tm_route_prepare": (C.c_int, [_P, _P, _I64, _P, _I32, _P]),
+    "tm_match_routed": (C.c_int, [_P, _I32, _I32, _P, _P, _P]),
     "tm_profile_end": (C.c_int, [_P, _I32, _P, _P]),
 }
 

@@ -50,12 +50,91 @@ __global__ void __launch_bounds__(kPlanNT) k_plan(DevView v, Batch b, int64_t *r
 // K1 walk.  Per query: root lookup (session, q[0]) -> row; compare the row's own
 // segment from the current position; at the first mismatch j look up the child
 // branching at (row, j, q[j]); continue in the child or finish.
+
+// Where one query's results go (element pointers; tnext/spar only when recording).
+struct WalkOut {
+  int64_t *m, *parent, *dup;
+  int32_t *tnext, *spar;
+};
+
+struct WalkShared {
+  int red[32];
+  long long row;
+  int lo;
+};
+
+// Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).
+template <int NT, int U>
+__device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
+                                           WalkOut o, WalkShared &sh) {
+  if (threadIdx.x == 0) {
+    int64_t r = -1;
+    if (root_hint) r = *root_hint;
+    else if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+    if (r < 0) {  // nothing shares the first token: matched 0
+      *o.m = 0;
+      *o.parent = -1;
+      *o.dup = -1;
+      if (o.tnext) { *o.tnext = L > 0 ? q[0] : -1; *o.spar = -1; }
+    }
+    sh.row = r;
+    sh.lo = 1;
+  }
+  __syncthreads();
+  int64_t r = sh.row;
+  int lo = sh.lo;
+  __syncthreads();
+  while (r >= 0) {
+    const int Lr = v.row_len[r];
+    const int hi = min(Lr, L);
+    const int32_t *a = v.arena + v.row_vb[r];
+    const int j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+    if (threadIdx.x == 0) {
+      int64_t next = -1;
+      if (j < L) {
+        const int32_t t = q[j];
+        next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
+        if (next < 0) {
+          *o.m = j;
+          *o.parent = r;
+          *o.dup = -1;
+          if (o.tnext) { *o.tnext = t; *o.spar = j < Lr ? a[j] : -1; }
+        }
+      } else {  // the query ended inside (or at the end of) row r
+        int64_t dup = (L == Lr) ? r : ht_find(v, (uint64_t)r, dt_key(L, 0, true));
+        *o.m = L;
+        *o.parent = r;
+        *o.dup = dup;
+        if (o.tnext) { *o.tnext = -1; *o.spar = L < Lr ? a[L] : -1; }
+      }
+      sh.row = next;
+      sh.lo = j + 1;
+    }
+    __syncthreads();
+    r = sh.row;
+    lo = sh.lo;
+    __syncthreads();
+  }
+}
+
+// The last CTA out leaves the scheduler block zeroed for the next launch, so a steady
+// stream of batches needs no memset.
+__device__ __forceinline__ void sched_exit(Sched *sc) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&sc->exit, 1u) == gridDim.x - 1) {
+      for (int i = 0; i < kPlanNB; i++) sc->count[i] = 0;
+      sc->work = 0;
+      sc->exit = 0;
+      __threadfence();
+    }
+  }
+}
+
 template <int NT, int U>
 __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
-  __shared__ int s_red[NT / 32];
+  __shared__ WalkShared sh;
   __shared__ long long s_item;
-  __shared__ long long s_row;
-  __shared__ int s_lo;
   __shared__ int s_base[kPlanNB + 1];
   if (b.bucket_items) {  // exclusive scan of the planner's bucket sizes
     if (threadIdx.x == 0) {
@@ -81,70 +160,135 @@ __global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
     __syncthreads();
     const int64_t w = s_item;
     if (w >= b.n) {
-      // the last CTA out leaves the scheduler block zeroed for the next launch, so a
-      // steady stream of batches needs no memset
-      if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&b.sched->exit, 1u) == gridDim.x - 1) {
-          for (int i = 0; i < kPlanNB; i++) b.sched->count[i] = 0;
-          b.sched->work = 0;
-          b.sched->exit = 0;
-          __threadfence();
-        }
-      }
+      sched_exit(b.sched);
       return;
     }
-    const int32_t *q = b.tok + b.off[w];
-    const int L = (int)b.len[w];
-    const int32_t sid = b.sids[w];
-    if (threadIdx.x == 0) {
-      int64_t r = -1;
-      if (b.root) r = b.root[w];
-      else if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
-      if (r < 0) {  // nothing shares the first token: matched 0
-        b.o_m[w] = 0;
-        b.o_parent[w] = -1;
-        b.o_dup[w] = -1;
-        if (b.o_tnext) { b.o_tnext[w] = L > 0 ? q[0] : -1; b.o_spar[w] = -1; }
-      }
-      s_row = r;
-      s_lo = 1;
-    }
+    WalkOut o{b.o_m + w, b.o_parent + w, b.o_dup + w, b.o_tnext ? b.o_tnext + w : nullptr,
+              b.o_spar ? b.o_spar + w : nullptr};
+    walk_query<NT, U>(v, b.tok + b.off[w], (int)b.len[w], b.sids[w], b.root ? b.root + w : nullptr, o, sh);
+  }
+}
+
+// ----------------------------------------------------------------------------------
+// Cross-GPU routing on one node (config 5).  Every rank publishes its query batch in
+// an IPC-shared region (RouteDesc + arrays); k_route buckets the batch by owner rank
+// (session-hash sharding); after a cross-rank barrier each owner runs k_walk_routed,
+// which reads its queries straight out of the requesters' HBM over NVLink (P2P loads)
+// and writes the results back into the requesters' output arrays (P2P stores): the
+// exchange is fused into the match kernel — no staging copies, no reverse collective.
+
+__device__ __forceinline__ int owner_of(int64_t gsid, int nranks) {
+  return (int)(mix64((uint64_t)gsid + 0x9e3779b97f4a7c15ull) % (uint64_t)nranks);
+}
+
+constexpr int kRouteNT = 1024;
+
+// One CTA buckets the batch by (owner, length bucket) — owner-major, longest first.
+__global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
+  RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
+  const int64_t n = d->n;
+  const int64_t *gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
+  const int64_t *len = reinterpret_cast<const int64_t *>(region + d->len_off);
+  int32_t *idx = reinterpret_cast<int32_t *>(region + d->idx_off);
+  constexpr int NC = kMaxRanks * kPlanNB;
+  __shared__ int cnt[NC];
+  __shared__ int wsum[kRouteNT / 32];
+  for (int i = threadIdx.x; i < NC; i += kRouteNT) cnt[i] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += kRouteNT)
+    atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1);
+  __syncthreads();
+  // exclusive scan of the 2048 counters (2 per thread)
+  constexpr int PER = NC / kRouteNT;
+  int loc[PER], acc = 0;
+#pragma unroll
+  for (int j = 0; j < PER; j++) { loc[j] = acc; acc += cnt[threadIdx.x * PER + j]; }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = acc;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, s);
+    if (lane >= s) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int pre = 0;
+  for (int w = 0; w < warp; w++) pre += wsum[w];
+  const int excl = pre + x - acc;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PER; j++) {
+    const int c = threadIdx.x * PER + j;
+    d->bcount[c] = cnt[c];
+    d->bstart[c] = excl + loc[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxRanks) {
+    int tot = 0;
+    for (int b2 = 0; b2 < kPlanNB; b2++) tot += d->bcount[threadIdx.x * kPlanNB + b2];
+    d->count[threadIdx.x] = tot;
+    d->start[threadIdx.x] = d->bstart[threadIdx.x * kPlanNB];
+  }
+#pragma unroll
+  for (int j = 0; j < PER; j++) cnt[threadIdx.x * PER + j] = excl + loc[j];  // cursors
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += kRouteNT)
+    idx[atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1)] = (int32_t)i;
+}
+
+// Owner side.  Items are ordered (length bucket, requester): the global longest-first
+// order over all requesters' queries owned here; rank -> item via a prefix table.
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) k_walk_routed(DevView v, RoutedArgs a) {
+  __shared__ WalkShared sh;
+  __shared__ long long s_item;
+  __shared__ int s_pre[kPlanNB * kMaxRanks + 1];  // prefix over (bucket, peer)
+  __shared__ int s_bs[kPlanNB * kMaxRanks];       // bstart of (bucket, peer)
+  const int np = a.nranks;
+  for (int c = threadIdx.x; c < kPlanNB * np; c += NT) {
+    const int bk = c / np, p = c % np;
+    const RouteDesc *d = reinterpret_cast<const RouteDesc *>(a.peer[p]);
+    s_pre[c] = d->bcount[a.rank * kPlanNB + bk];  // counts, scanned below
+    s_bs[c] = d->bstart[a.rank * kPlanNB + bk];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < kPlanNB * np; c++) { int t = s_pre[c]; s_pre[c] = acc; acc += t; }
+    s_pre[kPlanNB * np] = acc;
+  }
+  __syncthreads();
+  const int total = s_pre[kPlanNB * np];
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
     __syncthreads();
-    int64_t r = s_row;
-    int lo = s_lo;
-    __syncthreads();
-    while (r >= 0) {
-      const int Lr = v.row_len[r];
-      const int hi = min(Lr, L);
-      const int32_t *a = v.arena + v.row_vb[r];
-      const int j = block_first_mismatch<NT, U>(q, a, lo, hi, s_red);
-      if (threadIdx.x == 0) {
-        int64_t next = -1;
-        if (j < L) {
-          const int32_t t = q[j];
-          next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
-          if (next < 0) {
-            b.o_m[w] = j;
-            b.o_parent[w] = r;
-            b.o_dup[w] = -1;
-            if (b.o_tnext) { b.o_tnext[w] = t; b.o_spar[w] = j < Lr ? a[j] : -1; }
-          }
-        } else {  // the query ended inside (or at the end of) row r
-          int64_t dup = (L == Lr) ? r : ht_find(v, (uint64_t)r, dt_key(L, 0, true));
-          b.o_m[w] = L;
-          b.o_parent[w] = r;
-          b.o_dup[w] = dup;
-          if (b.o_tnext) { b.o_tnext[w] = -1; b.o_spar[w] = L < Lr ? a[L] : -1; }
-        }
-        s_row = next;
-        s_lo = j + 1;
-      }
-      __syncthreads();
-      r = s_row;
-      lo = s_lo;
-      __syncthreads();
+    const long long it = s_item;
+    if (it >= total) {
+      sched_exit(a.sched);
+      return;
     }
+    int lo = 0, hi = kPlanNB * np;  // last cell with prefix <= it
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= it) lo = mid; else hi = mid;
+    }
+    const int p = lo % np;
+    const char *reg = a.peer[p];
+    const RouteDesc *d = reinterpret_cast<const RouteDesc *>(reg);
+    const int32_t qi = reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[lo] + (it - s_pre[lo])];
+    const int64_t g = reinterpret_cast<const int64_t *>(reg + d->sid_off)[qi];
+    const int64_t off = reinterpret_cast<const int64_t *>(reg + d->qoff_off)[qi];
+    const int L = (int)reinterpret_cast<const int64_t *>(reg + d->len_off)[qi];
+    char *wreg = const_cast<char *>(reg);
+    WalkOut o{reinterpret_cast<int64_t *>(wreg + d->m_off) + qi, reinterpret_cast<int64_t *>(wreg + d->par_off) + qi,
+              reinterpret_cast<int64_t *>(wreg + d->dup_off) + qi, nullptr, nullptr};
+    const int32_t sid = a.g2l[g];
+    if (sid < 0) {  // routed to the wrong owner: flag it, never guess
+      if (threadIdx.x == 0) { *o.m = -1; *o.parent = -1; *o.dup = -1; }
+      __syncthreads();
+      continue;
+    }
+    walk_query<NT, U>(v, reinterpret_cast<const int32_t *>(reg + d->tok_off) + off, L, sid, nullptr, o, sh);
   }
 }
 
@@ -457,5 +601,20 @@ cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s
 }
 
 int export_tile_tokens() { return kExportTile; }
+
+cudaError_t launch_route(char *region, int nranks, cudaStream_t s) {
+  k_route<<<1, kRouteNT, 0, s>>>(region, nranks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_routed<kWalkNT, kWalkU>, kWalkNT, 0);
+    if (occ < 1) occ = 1;
+  }
+  k_walk_routed<kWalkNT, kWalkU><<<num_sms * occ, kWalkNT, 0, s>>>(v, a);
+  return cudaGetLastError();
+}
 
 }  // namespace tms

@@ -50,6 +50,32 @@ struct Sched {
   unsigned int exit;
 };
 
+// Routing descriptor at the start of every rank's IPC-shared region (byte offsets are
+// relative to the region base; arrays hold the rank's query batch and its results).
+constexpr int kMaxRanks = 16;
+struct RouteDesc {
+  int64_t n;        // queries in this rank's batch
+  int64_t sid_off;  // int64 global session id per query
+  int64_t qoff_off; // int64 token offset per query (multiple of 32)
+  int64_t len_off;  // int64 length per query
+  int64_t tok_off;  // int32 tokens
+  int64_t idx_off;  // int32 query indices grouped by owner (written by k_route)
+  int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
+  int32_t count[kMaxRanks];  // queries owned by each rank (written by k_route)
+  int32_t start[kMaxRanks];
+  // per (owner, length bucket; longest first) counts and starts in idx[], so owners can
+  // process every requester's queries in one global longest-first order
+  int32_t bcount[kMaxRanks * kPlanNB];
+  int32_t bstart[kMaxRanks * kPlanNB];
+};
+
+struct RoutedArgs {
+  int nranks, rank;
+  const char *peer[kMaxRanks];  // every rank's region as mapped on this GPU (own included)
+  const int32_t *g2l;           // global session id -> local session id (-1: not owned)
+  Sched *sched;
+};
+
 // one batch of sequences resident on the device
 struct Batch {
   int64_t n;

@@ -6,6 +6,7 @@
 namespace tms {
 struct DevView;
 struct Batch;
+struct RoutedArgs;
 
 struct ExportArgsHost {
   int64_t n;
@@ -29,4 +30,6 @@ cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t 
                           int64_t ocap, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
 int export_tile_tokens();
+cudaError_t launch_route(char *region, int nranks, cudaStream_t s);
+cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s);
 }  // namespace tms

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -444,11 +445,11 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                     const int64_t *tok_off, const int64_t *tok_len, const int64_t *run_off,
                     const int32_t *run_start, const uint8_t *run_origin, const int32_t *run_version,
                     int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
-                    int32_t *out_parent_local, int64_t *out_added) {
+                    int32_t *out_parent_local, int64_t *out_added, void *stream) {
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
-    if (mem != TM_MEM_HOST) fail(TM_EINVAL, "tm_record_batch: only TM_MEM_HOST inputs are supported");
+    if (mem != TM_MEM_HOST && mem != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
     // ---- validate (trie.py:128-131) and build waves: entry k of a session goes to
     // wave (number of earlier entries of that session in the batch)
     std::vector<int32_t> occ(s->n_sess, 0);
@@ -490,7 +491,25 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       wait_prev(s, s->stream);
       // ---- stage tokens and per-entry arrays
       std::vector<int64_t> doff;
-      stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
+      const int32_t *tok_base;
+      if (mem == TM_MEM_DEVICE) {  // tokens already in HBM (e.g. produced by the engine)
+        if (stream && (cudaStream_t)stream != s->stream) {  // order after their producer
+          cudaEvent_t ev;
+          ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+          ck(cudaEventRecord(ev, (cudaStream_t)stream), "event");
+          ck(cudaStreamWaitEvent(s->stream, ev, 0), "wait");
+          cudaEventDestroy(ev);
+        }
+        doff.resize(n);
+        for (int64_t k = 0; k < n; k++) {
+          doff[k] = tok_off[perm[k]];
+          if (doff[k] % tms::kAlignWords) fail(TM_EINVAL, "device token offsets must be multiples of 32");
+        }
+        tok_base = tokens;
+      } else {
+        stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
+        tok_base = (const int32_t *)s->dtok.p;
+      }
       Layout lay;
       size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
              o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs);
@@ -527,7 +546,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         Batch b{};
         b.n = b1 - b0;
         b.sids = (const int32_t *)(d + o_sid) + b0;
-        b.tok = (const int32_t *)s->dtok.p;
+        b.tok = tok_base;
         b.off = (const int64_t *)(d + o_off) + b0;
         b.len = (const int64_t *)(d + o_len) + b0;
         b.sched = s->sched;
@@ -830,6 +849,87 @@ int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *are
 
 int tm_store_stream(tm_store *s, void **out_stream) {
   return guarded(s, [&] { *out_stream = (void *)s->stream; });
+}
+
+int tm_shared_alloc(tm_store *s, int64_t bytes, void **out_ptr) {
+  return guarded(s, [&] {
+    if (bytes <= 0) fail(TM_EINVAL, "bad size");
+    ck(cudaMalloc(out_ptr, (size_t)bytes), "cudaMalloc(shared)");  // a whole allocation: IPC-exportable
+    ck(cudaMemset(*out_ptr, 0, (size_t)bytes), "memset(shared)");
+  });
+}
+
+int tm_shared_free(tm_store *s, void *ptr) {
+  return guarded(s, [&] { ck(cudaFree(ptr), "cudaFree(shared)"); });
+}
+
+int tm_ipc_handle(tm_store *s, void *ptr, void *out_handle) {
+  return guarded(s, [&] {
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, ptr), "cudaIpcGetMemHandle");
+    memcpy(out_handle, &h, sizeof(h));
+  });
+}
+
+int tm_ipc_open(tm_store *s, const void *handle, void **out_ptr) {
+  return guarded(s, [&] {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    ck(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int tm_ipc_close(tm_store *s, void *ptr) {
+  return guarded(s, [&] { ck(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); });
+}
+
+int tm_route_desc_bytes(int64_t *out_bytes) {
+  *out_bytes = (int64_t)sizeof(tms::RouteDesc);
+  return TM_OK;
+}
+
+int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, void *stream) {
+  return guarded(s, [&] {
+    if (nranks < 1 || nranks > tms::kMaxRanks) fail(TM_EINVAL, "nranks out of range");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    tms::RouteDesc d{};  // counts are (re)written by k_route
+    if (offsets[0] < (int64_t)sizeof(d)) fail(TM_EINVAL, "routing arrays overlap the RouteDesc header");
+    d.n = n;
+    d.sid_off = offsets[0];
+    d.qoff_off = offsets[1];
+    d.len_off = offsets[2];
+    d.tok_off = offsets[3];
+    d.idx_off = offsets[4];
+    d.m_off = offsets[5];
+    d.par_off = offsets[6];
+    d.dup_off = offsets[7];
+    // pageable source: the copy is staged before this call returns
+    ck(cudaMemcpyAsync(region, &d, offsetof(tms::RouteDesc, count), cudaMemcpyHostToDevice, st), "H2D route desc");
+    ck(tms::launch_route((char *)region, nranks, st), "route");
+  });
+}
+
+int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                    void *stream) {
+  return guarded(s, [&] {
+    if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    tm_store::MatchSlot *slot = &s->slots[s->next_slot++ % tm_store::kSlots];
+    ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
+    if (slot->used) ck(cudaStreamWaitEvent(st, slot->done, 0), "cudaStreamWaitEvent");
+    tms::RoutedArgs a{};
+    a.nranks = nranks;
+    a.rank = rank;
+    for (int p = 0; p < nranks; p++) a.peer[p] = (const char *)peer_regions[p];
+    a.g2l = g2l;
+    a.sched = slot->sched;
+    {
+      ProfScope ps(s, 0, st);
+      ck(tms::launch_walk_routed(s->v, a, s->num_sms, st), "walk_routed");
+    }
+    ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
+    slot->used = true;
+  });
 }
 
 int tm_profile_begin(tm_store *s) {

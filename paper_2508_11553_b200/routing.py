@@ -1,0 +1,149 @@
+"""Multi-GPU session sharding and cross-shard query routing on one node.
+
+Sessions are independent (the reference keeps one trie + lock per session,
+trajectory.py:101-104, 137-145), so the store is sharded by session across GPUs, one
+process per GPU: ``owner(gsid) = splitmix64(gsid) mod nranks``.
+
+Host-originated requests (every reference entry point) are sent by the host straight to
+the owner's store — no collective.  GPU-originated batches (config 5: each rank holds a
+batch of queries in HBM for sessions owned anywhere) use ``Router.match``:
+
+1. ``tm_route_prepare`` buckets the local batch by owner inside this rank's IPC-shared
+   region;
+2. a cross-rank barrier (a one-element NCCL all-reduce on the same stream);
+3. ``tm_match_routed``: every owner's K1 kernel reads its queries directly from the
+   requesters' regions over NVLink (P2P loads) and writes matched / parent / dup back
+   into them (P2P stores) — the exchange is fused into the match kernel;
+4. a second barrier publishes the results to the requesters.
+
+PyTorch provides the process group (plumbing); the routing and matching run in the
+CUDA kernels behind include/tmstore.h.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check
+from .store import DeviceStore
+
+_M = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint64(30))
+        x = x * np.uint64(0xBF58476D1CE4E5B9)
+        x = x ^ (x >> np.uint64(27))
+        x = x * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return x
+
+
+def owner_of(gsid, nranks: int) -> np.ndarray:
+    """Owner rank of global session ids (same function as the device's owner_of)."""
+    g = np.asarray(gsid, dtype=np.int64).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        g = g + np.uint64(0x9E3779B97F4A7C15)
+    return (_mix64(g) % np.uint64(nranks)).astype(np.int64)
+
+
+class _CudaArray:
+    """Zero-copy view of raw device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def route_layout(n_max: int, tokens_max: int, header: int | None = None) -> tuple[list[int], int]:
+    """Byte offsets (sid, qoff, len, tok, idx, m, par, dup) and total bytes of a region."""
+    if header is None:
+        from . import _lib
+
+        hb = C.c_int64()
+        check(_lib.load().tm_route_desc_bytes(C.byref(hb)))
+        header = hb.value
+    off, cur = [], (header + 255) // 256 * 256  # RouteDesc header
+    for nbytes in (8 * n_max, 8 * n_max, 8 * n_max, 4 * tokens_max, 4 * n_max, 8 * n_max, 8 * n_max, 8 * n_max):
+        off.append(cur)
+        cur += (nbytes + 255) // 256 * 256
+    return off, cur
+
+
+class Router:
+    """One rank's side of cross-GPU routing (collective construction: every rank of
+    ``group`` must build its Router in the same order)."""
+
+    def __init__(self, store: DeviceStore, group, n_max: int, tokens_max: int, g2l):
+        import torch
+        import torch.distributed as dist
+
+        self.store, self.group = store, group
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        self.n_max, self.tokens_max = n_max, tokens_max
+        self.offsets, self.bytes = route_layout(n_max, tokens_max)
+        ptr = C.c_void_p()
+        check(store.lib.tm_shared_alloc(store.h, self.bytes, C.byref(ptr)))
+        self.base = ptr.value
+        h = (C.c_char * 64)()
+        check(store.lib.tm_ipc_handle(store.h, C.c_void_p(self.base), h))
+        handles = [None] * self.nranks
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.peers = []
+        for p, hb in enumerate(handles):
+            if p == self.rank:
+                self.peers.append(self.base)
+                continue
+            out = C.c_void_p()
+            check(store.lib.tm_ipc_open(store.h, (C.c_char * 64).from_buffer_copy(hb), C.byref(out)))
+            self.peers.append(out.value)
+        self._peer_arr = (C.c_void_p * self.nranks)(*self.peers)
+        self._off_arr = (C.c_int64 * 8)(*self.offsets)
+        dev = torch.device("cuda", store.device)
+        view = lambda i, n, ts, dt: torch.as_tensor(_CudaArray(self.base + self.offsets[i], (n,), ts), device=dev)  # noqa: E731
+        self.gsid = view(0, n_max, "<i8", None)
+        self.qoff = view(1, n_max, "<i8", None)
+        self.qlen = view(2, n_max, "<i8", None)
+        self.tokens = view(3, tokens_max, "<i4", None)
+        self.out_matched = view(5, n_max, "<i8", None)
+        self.out_parent = view(6, n_max, "<i8", None)
+        self.out_dup = view(7, n_max, "<i8", None)
+        self.g2l = torch.as_tensor(np.asarray(g2l, np.int32), device=dev)
+        self._bar = torch.zeros(1, device=dev)
+        dist.barrier(group=group)
+
+    def _barrier(self):
+        import torch.distributed as dist
+
+        dist.all_reduce(self._bar, group=self.group)  # stream-ordered cross-rank barrier
+
+    def match(self, n: int):
+        """Match the n queries staged in this rank's region (gsid / qoff / qlen / tokens)
+        against their owners' shards; results land in out_matched / out_parent / out_dup.
+        Enqueued on torch's current stream (the barriers' stream)."""
+        import torch
+
+        if n > self.n_max:
+            raise ValueError("batch larger than the routing region")
+        st = torch.cuda.current_stream(self.store.device).cuda_stream
+        st = C.c_void_p(1 if st == 0 else st)
+        lib, h = self.store.lib, self.store.h
+        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, st))
+        if self.nranks > 1:
+            self._barrier()
+        check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, C.c_void_p(self.g2l.data_ptr()), st))
+        if self.nranks > 1:
+            self._barrier()
+
+    def close(self):
+        lib, h = self.store.lib, self.store.h
+        for p, ptr in enumerate(self.peers):
+            if p != self.rank and ptr:
+                lib.tm_ipc_close(h, C.c_void_p(ptr))
+        if self.base:
+            lib.tm_shared_free(h, C.c_void_p(self.base))
+            self.base = None

@@ -152,7 +152,32 @@ class DeviceStore:
         check(self.lib.tm_record_batch(
             self.h, n, TM_MEM_HOST, _ptr(sids), _ptr(tokens), _ptr(tok_off), _ptr(tok_len), _ptr(run_off),
             _ptr(run_start), _ptr(run_origin), _ptr(run_version), _ptr(r.matched), _ptr(r.row), _ptr(r.local),
-            _ptr(r.parent), _ptr(r.parent_local), _ptr(r.added)))
+            _ptr(r.parent), _ptr(r.parent_local), _ptr(r.added), None))
+        return r
+
+    def record_device(self, sids, tokens, tok_off, tok_len, run_off, run_start, run_origin, run_version,
+                      stream=None) -> RecordResult:
+        """record_packed with the token buffer already on the GPU (a CUDA tensor, every
+        sequence starting at a multiple of 32 words); other arrays are host arrays.  The
+        tokens are read after the work queued on ``stream`` (default: torch's current)."""
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        sids = np.ascontiguousarray(sids, np.int32)
+        tok_off = np.ascontiguousarray(tok_off, np.int64)
+        tok_len = np.ascontiguousarray(tok_len, np.int64)
+        run_off = np.ascontiguousarray(run_off, np.int64)
+        run_start = np.ascontiguousarray(run_start, np.int32)
+        run_origin = np.ascontiguousarray(run_origin, np.uint8)
+        run_version = np.ascontiguousarray(run_version, np.int32)
+        n = len(sids)
+        r = RecordResult(np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n, np.int32),
+                         np.empty(n, np.int64), np.empty(n, np.int32), np.empty(n, np.int64))
+        check(self.lib.tm_record_batch(
+            self.h, n, TM_MEM_DEVICE, _ptr(sids), _tptr(tokens), _ptr(tok_off), _ptr(tok_len), _ptr(run_off),
+            _ptr(run_start), _ptr(run_origin), _ptr(run_version), _ptr(r.matched), _ptr(r.row), _ptr(r.local),
+            _ptr(r.parent), _ptr(r.parent_local), _ptr(r.added), self._stream_arg(stream)))
         return r
 
     def record(self, sids, seqs, runs) -> RecordResult:

