@@ -7,6 +7,7 @@
 //  k_export        K3: chain walk + gather into packed tokens / loss_mask / versions
 //  k_rehash        branch-index growth
 #include "kernels.cuh"
+
 #include "launch.h"
 
 #include <cstdlib>
@@ -293,9 +294,13 @@ __global__ void __launch_bounds__(NT) k_walk_routed(DevView v, RoutedArgs a) {
 }
 
 // ----------------------------------------------------------------------------------
-// Commit planner: one CTA scans the batch for new rows and allocates row ids, arena
-// slots (128-byte lines covering [floor32(m), ceil32(L)) ) and metadata-run slots.
-constexpr int kScanNT = 1024;
+// K2 record: one persistent launch per batch.  Work item = a session's CHAIN of entries
+// (its inserts in batch order: the sequential semantics of lpm_insert, trie.py:120-179,
+// only bind entries of the same session — sessions never share rows or branch keys).
+// The CTA owning a chain walks (K1) and commits each entry in order; chains run in
+// parallel, longest first.  Row ids are reserved by the host in batch order
+// (deterministic; an entry that re-records an existing sequence leaves its slot
+// unused); arena lines and run slots come from atomic bump counters.
 
 __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m) {
   // index (relative) of the run containing position m (runs start at 0, ascending)
@@ -308,129 +313,106 @@ __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m
   return (int)(lo - r0);
 }
 
-__global__ void __launch_bounds__(kScanNT) k_commit_plan(DevView v, Batch b) {
-  __shared__ long long s_w[kScanNT / 32], s_r[kScanNT / 32], s_n[kScanNT / 32];
-  __shared__ long long base_w, base_r, base_n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) { base_w = v.ctr[0]; base_n = v.ctr[1]; base_r = v.ctr[2]; }
-  __syncthreads();
-  for (int64_t t0 = 0; t0 < b.n; t0 += kScanNT) {
-    const int64_t w = t0 + threadIdx.x;
-    long long words = 0, runs = 0, isnew = 0;
-    int fr = 0;
-    int64_t m = 0, L = 0;
-    if (w < b.n) {
-      m = b.o_m[w];
-      L = b.len[w];
-      if (b.o_dup[w] < 0) {
-        isnew = 1;
-        if (L > m) {
-          words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
-          fr = first_run_at(b, w, m);
-          runs = (b.run_off[w + 1] - b.run_off[w]) - fr;
-        }
-      }
-    }
-    // block exclusive scans of (words, runs, isnew)
-    long long xw = words, xr = runs, xn = isnew;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      long long yw = __shfl_up_sync(0xffffffffu, xw, d);
-      long long yr = __shfl_up_sync(0xffffffffu, xr, d);
-      long long yn = __shfl_up_sync(0xffffffffu, xn, d);
-      if (lane >= d) { xw += yw; xr += yr; xn += yn; }
-    }
-    if (lane == 31) { s_w[warp] = xw; s_r[warp] = xr; s_n[warp] = xn; }
-    __syncthreads();
-    if (warp == 0) {
-      long long a = s_w[lane], c = s_r[lane], e = s_n[lane];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        long long ya = __shfl_up_sync(0xffffffffu, a, d);
-        long long yc = __shfl_up_sync(0xffffffffu, c, d);
-        long long ye = __shfl_up_sync(0xffffffffu, e, d);
-        if (lane >= d) { a += ya; c += yc; e += ye; }
-      }
-      s_w[lane] = a; s_r[lane] = c; s_n[lane] = e;  // inclusive per-warp totals
-    }
-    __syncthreads();
-    const long long pw = (warp ? s_w[warp - 1] : 0) + xw - words;
-    const long long pr = (warp ? s_r[warp - 1] : 0) + xr - runs;
-    const long long pn = (warp ? s_n[warp - 1] : 0) + xn - isnew;
-    if (w < b.n) {
-      if (isnew) {
-        b.c_row[w] = base_n + pn;
-        b.c_vb[w] = base_w + pw - (m / kAlignWords) * kAlignWords;
-        b.c_run0[w] = base_r + pr;
-        b.c_firstrun[w] = fr;
-      } else {
-        b.c_row[w] = b.o_dup[w];
-        b.c_vb[w] = 0;
-        b.c_run0[w] = 0;
-        b.c_firstrun[w] = 0;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      base_w += s_w[kScanNT / 32 - 1];
-      base_r += s_r[kScanNT / 32 - 1];
-      base_n += s_n[kScanNT / 32 - 1];
-    }
-    __syncthreads();
+// allocation need of entry e: (arena words, runs, new row)
+__device__ __forceinline__ void entry_need(const Batch &b, int64_t e, long long &words, long long &runs,
+                                           long long &isnew) {
+  words = runs = isnew = 0;
+  const int64_t m = b.o_m[e], L = b.len[e];
+  b.c_firstrun[e] = 0;
+  if (b.o_dup[e] >= 0) return;
+  isnew = 1;
+  if (L > m) {
+    words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
+    const int fr = first_run_at(b, e, m);
+    b.c_firstrun[e] = fr;
+    runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
   }
-  if (threadIdx.x == 0) { v.ctr[0] = base_w; v.ctr[1] = base_n; v.ctr[2] = base_r; }
 }
 
-// ----------------------------------------------------------------------------------
-// K2 commit: one CTA per entry (grid-stride).  At most one entry per session per
-// wave, so session counters need no atomics.
-constexpr int kCommitNT = 256;
-
-__global__ void __launch_bounds__(kCommitNT) k_commit(DevView v, Batch b) {
-  for (int64_t w = blockIdx.x; w < b.n; w += gridDim.x) {
-    const int64_t m = b.o_m[w];
-    const int64_t L = b.len[w];
-    const int32_t sid = b.sids[w];
-    const int64_t row = b.c_row[w];
-    const bool isnew = b.o_dup[w] < 0;
-    if (threadIdx.x == 0) {
-      if (isnew) {
-        const int64_t par = b.o_parent[w];
-        const int32_t local = v.s_nrows[sid];
-        v.s_nrows[sid] = local + 1;
-        v.row_vb[row] = b.c_vb[w];
-        v.row_m[row] = (int32_t)m;
-        v.row_len[row] = (int32_t)L;
-        v.row_parent[row] = par;
-        v.row_sess[row] = sid;
-        v.row_local[row] = local;
-        v.row_depth[row] = par >= 0 ? v.row_depth[par] + 1 : 0;
-        v.row_run0[row] = b.c_run0[w];
-        v.row_nrun[row] = L > m ? (int32_t)(b.run_off[w + 1] - b.run_off[w] - b.c_firstrun[w]) : 0;
-        v.s_stored[sid] += L - m;
-        const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
-        if (L > m) ht_insert(v, owner, dt_key(m, b.tok[b.off[w] + m], false), row);
-        else ht_insert(v, owner, dt_key(m, 0, true), row);
-        b.c_local[w] = local;
-      } else {
-        b.c_local[w] = v.row_local[row];
-      }
-      v.s_naive[sid] += L;
+// commit entry e (whole CTA)
+template <int NT>
+__device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, int64_t e) {
+  const int64_t m = b.o_m[e];
+  const int64_t L = b.len[e];
+  const int32_t sid = b.sids[e];
+  const int64_t row = b.c_row[e];
+  const bool isnew = b.o_dup[e] < 0;
+  if (threadIdx.x == 0) {
+    if (isnew) {
+      const int64_t par = b.o_parent[e];
+      const int32_t local = v.s_nrows[sid];
+      v.s_nrows[sid] = local + 1;
+      v.row_vb[row] = b.c_vb[e];
+      v.row_m[row] = (int32_t)m;
+      v.row_len[row] = (int32_t)L;
+      v.row_parent[row] = par;
+      v.row_sess[row] = sid;
+      v.row_local[row] = local;
+      v.row_depth[row] = par >= 0 ? v.row_depth[par] + 1 : 0;
+      v.row_run0[row] = b.c_run0[e];
+      v.row_nrun[row] = L > m ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
+      v.s_stored[sid] += L - m;
+      const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
+      if (L > m) ht_insert(v, owner, dt_key(m, b.tok[b.off[e] + m], false), row);
+      else ht_insert(v, owner, dt_key(m, 0, true), row);
+      b.c_local[e] = local;
+    } else {
+      b.c_local[e] = v.row_local[row];
     }
-    if (!isnew || L <= m) continue;
-    // novel suffix: int4 copy of [m, L) (congruent mod 4 words; edges land in padding)
-    const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[w]);
-    int4 *dst = reinterpret_cast<int4 *>(v.arena + b.c_vb[w]);
-    for (int64_t i = (m >> 2) + threadIdx.x; i < ((L + 3) >> 2); i += kCommitNT) dst[i] = ldg_stream(src + i);
-    // metadata runs overlapping [m, L), first one clamped to m
-    const int64_t r0 = b.run_off[w] + b.c_firstrun[w];
-    const int64_t nr = b.run_off[w + 1] - r0;
-    for (int64_t k = threadIdx.x; k < nr; k += kCommitNT) {
-      const int64_t d = b.c_run0[w] + k;
-      const int32_t st = b.run_start[r0 + k];
-      v.run_start[d] = (int32_t)(st > m ? (int64_t)st : m);
-      v.run_origin[d] = b.run_origin[r0 + k];
-      v.run_version[d] = b.run_version[r0 + k];
+    v.s_naive[sid] += L;
+  }
+  if (!isnew || L <= m) return;
+  // novel suffix: int4 copy of [m, L) (congruent mod 4 words; edges land in padding)
+  const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[e]);
+  int4 *dst = reinterpret_cast<int4 *>(v.arena + b.c_vb[e]);
+  for (int64_t i = (m >> 2) + threadIdx.x; i < ((L + 3) >> 2); i += NT) dst[i] = ldg_stream(src + i);
+  // metadata runs overlapping [m, L), first one clamped to m
+  const int64_t r0 = b.run_off[e] + b.c_firstrun[e];
+  const int64_t nr = b.run_off[e + 1] - r0;
+  for (int64_t k = threadIdx.x; k < nr; k += NT) {
+    const int64_t d = b.c_run0[e] + k;
+    const int32_t st = b.run_start[r0 + k];
+    v.run_start[d] = (int32_t)(st > m ? (int64_t)st : m);
+    v.run_origin[d] = b.run_origin[r0 + k];
+    v.run_version[d] = b.run_version[r0 + k];
+  }
+}
+
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
+  const Batch &b = a.b;
+  __shared__ WalkShared sh;
+  __shared__ long long s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
+    __syncthreads();
+    const int64_t it = s_item;
+    __syncthreads();
+    if (it >= a.nchains) {
+      sched_exit(a.sched);
+      return;
+    }
+    const int64_t c = a.chain_order[it];
+    for (int64_t e = a.chain_beg[c]; e < a.chain_beg[c + 1]; e++) {
+      WalkOut o{b.o_m + e, b.o_parent + e, b.o_dup + e, b.o_tnext + e, b.o_spar + e};
+      walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh);
+      if (threadIdx.x == 0) {  // allocate (the reserved row id is already in c_row)
+        long long words, runs, isnew;
+        entry_need(b, e, words, runs, isnew);
+        const int64_t m = b.o_m[e];
+        if (isnew) {
+          const long long base = words ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)words) : 0;
+          b.c_vb[e] = base - (m / kAlignWords) * kAlignWords;
+          b.c_run0[e] = runs ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)runs) : 0;
+        } else {
+          b.c_row[e] = b.o_dup[e];
+          b.c_vb[e] = 0;
+          b.c_run0[e] = 0;
+        }
+      }
+      __syncthreads();
+      commit_entry<NT>(v, b, e);
+      __syncthreads();  // the next entry of the chain sees this one (same CTA)
     }
   }
 }
@@ -572,11 +554,16 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
   }
 }
 
-cudaError_t launch_commit(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
-  k_commit_plan<<<1, kScanNT, 0, s>>>(v, b);
-  int64_t grid = b.n < (int64_t)num_sms * 8 ? b.n : (int64_t)num_sms * 8;
+cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<kWalkNT, kWalkU>, kWalkNT, 0);
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)num_sms * occ;
+  if (grid > a.nchains) grid = a.nchains;
   if (grid < 1) grid = 1;
-  k_commit<<<(int)grid, kCommitNT, 0, s>>>(v, b);
+  k_record<kWalkNT, kWalkU><<<(int)grid, kWalkNT, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 

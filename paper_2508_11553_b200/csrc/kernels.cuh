@@ -106,6 +106,14 @@ struct Batch {
   int32_t *c_local;
 };
 
+struct RecordArgs {
+  Batch b;                    // entries grouped by session chain, batch order inside a chain
+  const int64_t *chain_beg;   // nchains + 1 entry offsets
+  const int64_t *chain_order; // chains in processing order (longest first)
+  int64_t nchains;
+  Sched *sched;               // work counter (self-cleaning)
+};
+
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 30;
   x *= 0xbf58476d1ce4e5b9ull;

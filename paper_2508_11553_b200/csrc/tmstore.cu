@@ -114,6 +114,7 @@ struct tm_store {
   DevView v{};
   int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
   int64_t arena_used = 0, n_runs = 0, n_sess = 0;
+  int64_t n_real_rows = 0;  // rows minus reserved-but-unused slots
   std::vector<RowHost> rows;
   std::vector<std::vector<int64_t>> sess_rows;
   std::vector<int64_t> sess_stored, sess_naive;
@@ -253,6 +254,8 @@ struct ProfScope {
 };
 
 // exclusive operations (record, export, host-buffer match) wait for everything before them
+bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->rows.size() && s->rows[r].sid >= 0; }
+
 void wait_prev(tm_store *s, cudaStream_t st) {
   ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
   for (auto &sl : s->slots)
@@ -450,11 +453,12 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
     if (mem != TM_MEM_HOST && mem != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
-    // ---- validate (trie.py:128-131) and build waves: entry k of a session goes to
-    // wave (number of earlier entries of that session in the batch)
-    std::vector<int32_t> occ(s->n_sess, 0);
-    std::vector<int32_t> wave(n);
-    int32_t nwaves = 0;
+    // ---- validate (trie.py:128-131); group entries into per-session chains (batch order
+    // inside a chain: sequential semantics), chains ordered longest first
+    std::vector<int32_t> chain_of_sid(s->n_sess, -1);
+    std::vector<int64_t> chain_tokens;
+    std::vector<int32_t> chain_len;
+    std::vector<int32_t> chain_idx(n);
     int64_t total_runs = 0, words_upper = 0;
     for (int64_t k = 0; k < n; k++) {
       int32_t sid = sids[k];
@@ -469,151 +473,158 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
           fail(TM_EINVAL, "tokens, origins, versions must be parallel");
       for (int64_t r = r0; r < r1; r++)
         if (run_origin[r] > 1) fail(TM_EINVAL, "bad origin");
-      wave[k] = occ[sid]++;
-      nwaves = std::max(nwaves, wave[k] + 1);
+      if (mem == TM_MEM_DEVICE && tok_off[k] % tms::kAlignWords)
+        fail(TM_EINVAL, "device token offsets must be multiples of 32");
+      int32_t c = chain_of_sid[sid];
+      if (c < 0) {
+        c = chain_of_sid[sid] = (int32_t)chain_tokens.size();
+        chain_tokens.push_back(0);
+        chain_len.push_back(0);
+      }
+      chain_idx[k] = c;
+      chain_tokens[c] += L;
+      chain_len[c]++;
       total_runs += r1 - r0;
       words_upper += round_up(L, tms::kAlignWords) + tms::kAlignWords;
     }
-    // stable order by wave
-    std::vector<int64_t> perm(n);
+    const int64_t nchains = (int64_t)chain_tokens.size();
+    std::vector<int64_t> chain_beg(nchains + 1, 0);
+    for (int64_t c = 0; c < nchains; c++) chain_beg[c + 1] = chain_beg[c] + chain_len[c];
+    std::vector<int64_t> perm(n);  // position in chain order -> batch index
     {
-      std::vector<int64_t> cnt(nwaves + 1, 0);
-      for (int64_t k = 0; k < n; k++) cnt[wave[k] + 1]++;
-      for (int32_t w = 0; w < nwaves; w++) cnt[w + 1] += cnt[w];
-      std::vector<int64_t> wbeg(cnt.begin(), cnt.end());
-      for (int64_t k = 0; k < n; k++) perm[cnt[wave[k]]++] = k;
-      cnt.assign(wbeg.begin(), wbeg.end());
-      // capacity (upper bounds)
-      ensure_arena(s, s->arena_used + words_upper);
-      ensure_rows(s, (int64_t)s->rows.size() + n);
-      ensure_runs(s, s->n_runs + total_runs);
-      ensure_table(s, (int64_t)s->rows.size() + n);
-      wait_prev(s, s->stream);
-      // ---- stage tokens and per-entry arrays
-      std::vector<int64_t> doff;
-      const int32_t *tok_base;
-      if (mem == TM_MEM_DEVICE) {  // tokens already in HBM (e.g. produced by the engine)
-        if (stream && (cudaStream_t)stream != s->stream) {  // order after their producer
-          cudaEvent_t ev;
-          ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-          ck(cudaEventRecord(ev, (cudaStream_t)stream), "event");
-          ck(cudaStreamWaitEvent(s->stream, ev, 0), "wait");
-          cudaEventDestroy(ev);
-        }
-        doff.resize(n);
-        for (int64_t k = 0; k < n; k++) {
-          doff[k] = tok_off[perm[k]];
-          if (doff[k] % tms::kAlignWords) fail(TM_EINVAL, "device token offsets must be multiples of 32");
-        }
-        tok_base = tokens;
-      } else {
-        stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
-        tok_base = (const int32_t *)s->dtok.p;
-      }
-      Layout lay;
-      size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
-             o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs);
-      size_t in_bytes = lay.bytes;
-      size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
-             o_sp = lay.add(4 * n), o_crow = lay.add(8 * n), o_cloc = lay.add(4 * n);
-      size_t out_end = lay.bytes;
-      size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n),
-             o_root = lay.add(8 * n), o_plan = lay.add(4 * (size_t)tms::plan_items_ints(n));
-      char *h = (char *)s->pin.need(lay.bytes);
-      char *d = (char *)s->scratch.need(lay.bytes);
-      int32_t *h_sid = (int32_t *)(h + o_sid);
-      int64_t *h_off = (int64_t *)(h + o_off), *h_len = (int64_t *)(h + o_len), *h_roff = (int64_t *)(h + o_roff);
-      int32_t *h_rs = (int32_t *)(h + o_rs), *h_rv = (int32_t *)(h + o_rv);
-      uint8_t *h_ro = (uint8_t *)(h + o_ro);
-      int64_t rr = 0;
-      for (int64_t k = 0; k < n; k++) {
-        int64_t e = perm[k];
-        h_sid[k] = sids[e];
-        h_off[k] = doff[k];
-        h_len[k] = tok_len[e];
-        h_roff[k] = rr;
-        int64_t r0 = run_off[e], r1 = run_off[e + 1];
-        memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
-        memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
-        memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
-        rr += r1 - r0;
-      }
-      h_roff[n] = rr;
-      ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
-      // ---- waves: walk (K1) then commit (K2)
-      for (int32_t w = 0; w < nwaves; w++) {
-        int64_t b0 = wbeg[w], b1 = wbeg[w + 1];
-        Batch b{};
-        b.n = b1 - b0;
-        b.sids = (const int32_t *)(d + o_sid) + b0;
-        b.tok = tok_base;
-        b.off = (const int64_t *)(d + o_off) + b0;
-        b.len = (const int64_t *)(d + o_len) + b0;
-        b.sched = s->sched;
-        b.o_m = (int64_t *)(d + o_m) + b0;
-        b.o_parent = (int64_t *)(d + o_par) + b0;
-        b.o_dup = (int64_t *)(d + o_dup) + b0;
-        b.o_tnext = (int32_t *)(d + o_tn) + b0;
-        b.o_spar = (int32_t *)(d + o_sp) + b0;
-        b.run_off = (const int64_t *)(d + o_roff) + b0;
-        b.run_start = (const int32_t *)(d + o_rs);
-        b.run_origin = (const uint8_t *)(d + o_ro);
-        b.run_version = (const int32_t *)(d + o_rv);
-        b.c_row = (int64_t *)(d + o_crow) + b0;
-        b.c_vb = (int64_t *)(d + o_cvb) + b0;
-        b.c_run0 = (int64_t *)(d + o_cr0) + b0;
-        b.c_firstrun = (int32_t *)(d + o_cfr) + b0;
-        b.c_local = (int32_t *)(d + o_cloc) + b0;
-        if (b.n >= s->plan_min) {
-          ProfScope ps(s, 3, s->stream);
-          ck(tms::launch_plan(s->v, b, s->plan_roots ? (int64_t *)(d + o_root) + b0 : nullptr, (int *)(d + o_plan),
-                              s->stream), "plan");
-        }
-        {
-          ProfScope ps(s, 0, s->stream);
-          ck(tms::launch_walk(s->v, b, s->num_sms, s->stream), "walk");
-        }
-        {
-          ProfScope ps(s, 1, s->stream);
-          ck(tms::launch_commit(s->v, b, s->num_sms, s->stream), "commit");
-        }
-      }
-      // ---- results back
-      char *hout = h + o_m;
-      ck(cudaMemcpyAsync(hout, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, s->stream), "D2H results");
-      int64_t ctr[4];
-      ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
-      mark_done(s, s->stream);
-      ck(cudaStreamSynchronize(s->stream), "record sync");
-      const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
-                    *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
-      const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
-                    *r_loc = (const int32_t *)(h + o_cloc);
-      for (int64_t k = 0; k < n; k++) {
-        int64_t e = perm[k];
-        int32_t sid = sids[e];
-        int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
-        if (r_dup[k] < 0) {
-          if (row != (int64_t)s->rows.size()) fail(TM_ECUDA, "row numbering out of sync");
-          RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
-          rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
-          s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
-          s->rows.push_back(rh);
-          s->sess_rows[sid].push_back(row);
-          s->sess_stored[sid] += L - m;
-        }
-        s->sess_naive[sid] += L;
-        if (out_matched) out_matched[e] = m;
-        if (out_row) out_row[e] = row;
-        if (out_local) out_local[e] = r_loc[k];
-        if (out_parent) out_parent[e] = par;
-        if (out_parent_local) out_parent_local[e] = par >= 0 ? s->rows[par].local : -1;
-        if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
-      }
-      s->arena_used = ctr[0];
-      s->n_runs = ctr[2];
-      if (ctr[1] != (int64_t)s->rows.size()) fail(TM_ECUDA, "row counter out of sync");
+      std::vector<int64_t> cur(chain_beg.begin(), chain_beg.end() - 1);
+      for (int64_t k = 0; k < n; k++) perm[cur[chain_idx[k]]++] = k;
     }
+    std::vector<int64_t> order(nchains);
+    for (int64_t c = 0; c < nchains; c++) order[c] = c;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return chain_tokens[x] > chain_tokens[y]; });
+    // ---- capacity (upper bounds); every entry reserves a row id (batch order)
+    const int64_t row_base = (int64_t)s->rows.size();
+    ensure_arena(s, s->arena_used + words_upper);
+    ensure_rows(s, row_base + n);
+    ensure_runs(s, s->n_runs + total_runs);
+    ensure_table(s, s->n_real_rows + n);
+    wait_prev(s, s->stream);
+    if (mem == TM_MEM_DEVICE && stream && (cudaStream_t)stream != s->stream) {  // order after the producer
+      cudaEvent_t ev;
+      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(ev, (cudaStream_t)stream), "event");
+      ck(cudaStreamWaitEvent(s->stream, ev, 0), "wait");
+      cudaEventDestroy(ev);
+    }
+    // ---- stage tokens and per-entry arrays (chain order)
+    std::vector<int64_t> doff;
+    const int32_t *tok_base;
+    if (mem == TM_MEM_DEVICE) {  // tokens already in HBM (e.g. produced by the engine)
+      doff.resize(n);
+      for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm[k]];
+      tok_base = tokens;
+    } else {
+      stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
+      tok_base = (const int32_t *)s->dtok.p;
+    }
+    Layout lay;
+    size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
+           o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs),
+           o_crow = lay.add(8 * n), o_cbeg = lay.add(8 * (nchains + 1)), o_cord = lay.add(8 * nchains);
+    size_t in_bytes = lay.bytes;
+    size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
+           o_sp = lay.add(4 * n), o_cloc = lay.add(4 * n);
+    size_t out_end = lay.bytes;
+    size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n);
+    char *h = (char *)s->pin.need(lay.bytes);
+    char *d = (char *)s->scratch.need(lay.bytes);
+    int32_t *h_sid = (int32_t *)(h + o_sid);
+    int64_t *h_off = (int64_t *)(h + o_off), *h_len = (int64_t *)(h + o_len), *h_roff = (int64_t *)(h + o_roff);
+    int64_t *h_crow = (int64_t *)(h + o_crow);
+    int32_t *h_rs = (int32_t *)(h + o_rs), *h_rv = (int32_t *)(h + o_rv);
+    uint8_t *h_ro = (uint8_t *)(h + o_ro);
+    int64_t rr = 0;
+    for (int64_t k = 0; k < n; k++) {
+      int64_t e = perm[k];
+      h_sid[k] = sids[e];
+      h_off[k] = doff[k];
+      h_len[k] = tok_len[e];
+      h_roff[k] = rr;
+      h_crow[k] = row_base + e;  // reserved id (batch order)
+      int64_t r0 = run_off[e], r1 = run_off[e + 1];
+      memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
+      memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
+      memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
+      rr += r1 - r0;
+    }
+    h_roff[n] = rr;
+    memcpy(h + o_cbeg, chain_beg.data(), 8 * (nchains + 1));
+    memcpy(h + o_cord, order.data(), 8 * nchains);
+    ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
+    {
+      tms::RecordArgs ra{};
+      Batch &b = ra.b;
+      b.n = n;
+      b.sids = (const int32_t *)(d + o_sid);
+      b.tok = tok_base;
+      b.off = (const int64_t *)(d + o_off);
+      b.len = (const int64_t *)(d + o_len);
+      b.o_m = (int64_t *)(d + o_m);
+      b.o_parent = (int64_t *)(d + o_par);
+      b.o_dup = (int64_t *)(d + o_dup);
+      b.o_tnext = (int32_t *)(d + o_tn);
+      b.o_spar = (int32_t *)(d + o_sp);
+      b.run_off = (const int64_t *)(d + o_roff);
+      b.run_start = (const int32_t *)(d + o_rs);
+      b.run_origin = (const uint8_t *)(d + o_ro);
+      b.run_version = (const int32_t *)(d + o_rv);
+      b.c_row = (int64_t *)(d + o_crow);
+      b.c_vb = (int64_t *)(d + o_cvb);
+      b.c_run0 = (int64_t *)(d + o_cr0);
+      b.c_firstrun = (int32_t *)(d + o_cfr);
+      b.c_local = (int32_t *)(d + o_cloc);
+      ra.chain_beg = (const int64_t *)(d + o_cbeg);
+      ra.chain_order = (const int64_t *)(d + o_cord);
+      ra.nchains = nchains;
+      ra.sched = s->sched;
+      ProfScope ps(s, 1, s->stream);
+      ck(tms::launch_record(s->v, ra, s->num_sms, s->stream), "record");
+    }
+    // ---- results back (chain order), into the host mirror in batch order
+    ck(cudaMemcpyAsync(h + o_crow, d + o_crow, 8 * n, cudaMemcpyDeviceToHost, s->stream), "D2H rows");
+    ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, s->stream), "D2H results");
+    int64_t ctr[4];
+    ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
+    mark_done(s, s->stream);
+    ck(cudaStreamSynchronize(s->stream), "record sync");
+    const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
+                  *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
+    const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
+                  *r_loc = (const int32_t *)(h + o_cloc);
+    std::vector<int64_t> pos(n);  // batch index -> chain position
+    for (int64_t k = 0; k < n; k++) pos[perm[k]] = k;
+    s->rows.resize(row_base + n, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
+    for (int64_t e = 0; e < n; e++) {  // batch order: local ordinals are assigned in it
+      const int64_t k = pos[e];
+      const int32_t sid = sids[e];
+      const int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
+      if (r_dup[k] < 0) {
+        if (row != row_base + e) fail(TM_ECUDA, "row numbering out of sync");
+        RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
+        rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
+        s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
+        s->rows[row] = rh;
+        if (r_loc[k] != (int32_t)s->sess_rows[sid].size()) fail(TM_ECUDA, "session ordinal out of sync");
+        s->sess_rows[sid].push_back(row);
+        s->sess_stored[sid] += L - m;
+        s->n_real_rows++;
+      }
+      s->sess_naive[sid] += L;
+      if (out_matched) out_matched[e] = m;
+      if (out_row) out_row[e] = row;
+      if (out_local) out_local[e] = r_loc[k];
+      if (out_parent) out_parent[e] = par;
+      if (out_parent_local) out_parent_local[e] = par >= 0 ? s->rows[par].local : -1;
+      if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
+    }
+    s->arena_used = ctr[0];
+    s->n_runs = ctr[2];
   });
 }
 
@@ -703,7 +714,7 @@ int tm_rows_total(tm_store *s, int64_t n, const int64_t *rows, int64_t *out_tota
   return guarded(s, [&] {
     int64_t t = 0;
     for (int64_t k = 0; k < n; k++) {
-      if (rows[k] < 0 || rows[k] >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
+      if (!valid_row(s, rows[k])) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
       t += s->rows[rows[k]].len;
     }
     *out_total = t;
@@ -722,7 +733,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
     std::vector<int64_t> tile(n + 1);
     tile[0] = 0;
     for (int64_t k = 0; k < n; k++) {
-      if (rows[k] < 0 || rows[k] >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
+      if (!valid_row(s, rows[k])) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
       int64_t L = s->rows[rows[k]].len;
       out_offsets[k + 1] = out_offsets[k] + L;
       tile[k + 1] = tile[k] + (L + T - 1) / T;
@@ -828,7 +839,7 @@ int tm_session_rows(tm_store *s, int32_t sid, int32_t order, int64_t *out_rows, 
 int tm_row_info(tm_store *s, int64_t row, int32_t *sid, int32_t *local, int64_t *parent, int64_t *matched,
                 int64_t *length) {
   return guarded(s, [&] {
-    if (row < 0 || row >= (int64_t)s->rows.size()) fail(TM_ENOENT, "node " + std::to_string(row) + " not in store");
+    if (!valid_row(s, row)) fail(TM_ENOENT, "node " + std::to_string(row) + " not in store");
     const RowHost &R = s->rows[row];
     if (sid) *sid = R.sid;
     if (local) *local = R.local;
@@ -840,7 +851,7 @@ int tm_row_info(tm_store *s, int64_t row, int32_t *sid, int32_t *local, int64_t 
 
 int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *arena_cap, int64_t *max_depth) {
   return guarded(s, [&] {
-    if (rows) *rows = (int64_t)s->rows.size();
+    if (rows) *rows = s->n_real_rows;
     if (arena_used) *arena_used = s->arena_used;
     if (arena_cap) *arena_cap = s->arena_cap;
     if (max_depth) *max_depth = s->max_depth;
