@@ -435,6 +435,55 @@ struct ExportArgs {
   unsigned long long *resp;  // n (atomicMax), may be null
 };
 
+// Copy / fill helpers for one piece [pa, pb) of an output row starting at word o.  When
+// o is a multiple of 4 every output position is 16-byte congruent with its arena
+// position (arena rows are 128-byte aligned), so the body moves int4 / uchar4 vectors.
+__device__ __forceinline__ void copy_tokens(int32_t *__restrict__ out, const int32_t *__restrict__ src, int64_t o,
+                                            int64_t pa, int64_t pb) {
+  if ((o & 3) == 0) {
+    const int64_t va = (pa + 3) >> 2, vb = pb >> 2;  // int4 body [4va, 4vb)
+    if (va < vb) {
+      for (int64_t p = pa + threadIdx.x; p < 4 * va; p += kExportNT) out[o + p] = src[p];
+      for (int64_t p = 4 * vb + threadIdx.x; p < pb; p += kExportNT) out[o + p] = src[p];
+      const int4 *s4 = reinterpret_cast<const int4 *>(src);
+      int4 *d4 = reinterpret_cast<int4 *>(out + o);
+      int64_t q = va + threadIdx.x;
+      for (; q + 3 * kExportNT < vb; q += 4 * kExportNT) {
+        const int4 x0 = ldg_stream(s4 + q), x1 = ldg_stream(s4 + q + kExportNT);
+        const int4 x2 = ldg_stream(s4 + q + 2 * kExportNT), x3 = ldg_stream(s4 + q + 3 * kExportNT);
+        d4[q] = x0;
+        d4[q + kExportNT] = x1;
+        d4[q + 2 * kExportNT] = x2;
+        d4[q + 3 * kExportNT] = x3;
+      }
+      for (; q < vb; q += kExportNT) d4[q] = ldg_stream(s4 + q);
+      return;
+    }
+  }
+  for (int64_t p = pa + threadIdx.x; p < pb; p += kExportNT) out[o + p] = src[p];
+}
+
+__device__ __forceinline__ void fill_meta(uint8_t *__restrict__ mask, int32_t *__restrict__ vers, int64_t o,
+                                          int64_t xa, int64_t xb, uint8_t org, int32_t ver) {
+  if ((o & 3) == 0) {
+    const int64_t va = (xa + 3) >> 2, vb = xb >> 2;
+    if (va < vb) {
+      for (int64_t p = xa + threadIdx.x; p < 4 * va; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
+      for (int64_t p = 4 * vb + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
+      const uint32_t m4 = 0x01010101u * org;
+      const int4 v4 = make_int4(ver, ver, ver, ver);
+      uint32_t *dm = reinterpret_cast<uint32_t *>(mask + o);
+      int4 *dv = reinterpret_cast<int4 *>(vers + o);
+      for (int64_t q = va + threadIdx.x; q < vb; q += kExportNT) {
+        dm[q] = m4;
+        dv[q] = v4;
+      }
+      return;
+    }
+  }
+  for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
+}
+
 __global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
   for (int64_t t = blockIdx.x; t < e.ntiles; t += gridDim.x) {
     int64_t lo = 0, hi = e.n;  // largest i with tile_off[i] <= t
@@ -449,12 +498,11 @@ __global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
     const int64_t o = e.out_off[i];
     int64_t cur = row, upper = v.row_len[row];
     long long respmax = 0;
-    while (cur >= 0 && upper > a) {
+    while (cur >= 0 && upper > a) {  // ancestors own [m_x, upper)
       const int64_t mx = v.row_m[cur];
       const int64_t pa = max(mx, a), pb = min(upper, b);
       if (pa < pb) {
-        const int32_t *src = v.arena + v.row_vb[cur];
-        for (int64_t p = pa + threadIdx.x; p < pb; p += kExportNT) e.tokens[o + p] = src[p];
+        copy_tokens(e.tokens, v.arena + v.row_vb[cur], o, pa, pb);
         const int64_t r0 = v.row_run0[cur];
         const int nr = v.row_nrun[cur];
         const int64_t lenx = v.row_len[cur];
@@ -469,11 +517,7 @@ __global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
           const int64_t re = (k + 1 < nr) ? v.run_start[r0 + k + 1] : lenx;
           const int64_t xa = max(rs, pa), xb = min(re, pb);
           const uint8_t org = v.run_origin[r0 + k];
-          const int32_t ver = v.run_version[r0 + k];
-          for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) {
-            e.mask[o + p] = org;
-            e.versions[o + p] = ver;
-          }
+          fill_meta(e.mask, e.versions, o, xa, xb, org, v.run_version[r0 + k]);
           if (org == 0 && xb > respmax) respmax = xb;
         }
       }
