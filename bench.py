@@ -255,10 +255,15 @@ def run_c5(args):
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,
         "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * args.steps / elapsed / 1e9,
-        "roofline": {"bound": "hbm+nvlink", "kernel": "k_walk_routed", "achieved": per_gpu_alg * args.steps / elapsed / 1e9,
-                     "peak": peak, "unit": "GB/s", "frac": per_gpu_alg * args.steps / elapsed / 1e9 / peak,
-                     "peak_kind": peak_kind, "traffic": None,
-                     "note": "remote query bytes cross NVLink (770 GB/s measured per direction), history bytes from HBM"},
+        "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
+                     "achieved": (4.0 * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
+                     "peak": 770.0 if world > 1 else peak, "unit": "GB/s",
+                     "frac": ((4.0 * remote_toks / world) / 770.0 if world > 1 else per_gpu_alg / peak)
+                     * args.steps / elapsed / 1e9,
+                     "peak_kind": "measured peer copy per direction (B200_PROFILING.md)" if world > 1 else peak_kind,
+                     "traffic": None,
+                     "note": "N>1: remote query bytes cross NVLink (tools/p2p_probe: SM peer reads 780 GB/s one "
+                             "direction, 670 GB/s both directions at once); history bytes come from local HBM"},
         "gpu_launches": args.steps * 2,
         "clocks": clk.summary(),
     }
