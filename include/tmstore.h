@@ -118,6 +118,15 @@ int tm_export_rows(tm_store *store, int64_t n, const int64_t *rows, int32_t mem_
                    int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
                    void *stream);
 
+/* Canonical NDJSON of rows, formatted on the GPU and byte-identical to
+ * "".join(trajectory_to_line(t) + "\n") (core.py:182-183; the /traj/export payload of
+ * api.py:248-254).  sid_json/sid_off[n+1]: per row, the session id as a JSON string
+ * literal exactly as json.dumps(session_id) prints it, concatenated.  With out == NULL
+ * or cap too small only *out_bytes (the exact size) is set; otherwise the text is
+ * written to `out` (host or device memory per mem_out). */
+int tm_export_ndjson(tm_store *store, int64_t n, const int64_t *rows, const char *sid_json, const int64_t *sid_off,
+                     int32_t mem_out, char *out, int64_t cap, int64_t *out_bytes, void *stream);
+
 /* StorageStats of a session (trie.py:78-87, 184-185; trajectory.py:369-372). */
 int tm_session_stats(tm_store *store, int32_t sid, int64_t *stored, int64_t *naive, int64_t *nrows);
 

@@ -36,6 +36,7 @@ SIGNATURES = {
     "tm_rows_total": (C.c_int, [_P, _I64, _P, _P]),
     "tm_export_rows": (C.c_int, [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "tm_session_stats": (C.c_int, [_P, _I32, _P, _P, _P]),
+    "tm_export_ndjson": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _P, _P]),
     "tm_session_rows": (C.c_int, [_P, _I32, _I32, _P, _I64, _P]),
     "tm_row_info": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "tm_store_stats": (C.c_int, [_P, _P, _P, _P, _P]),

@@ -529,6 +529,153 @@ __global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
 }
 
 // ----------------------------------------------------------------------------------
+// NDJSON formatter (core.py:182-183 trajectory_to_line, byte-identical):
+//   {"session_id":<json literal>,"tokens":[t,...],"loss_mask":[0|1,...],"versions":[v,...]}\n
+// from packed rows.  Pass 1 (k_json_sums) sums the decimal widths of tokens and versions
+// per 4096-position tile; the host turns them into byte offsets; pass 2 (k_json_write)
+// prints every number at its offset (block scan of widths inside the tile).
+constexpr int kJsonNT = 256;
+constexpr int kJsonPer = 16;  // positions per thread: tile = 4096 = export tile
+static_assert(kJsonNT * kJsonPer == kExportTile, "json tile == export tile");
+
+__device__ __forceinline__ int dec_width(int32_t v) {
+  uint32_t u = v < 0 ? (uint32_t)(-(int64_t)v) : (uint32_t)v;
+  int d = 1;
+  while (u >= 10) { u /= 10; d++; }
+  return d + (v < 0);
+}
+
+__device__ __forceinline__ void dec_write(char *dst, int32_t v, int w) {
+  uint32_t u = v < 0 ? (uint32_t)(-(int64_t)v) : (uint32_t)v;
+  for (int i = w - 1; i >= (v < 0 ? 1 : 0); i--) { dst[i] = (char)('0' + u % 10); u /= 10; }
+  if (v < 0) dst[0] = '-';
+}
+
+struct JsonArgs {
+  int64_t n;                 // rows
+  const int64_t *out_off;    // packed row offsets (n+1)
+  const int64_t *tile_off;   // tiles per row prefix (n+1)
+  int64_t ntiles;
+  const int32_t *tokens;
+  const uint8_t *mask;
+  const int32_t *versions;
+  long long *sums;           // pass 1: 2 per tile (token widths, version widths)
+  const long long *toff;     // pass 2: 3 per tile (tokens, mask, versions byte offsets)
+  const long long *roff;     // pass 2: 4 per row (row start, tokens start, mask start, versions start)
+  const char *sid;           // session-id JSON literals, concatenated
+  const int64_t *sid_off;    // n+1
+  char *out;
+};
+
+__device__ __forceinline__ int64_t json_row_of(const JsonArgs &j, int64_t t) {
+  int64_t lo = 0, hi = j.n;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (j.tile_off[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kJsonNT) k_json_sums(JsonArgs j) {
+  __shared__ long long sm[2][kJsonNT / 32];
+  for (int64_t t = blockIdx.x; t < j.ntiles; t += gridDim.x) {
+    const int64_t i = json_row_of(j, t);
+    const int64_t L = j.out_off[i + 1] - j.out_off[i];
+    const int64_t a = (t - j.tile_off[i]) * kExportTile, b = min(a + (int64_t)kExportTile, L);
+    const int64_t base = j.out_off[i];
+    long long st = 0, sv = 0;
+    for (int64_t p = a + threadIdx.x; p < b; p += kJsonNT) {
+      st += dec_width(j.tokens[base + p]);
+      sv += dec_width(j.versions[base + p]);
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      st += __shfl_xor_sync(0xffffffffu, st, d);
+      sv += __shfl_xor_sync(0xffffffffu, sv, d);
+    }
+    if ((threadIdx.x & 31) == 0) { sm[0][threadIdx.x >> 5] = st; sm[1][threadIdx.x >> 5] = sv; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long a0 = 0, a1 = 0;
+      for (int w = 0; w < kJsonNT / 32; w++) { a0 += sm[0][w]; a1 += sm[1][w]; }
+      j.sums[2 * t] = a0;
+      j.sums[2 * t + 1] = a1;
+    }
+    __syncthreads();
+  }
+}
+
+// exclusive block scan of one value per thread
+__device__ __forceinline__ long long block_excl_scan(long long x, long long *sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long y = x;
+  for (int d = 1; d < 32; d <<= 1) {
+    long long z = __shfl_up_sync(0xffffffffu, y, d);
+    if (lane >= d) y += z;
+  }
+  if (lane == 31) sm[w] = y;
+  __syncthreads();
+  long long pre = 0;
+  for (int k = 0; k < w; k++) pre += sm[k];
+  __syncthreads();
+  return pre + y - x;
+}
+
+__device__ __forceinline__ void put(char *dst, const char *s, int n) {
+  for (int k = 0; k < n; k++) dst[k] = s[k];
+}
+
+__global__ void __launch_bounds__(kJsonNT) k_json_write(JsonArgs j) {
+  __shared__ long long sm[kJsonNT / 32];
+  for (int64_t t = blockIdx.x; t < j.ntiles; t += gridDim.x) {
+    const int64_t i = json_row_of(j, t);
+    const int64_t L = j.out_off[i + 1] - j.out_off[i];
+    const int64_t a = (t - j.tile_off[i]) * kExportTile, b = min(a + (int64_t)kExportTile, L);
+    const int64_t base = j.out_off[i];
+    // this thread's consecutive positions [pa, pb)
+    const int64_t pa = a + (int64_t)threadIdx.x * kJsonPer, pb = min(pa + kJsonPer, b);
+    for (int sec = 0; sec < 2; sec++) {  // 0 tokens, 1 versions
+      const int32_t *vals = sec ? j.versions : j.tokens;
+      long long mine = 0;
+      for (int64_t p = pa; p < pb; p++) mine += dec_width(vals[base + p]) + 1;
+      long long off = j.toff[3 * t + (sec ? 2 : 0)] + block_excl_scan(mine, sm);
+      for (int64_t p = pa; p < pb; p++) {
+        const int32_t v = vals[base + p];
+        const int w = dec_width(v);
+        dec_write(j.out + off, v, w);
+        if (p + 1 < L) j.out[off + w] = ',';
+        off += w + 1;
+      }
+    }
+    const long long moff = j.toff[3 * t + 1];
+    for (int64_t p = a + threadIdx.x; p < b; p += kJsonNT) {
+      j.out[moff + 2 * (p - a)] = j.mask[base + p] ? '1' : '0';
+      if (p + 1 < L) j.out[moff + 2 * (p - a) + 1] = ',';
+    }
+    if (t == j.tile_off[i] && threadIdx.x == 0) {  // fixed parts of the row
+      const long long r0 = j.roff[4 * i], ts = j.roff[4 * i + 1], ms = j.roff[4 * i + 2], vs = j.roff[4 * i + 3];
+      const int64_t s0 = j.sid_off[i], sl = j.sid_off[i + 1] - s0;
+      put(j.out + r0, "{\"session_id\":", 14);
+      put(j.out + r0 + 14, j.sid + s0, (int)sl);
+      put(j.out + ts - 11, ",\"tokens\":[", 11);
+      put(j.out + ms - 15, "],\"loss_mask\":[", 15);
+      put(j.out + vs - 14, "],\"versions\":[", 14);
+      const long long vend = vs + (j.roff[4 * (i + 1)] - 3 - vs);
+      put(j.out + vend, "]}\n", 3);
+    }
+  }
+}
+
+cudaError_t launch_json(const JsonArgsHost &h, int pass, int num_sms, cudaStream_t s) {
+  JsonArgs j{h.n, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions, (long long *)h.sums,
+             (const long long *)h.toff, (const long long *)h.roff, h.sid, h.sid_off, h.out};
+  int64_t grid = h.ntiles < (int64_t)num_sms * 8 ? h.ntiles : (int64_t)num_sms * 8;
+  if (grid < 1) return cudaSuccess;
+  if (pass == 1) k_json_sums<<<(int)grid, kJsonNT, 0, s>>>(j);
+  else k_json_write<<<(int)grid, kJsonNT, 0, s>>>(j);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------
 __global__ void k_rehash(DevView v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval, int64_t ocap) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < ocap; s += (int64_t)gridDim.x * blockDim.x) {
     if (ok0[s] != kEmpty) ht_insert(v, ok0[s], ok1[s], oval[s]);

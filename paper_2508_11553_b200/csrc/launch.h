@@ -21,6 +21,21 @@ struct ExportArgsHost {
 };
 
 // fills b.root (if root != null) and b.bucket_items (plan_items_ints(n) ints); counts go to b.sched
+struct JsonArgsHost {
+  int64_t n;
+  const int64_t *out_off, *tile_off;
+  int64_t ntiles;
+  const int32_t *tokens;
+  const uint8_t *mask;
+  const int32_t *versions;
+  int64_t *sums;
+  const int64_t *toff, *roff;
+  const char *sid;
+  const int64_t *sid_off;
+  char *out;
+};
+cudaError_t launch_json(const JsonArgsHost &h, int pass, int num_sms, cudaStream_t s);
+
 cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *items, cudaStream_t s);
 int64_t plan_items_ints(int64_t n);
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);

@@ -792,6 +792,110 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
   });
 }
 
+int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *sid_json, const int64_t *sid_off,
+                     int32_t mem_out, char *out, int64_t cap, int64_t *out_bytes, void *stream) {
+  return guarded(s, [&] {
+    if (n < 0) fail(TM_EINVAL, "negative batch size");
+    if (mem_out != TM_MEM_HOST && mem_out != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
+    *out_bytes = 0;
+    if (n == 0) return;
+    const int64_t T = tms::export_tile_tokens();
+    std::vector<int64_t> off(n + 1), tile(n + 1);
+    off[0] = tile[0] = 0;
+    for (int64_t k = 0; k < n; k++) {
+      if (!valid_row(s, rows[k])) fail(TM_ENOENT, "node " + std::to_string(rows[k]) + " not in store");
+      const int64_t L = s->rows[rows[k]].len;
+      off[k + 1] = off[k] + L;
+      tile[k + 1] = tile[k] + (L + T - 1) / T;
+    }
+    const int64_t total = off[n], ntiles = tile[n];
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    wait_prev(s, st);
+    Layout lay;
+    size_t o_rows = lay.add(8 * n), o_off = lay.add(8 * (n + 1)), o_tile = lay.add(8 * (n + 1));
+    size_t in_bytes = lay.bytes;
+    size_t o_tok = lay.add(4 * total), o_msk = lay.add(total), o_ver = lay.add(4 * total), o_sums = lay.add(16 * ntiles),
+           o_toff = lay.add(24 * ntiles), o_roff = lay.add(32 * (n + 1)), o_sidoff = lay.add(8 * (n + 1)),
+           o_sid = lay.add((size_t)sid_off[n]);
+    char *d = (char *)s->scratch.need(lay.bytes);
+    char *h = (char *)s->pin.need(std::max(in_bytes, (size_t)16 * ntiles));
+    memcpy(h + o_rows, rows, 8 * n);
+    memcpy(h + o_off, off.data(), 8 * (n + 1));
+    memcpy(h + o_tile, tile.data(), 8 * (n + 1));
+    ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D ndjson plan");
+    tms::ExportArgsHost e{};
+    e.n = n;
+    e.rows = (const int64_t *)(d + o_rows);
+    e.out_off = (const int64_t *)(d + o_off);
+    e.tile_off = (const int64_t *)(d + o_tile);
+    e.ntiles = ntiles;
+    e.tokens = (int32_t *)(d + o_tok);
+    e.mask = (uint8_t *)(d + o_msk);
+    e.versions = (int32_t *)(d + o_ver);
+    e.resp = nullptr;
+    {
+      ProfScope ps(s, 2, st);
+      ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
+    }
+    tms::JsonArgsHost j{};
+    j.n = n;
+    j.out_off = e.out_off;
+    j.tile_off = e.tile_off;
+    j.ntiles = ntiles;
+    j.tokens = e.tokens;
+    j.mask = e.mask;
+    j.versions = e.versions;
+    j.sums = (int64_t *)(d + o_sums);
+    ck(tms::launch_json(j, 1, s->num_sms, st), "json pass 1");
+    std::vector<int64_t> sums(2 * ntiles);
+    ck(cudaMemcpyAsync(h, j.sums, 16 * ntiles, cudaMemcpyDeviceToHost, st), "D2H json sums");
+    ck(cudaStreamSynchronize(st), "json sync");
+    memcpy(sums.data(), h, 16 * ntiles);
+    // byte layout of every row and tile
+    std::vector<int64_t> toff(3 * ntiles), roff(4 * (n + 1));
+    int64_t pos = 0;
+    for (int64_t i = 0; i < n; i++) {
+      const int64_t L = off[i + 1] - off[i], kl = sid_off[i + 1] - sid_off[i];
+      int64_t ts_sum = 0, vs_sum = 0;
+      for (int64_t t2 = tile[i]; t2 < tile[i + 1]; t2++) { ts_sum += sums[2 * t2]; vs_sum += sums[2 * t2 + 1]; }
+      const int64_t r0 = pos, ts = r0 + 14 + kl + 11, ms = ts + ts_sum + L - 1 + 15, vs = ms + 2 * L - 1 + 14;
+      roff[4 * i] = r0; roff[4 * i + 1] = ts; roff[4 * i + 2] = ms; roff[4 * i + 3] = vs;
+      int64_t at = ts, av = vs;
+      for (int64_t t2 = tile[i]; t2 < tile[i + 1]; t2++) {
+        const int64_t a = (t2 - tile[i]) * T, cnt = std::min(T, L - a);
+        toff[3 * t2] = at; toff[3 * t2 + 1] = ms + 2 * a; toff[3 * t2 + 2] = av;
+        at += sums[2 * t2] + cnt;
+        av += sums[2 * t2 + 1] + cnt;
+      }
+      pos = vs + vs_sum + L - 1 + 3;
+    }
+    roff[4 * n] = pos;
+    *out_bytes = pos;
+    if (!out || cap < pos) { mark_done(s, st); return; }  // size query
+    char *h2 = (char *)s->pin.need(24 * ntiles + 32 * (n + 1) + 8 * (n + 1) + sid_off[n] + 1024);
+    size_t a0 = 0, a1 = (24 * ntiles + 255) / 256 * 256, a2 = a1 + (32 * (n + 1) + 255) / 256 * 256,
+           a3 = a2 + (8 * (n + 1) + 255) / 256 * 256;
+    memcpy(h2 + a0, toff.data(), 24 * ntiles);
+    memcpy(h2 + a1, roff.data(), 32 * (n + 1));
+    memcpy(h2 + a2, sid_off, 8 * (n + 1));
+    memcpy(h2 + a3, sid_json, sid_off[n]);
+    ck(cudaMemcpyAsync(d + o_toff, h2 + a0, 24 * ntiles, cudaMemcpyHostToDevice, st), "H2D json");
+    ck(cudaMemcpyAsync(d + o_roff, h2 + a1, 32 * (n + 1), cudaMemcpyHostToDevice, st), "H2D json");
+    ck(cudaMemcpyAsync(d + o_sidoff, h2 + a2, 8 * (n + 1), cudaMemcpyHostToDevice, st), "H2D json");
+    if (sid_off[n]) ck(cudaMemcpyAsync(d + o_sid, h2 + a3, sid_off[n], cudaMemcpyHostToDevice, st), "H2D json");
+    char *text = (char *)s->dtok.need((size_t)pos);  // token staging doubles as the text buffer here
+    j.toff = (const int64_t *)(d + o_toff);
+    j.roff = (const int64_t *)(d + o_roff);
+    j.sid = (const char *)(d + o_sid);
+    j.sid_off = (const int64_t *)(d + o_sidoff);
+    j.out = mem_out == TM_MEM_DEVICE ? out : text;
+    ck(tms::launch_json(j, 2, s->num_sms, st), "json pass 2");
+    if (mem_out == TM_MEM_HOST) ck(cudaMemcpyAsync(out, text, pos, cudaMemcpyDeviceToHost, st), "D2H json");
+    mark_done(s, st);
+    ck(cudaStreamSynchronize(st), "json sync");
+  });
+}
+
 int tm_session_stats(tm_store *s, int32_t sid, int64_t *stored, int64_t *naive, int64_t *nrows) {
   return guarded(s, [&] {
     if (sid < 0 || sid >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sid));

@@ -245,6 +245,29 @@ class DeviceStore:
                                       _ptr(resp), None))
         return Packed(off, tok, msk, ver, resp)
 
+    def export_ndjson(self, rows, session_ids) -> bytes:
+        """Canonical NDJSON lines of ``rows`` (one per row, "\n"-terminated), formatted on
+        the GPU; byte-identical to trajectory_to_line (core.py:182-183).  ``session_ids``:
+        the session id string of each row."""
+        import json
+
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = len(rows)
+        if n == 0:
+            return b""
+        lits = [json.dumps(s).encode("ascii") for s in session_ids]
+        sid_off = np.zeros(n + 1, np.int64)
+        np.cumsum([len(x) for x in lits], out=sid_off[1:])
+        sid = np.frombuffer(b"".join(lits) or b"\0", np.uint8)
+        size = C.c_int64()
+        check(self.lib.tm_export_ndjson(self.h, n, _ptr(rows), _ptr(sid), _ptr(sid_off), TM_MEM_HOST, None, 0,
+                                        C.byref(size), None))
+        out = np.empty(max(size.value, 1), np.uint8)
+        got = C.c_int64()
+        check(self.lib.tm_export_ndjson(self.h, n, _ptr(rows), _ptr(sid), _ptr(sid_off), TM_MEM_HOST, _ptr(out),
+                                        size.value, C.byref(got), None))
+        return out[: got.value].tobytes()
+
     def export_device(self, rows, stream=None) -> Packed:
         """Packed trajectories left on the GPU as torch tensors (trainer handoff)."""
         import torch

@@ -77,10 +77,14 @@ def main():
             t0 = time.perf_counter()
             ph = store.export(rows)
             t_exp_host = time.perf_counter() - t0
+            names = [f"sess-{int(sids[k])}" for k in range(len(rows))] if cfg != 1 else ["sess-0"] * len(rows)
+            t0 = time.perf_counter()
+            text = store.export_ndjson(rows, names)
+            t_json = time.perf_counter() - t0
             if rep == 0:
                 continue  # warm-up
             cur = dict(t_rec=t_rec, walk_ms=walk_ms, commit_ms=commit_ms, commit_n=commit_n, t_exp=t_exp, exp_ms=exp_ms,
-                       t_exp_host=t_exp_host)
+                       t_exp_host=t_exp_host, t_json=t_json)
             for k, v in cur.items():
                 best[k] = min(best.get(k, v), v)
         store.close()
@@ -101,7 +105,9 @@ def main():
                        "device_GBps": exp_bytes / best["exp_ms"] / 1e6,
                        "frac_of_peak": exp_bytes / best["exp_ms"] / 1e6 / peak,
                        "device_call_ms": 1e3 * best["t_exp"], "host_call_ms": 1e3 * best["t_exp_host"],
-                       "host_tokens_per_s": n_out / best["t_exp_host"]},
+                       "host_tokens_per_s": n_out / best["t_exp_host"],
+                       "ndjson_call_ms": 1e3 * best["t_json"], "ndjson_bytes": len(text),
+                       "ndjson_tokens_per_s": n_out / best["t_json"]},
         }
         if not args.no_cpu:
             ora = CRadixStore()
@@ -114,9 +120,21 @@ def main():
                 for k in ora.lex_rows(s):
                     n_exp += len(ora.export_row(s, int(k))[0])
             t_cpu_exp = time.perf_counter() - t0
+            # reference-format JSON on the CPU (json.dumps, as trajectory_to_line does) for a sample
+            import json as _json
+            t0 = time.perf_counter()
+            nj = 0
+            for k in range(min(len(rows), 200)):
+                a, b = ph.offsets[k], ph.offsets[k + 1]
+                _json.dumps({"session_id": names[k], "tokens": ph.tokens[a:b].tolist(),
+                             "loss_mask": ph.loss_mask[a:b].tolist(), "versions": ph.versions[a:b].tolist()},
+                            separators=(",", ":"))
+                nj += b - a
+            t_cpu_json = time.perf_counter() - t0
             line["cpu_port"] = {"cores": cores, "record_s": t_cpu_rec, "records_per_s": len(lens) / t_cpu_rec,
                                 "export_tokens_per_s": n_exp / t_cpu_exp,
-                                "export_sample": f"{min(wl.n_sessions, 200)} sessions, 1 thread (ctypes per row)"}
+                                "export_sample": f"{min(wl.n_sessions, 200)} sessions, 1 thread (ctypes per row)",
+                                "json_dumps_tokens_per_s": nj / t_cpu_json}
             ora.close()
         print(json.dumps(line), flush=True)
 
