@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -120,7 +121,7 @@ struct tm_store {
   std::vector<int64_t> sess_stored, sess_naive;
   int64_t max_depth = 0;
   DevBytes scratch, dtok;
-  PinBytes pin, ptok;
+  PinBytes pin, ptok, d2h_slot[2];
   // Device-memory match batches are read-only: they may overlap each other (a batch's
   // planner and grid ramp-up hide under the previous batch's tail) but not a mutation.
   // Each in-flight batch uses one slot (scratch + scheduler block + completion event).
@@ -254,6 +255,43 @@ struct ProfScope {
 };
 
 // exclusive operations (record, export, host-buffer match) wait for everything before them
+// Device -> pageable host copy of a large result: the driver stages pageable copies
+// through a small bounce buffer (measured ~1.5-5 GB/s here), so pipeline 64 MB chunks
+// through two pinned slots and spread the pinned->pageable memcpy over host threads.
+void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaStream_t st) {
+  constexpr int64_t CH = 64ll << 20;
+  if (bytes <= (8ll << 20)) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "D2H sync");
+    return;
+  }
+  const int nthreads = std::max(1, std::min(8, (int)std::thread::hardware_concurrency()));
+  const int64_t nch = (bytes + CH - 1) / CH;
+  cudaEvent_t ev[2];
+  for (auto &e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  auto issue = [&](int64_t c) {
+    const int64_t off = c * CH, len = std::min(CH, bytes - off);
+    char *slot = (char *)s->d2h_slot[c & 1].need(CH);
+    ck(cudaMemcpyAsync(slot, (const char *)src + off, len, cudaMemcpyDeviceToHost, st), "D2H chunk");
+    ck(cudaEventRecord(ev[c & 1], st), "event");
+  };
+  issue(0);
+  for (int64_t c = 0; c < nch; c++) {
+    ck(cudaEventSynchronize(ev[c & 1]), "D2H wait");
+    if (c + 1 < nch) issue(c + 1);
+    const int64_t off = c * CH, len = std::min(CH, bytes - off);
+    const char *slot = (const char *)s->d2h_slot[c & 1].p;
+    std::vector<std::thread> th;
+    const int64_t part = (len + nthreads - 1) / nthreads;
+    for (int k = 0; k < nthreads; k++) {
+      const int64_t a = k * part, b = std::min(len, a + part);
+      if (a < b) th.emplace_back([=] { memcpy((char *)dst + off + a, slot + a, (size_t)(b - a)); });
+    }
+    for (auto &x : th) x.join();
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+}
+
 bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->rows.size() && s->rows[r].sid >= 0; }
 
 void wait_prev(tm_store *s, cudaStream_t st) {
@@ -780,9 +818,9 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
     }
     if (mem_out == TM_MEM_HOST) {
-      if (out_tokens) ck(cudaMemcpyAsync(out_tokens, e.tokens, 4 * total, cudaMemcpyDeviceToHost, st), "D2H tokens");
-      if (out_mask) ck(cudaMemcpyAsync(out_mask, e.mask, total, cudaMemcpyDeviceToHost, st), "D2H mask");
-      if (out_versions) ck(cudaMemcpyAsync(out_versions, e.versions, 4 * total, cudaMemcpyDeviceToHost, st), "D2H versions");
+      if (out_tokens) d2h_pageable(s, out_tokens, e.tokens, 4 * total, st);
+      if (out_mask) d2h_pageable(s, out_mask, e.mask, total, st);
+      if (out_versions) d2h_pageable(s, out_versions, e.versions, 4 * total, st);
       if (out_resp_start) ck(cudaMemcpyAsync(out_resp_start, e.resp, 8 * n, cudaMemcpyDeviceToHost, st), "D2H resp");
       mark_done(s, st);
       ck(cudaStreamSynchronize(st), "export sync");
@@ -890,7 +928,7 @@ int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *si
     j.sid_off = (const int64_t *)(d + o_sidoff);
     j.out = mem_out == TM_MEM_DEVICE ? out : text;
     ck(tms::launch_json(j, 2, s->num_sms, st), "json pass 2");
-    if (mem_out == TM_MEM_HOST) ck(cudaMemcpyAsync(out, text, pos, cudaMemcpyDeviceToHost, st), "D2H json");
+    if (mem_out == TM_MEM_HOST) d2h_pageable(s, out, text, pos, st);
     mark_done(s, st);
     ck(cudaStreamSynchronize(st), "json sync");
   });

@@ -245,7 +245,7 @@ class DeviceStore:
                                       _ptr(resp), None))
         return Packed(off, tok, msk, ver, resp)
 
-    def export_ndjson(self, rows, session_ids) -> bytes:
+    def export_ndjson(self, rows, session_ids, *, as_array: bool = False):
         """Canonical NDJSON lines of ``rows`` (one per row, "\n"-terminated), formatted on
         the GPU; byte-identical to trajectory_to_line (core.py:182-183).  ``session_ids``:
         the session id string of each row."""
@@ -254,7 +254,7 @@ class DeviceStore:
         rows = np.ascontiguousarray(rows, np.int64)
         n = len(rows)
         if n == 0:
-            return b""
+            return np.zeros(0, np.uint8) if as_array else b""
         lits = [json.dumps(s).encode("ascii") for s in session_ids]
         sid_off = np.zeros(n + 1, np.int64)
         np.cumsum([len(x) for x in lits], out=sid_off[1:])
@@ -266,7 +266,7 @@ class DeviceStore:
         got = C.c_int64()
         check(self.lib.tm_export_ndjson(self.h, n, _ptr(rows), _ptr(sid), _ptr(sid_off), TM_MEM_HOST, _ptr(out),
                                         size.value, C.byref(got), None))
-        return out[: got.value].tobytes()
+        return out[: got.value] if as_array else out[: got.value].tobytes()
 
     def export_device(self, rows, stream=None) -> Packed:
         """Packed trajectories left on the GPU as torch tensors (trainer handoff)."""

@@ -79,7 +79,7 @@ def main():
             t_exp_host = time.perf_counter() - t0
             names = [f"sess-{int(sids[k])}" for k in range(len(rows))] if cfg != 1 else ["sess-0"] * len(rows)
             t0 = time.perf_counter()
-            text = store.export_ndjson(rows, names)
+            text = store.export_ndjson(rows, names, as_array=True)
             t_json = time.perf_counter() - t0
             if rep == 0:
                 continue  # warm-up
