@@ -172,6 +172,12 @@ int tm_route_prepare(tm_store *store, void *region, int64_t n, const int64_t *of
 int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
                     void *stream);
 
+/* Snapshot / restore (the reference store is in-memory only, trajectory.py:128): write
+ * the arena, row table, metadata runs, session counters and the host row mirror to a
+ * file; load them into an EMPTY store (any GPU), rebuilding the branch index. */
+int tm_store_save(tm_store *store, const char *path);
+int tm_store_load(tm_store *store, const char *path);
+
 /* Per-kernel CUDA-event timing for benchmarks.  tm_profile_begin starts recording an
  * event pair around every launch; tm_profile_end(kind) waits for them and returns the
  * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */

@@ -43,6 +43,8 @@ SIGNATURES = {
     "tm_store_stream": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
+    "tm_store_save": (C.c_int, [_P, C.c_char_p]),
+    "tm_store_load": (C.c_int, [_P, C.c_char_p]),
     "tm_route_desc_bytes": (C.c_int, [_P]),
     "tm_shared_alloc": (C.c_int, [_P, _I64, _P]),
     "tm_shared_free": (C.c_int, [_P, _P]),

@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
           const long long base = words ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)words) : 0;
           b.c_vb[e] = base - (m / kAlignWords) * kAlignWords;
           b.c_run0[e] = runs ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)runs) : 0;
-        } else {
+        } else {  // re-recorded sequence: its reserved slot stays an empty hole
+          v.row_len[b.c_row[e]] = 0;
+          v.row_sess[b.c_row[e]] = -1;
           b.c_row[e] = b.o_dup[e];
           b.c_vb[e] = 0;
           b.c_run0[e] = 0;
@@ -682,6 +684,22 @@ __global__ void k_rehash(DevView v, const uint64_t *ok0, const uint64_t *ok1, co
   }
 }
 
+// Rebuild the branch index from the row table (snapshot restore): every row's key is
+// (parent or ROOT|session, matched, its first own token), or the terminal key for rows
+// that end where they branch off (prefix rows).  Row slots reserved by an entry that
+// re-recorded an existing sequence are holes (row_len 0, written by k_record).
+__global__ void k_rebuild_index(DevView v, int64_t nrows) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t L = v.row_len[r];
+    if (L <= 0) continue;
+    const int64_t m = v.row_m[r], par = v.row_parent[r];
+    const int32_t sid = v.row_sess[r];
+    const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
+    if (L > m) ht_insert(v, owner, dt_key(m, v.arena[v.row_vb[r] + m], false), r);
+    else ht_insert(v, owner, dt_key(m, 0, true), r);
+  }
+}
+
 __global__ void k_fill_u64(uint64_t *p, int64_t n, uint64_t val) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) p[s] = val;
 }
@@ -770,6 +788,11 @@ cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s) {
   k_rehash<<<1024, 256, 0, s>>>(v, ok0, ok1, oval, ocap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s) {
+  if (nrows > 0) k_rebuild_index<<<1024, 256, 0, s>>>(v, nrows);
   return cudaGetLastError();
 }
 

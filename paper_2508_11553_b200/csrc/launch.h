@@ -44,6 +44,7 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &e, int num_sms, cudaStream_t s);
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s);
+cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
 int export_tile_tokens();
 cudaError_t launch_route(char *region, int nranks, cudaStream_t s);

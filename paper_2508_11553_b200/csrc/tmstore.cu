@@ -391,6 +391,50 @@ void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, 
 
 }  // namespace
 
+// ---- snapshot / restore -----------------------------------------------------------------
+namespace {
+constexpr char kMagic[8] = {'T', 'M', 'S', 'T', 'O', 'R', 'E', '1'};
+
+struct FileW {
+  FILE *f;
+  void put(const void *p, size_t n) {
+    if (n && fwrite(p, 1, n, f) != n) fail(TM_EINVAL, "snapshot write failed");
+  }
+  template <class T> void val(const T &x) { put(&x, sizeof(T)); }
+};
+struct FileR {
+  FILE *f;
+  void get(void *p, size_t n) {
+    if (n && fread(p, 1, n, f) != n) fail(TM_EINVAL, "snapshot truncated");
+  }
+  template <class T> T val() { T x; get(&x, sizeof(T)); return x; }
+};
+
+template <class T>
+void save_dev(tm_store *s, FileW &w, const T *d, int64_t n) {
+  const int64_t bytes = (int64_t)sizeof(T) * n;
+  constexpr int64_t CH = 64ll << 20;
+  char *h = (char *)s->pin.need(CH);
+  for (int64_t off = 0; off < bytes; off += CH) {
+    const int64_t len = std::min(CH, bytes - off);
+    ck(cudaMemcpy(h, (const char *)d + off, len, cudaMemcpyDeviceToHost), "snapshot D2H");
+    w.put(h, len);
+  }
+}
+
+template <class T>
+void load_dev(tm_store *s, FileR &r, T *d, int64_t n) {
+  const int64_t bytes = (int64_t)sizeof(T) * n;
+  constexpr int64_t CH = 64ll << 20;
+  char *h = (char *)s->pin.need(CH);
+  for (int64_t off = 0; off < bytes; off += CH) {
+    const int64_t len = std::min(CH, bytes - off);
+    r.get(h, len);
+    ck(cudaMemcpy((char *)d + off, h, len, cudaMemcpyHostToDevice), "restore H2D");
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char *tm_last_error(void) { return g_err.c_str(); }
@@ -1082,6 +1126,100 @@ int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer
     }
     ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
     slot->used = true;
+  });
+}
+
+
+int tm_store_save(tm_store *s, const char *path) {
+  return guarded(s, [&] {
+    wait_prev(s, s->stream);
+    ck(cudaStreamSynchronize(s->stream), "snapshot sync");
+    FILE *f = fopen(path, "wb");
+    if (!f) fail(TM_EINVAL, std::string("cannot open ") + path);
+    FileW w{f};
+    try {
+      w.put(kMagic, 8);
+      const int64_t nrows = (int64_t)s->rows.size();
+      w.val(s->n_sess); w.val(nrows); w.val(s->n_real_rows); w.val(s->arena_used); w.val(s->n_runs); w.val(s->max_depth);
+      w.put(s->rows.data(), sizeof(RowHost) * nrows);
+      for (int64_t i = 0; i < s->n_sess; i++) {
+        const int64_t k = (int64_t)s->sess_rows[i].size();
+        w.val(s->sess_stored[i]); w.val(s->sess_naive[i]); w.val(k);
+        w.put(s->sess_rows[i].data(), 8 * k);
+      }
+      save_dev(s, w, s->v.arena, s->arena_used);
+      save_dev(s, w, s->v.row_vb, nrows); save_dev(s, w, s->v.row_m, nrows); save_dev(s, w, s->v.row_len, nrows);
+      save_dev(s, w, s->v.row_parent, nrows); save_dev(s, w, s->v.row_sess, nrows);
+      save_dev(s, w, s->v.row_local, nrows); save_dev(s, w, s->v.row_depth, nrows);
+      save_dev(s, w, s->v.row_run0, nrows); save_dev(s, w, s->v.row_nrun, nrows);
+      save_dev(s, w, s->v.run_start, s->n_runs); save_dev(s, w, s->v.run_version, s->n_runs);
+      save_dev(s, w, s->v.run_origin, s->n_runs);
+      save_dev(s, w, s->v.s_nrows, s->n_sess); save_dev(s, w, s->v.s_stored, s->n_sess);
+      save_dev(s, w, s->v.s_naive, s->n_sess);
+      w.put(kMagic, 8);
+    } catch (...) {
+      fclose(f);
+      throw;
+    }
+    if (fclose(f)) fail(TM_EINVAL, "snapshot close failed");
+  });
+}
+
+int tm_store_load(tm_store *s, const char *path) {
+  return guarded(s, [&] {
+    if (s->n_sess || !s->rows.empty()) fail(TM_EINVAL, "restore needs an empty store");
+    FILE *f = fopen(path, "rb");
+    if (!f) fail(TM_ENOENT, std::string("cannot open ") + path);
+    FileR r{f};
+    try {
+      char m[8];
+      r.get(m, 8);
+      if (memcmp(m, kMagic, 8)) fail(TM_EINVAL, "not a tmstore snapshot");
+      const int64_t nsess = r.val<int64_t>(), nrows = r.val<int64_t>(), nreal = r.val<int64_t>();
+      const int64_t aused = r.val<int64_t>(), nruns = r.val<int64_t>(), maxd = r.val<int64_t>();
+      ensure_sessions(s, nsess);
+      ensure_rows(s, nrows);
+      ensure_runs(s, nruns);
+      ensure_arena(s, aused);
+      ensure_table(s, nreal);
+      s->rows.resize(nrows);
+      r.get(s->rows.data(), sizeof(RowHost) * nrows);
+      s->sess_rows.assign(nsess, {});
+      s->sess_stored.assign(nsess, 0);
+      s->sess_naive.assign(nsess, 0);
+      for (int64_t i = 0; i < nsess; i++) {
+        s->sess_stored[i] = r.val<int64_t>();
+        s->sess_naive[i] = r.val<int64_t>();
+        const int64_t k = r.val<int64_t>();
+        s->sess_rows[i].resize(k);
+        r.get(s->sess_rows[i].data(), 8 * k);
+      }
+      load_dev(s, r, s->v.arena, aused);
+      load_dev(s, r, s->v.row_vb, nrows); load_dev(s, r, s->v.row_m, nrows); load_dev(s, r, s->v.row_len, nrows);
+      load_dev(s, r, s->v.row_parent, nrows); load_dev(s, r, s->v.row_sess, nrows);
+      load_dev(s, r, s->v.row_local, nrows); load_dev(s, r, s->v.row_depth, nrows);
+      load_dev(s, r, s->v.row_run0, nrows); load_dev(s, r, s->v.row_nrun, nrows);
+      load_dev(s, r, s->v.run_start, nruns); load_dev(s, r, s->v.run_version, nruns);
+      load_dev(s, r, s->v.run_origin, nruns);
+      load_dev(s, r, s->v.s_nrows, nsess); load_dev(s, r, s->v.s_stored, nsess);
+      load_dev(s, r, s->v.s_naive, nsess);
+      r.get(m, 8);
+      if (memcmp(m, kMagic, 8)) fail(TM_EINVAL, "snapshot trailer missing");
+      s->n_sess = nsess;
+      s->n_real_rows = nreal;
+      s->arena_used = aused;
+      s->n_runs = nruns;
+      s->max_depth = maxd;
+      const int64_t ctr[4] = {aused, nrows, nruns, 0};
+      ck(cudaMemcpy(s->v.ctr, ctr, sizeof(ctr), cudaMemcpyHostToDevice), "ctr");
+      // the branch index is derived state: rebuild it from the row table
+      ck(tms::launch_rebuild_index(s->v, nrows, s->stream), "rebuild index");
+      ck(cudaStreamSynchronize(s->stream), "restore sync");
+    } catch (...) {
+      fclose(f);
+      throw;
+    }
+    fclose(f);
   });
 }
 

@@ -119,6 +119,17 @@ class DeviceStore:
         check(self.lib.tm_store_stream(self.h, C.byref(s)))
         return s.value or 0
 
+    def save(self, path: str) -> None:
+        """Snapshot the store (arena, rows, runs, counters) to ``path``."""
+        check(self.lib.tm_store_save(self.h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "DeviceStore":
+        """A new store on ``device`` restored from a snapshot (branch index rebuilt)."""
+        st = cls(device)
+        check(st.lib.tm_store_load(st.h, str(path).encode()))
+        return st
+
     KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3}
 
     def profile_begin(self):
