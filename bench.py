@@ -120,6 +120,15 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def c4_config(args, world, wl, mixed=None):
+    """The config object both arms print (the driver compares the arms on it)."""
+    return {"workload": "c4" if mixed is None else "c5-shard", "sessions": args.sessions,
+            "history_tokens": args.hist if mixed is None else f"log-uniform {mixed}",
+            "batch_queries": args.queries, "ext_frac": 0.75, "parallelism": f"session-shard x{world}",
+            "l2": "inputs larger than L2 (arena %.2f GB + queries %.2f GB per rank)" % (
+                wl.hist_off[-1] * 4 / 1e9, wl.q_off[-1] * 4 / 1e9)}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -139,8 +148,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "c4" if mixed is None else "c5-shard", "sessions": args.sessions,
-                   "history_tokens": args.hist if mixed is None else f"log-uniform {mixed}", "batch_queries": args.queries},
+        "config": c4_config(args, world, wl),
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
                          "sample": f"full c4 batch ({wl.n_queries} queries) per step, C radix-tree restatement (oracle/radix_oracle.c), {cores} threads"},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -422,11 +430,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "c4" if mixed is None else "c5-shard", "sessions": args.sessions,
-                   "history_tokens": args.hist if mixed is None else f"log-uniform {mixed}",
-                   "batch_queries": args.queries, "ext_frac": 0.75, "parallelism": f"session-shard x{world}",
-                   "l2": "inputs larger than L2 (arena %.2f GB + queries %.2f GB per rank)" % (
-                       wl.hist_off[-1] * 4 / 1e9, wl.q_off[-1] * 4 / 1e9)},
+        "config": c4_config(args, world, wl, mixed),
         "tokens_compared_per_s": toks_per_s,
         "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
         "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
