@@ -116,6 +116,9 @@ struct tm_store {
   int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
   int64_t arena_used = 0, n_runs = 0, n_sess = 0;
   int64_t n_real_rows = 0;  // rows minus reserved-but-unused slots
+  std::vector<uint64_t> chain_stamp;  // record: per-session batch stamp and chain slot
+  std::vector<int32_t> chain_slot;
+  uint64_t batch_stamp = 0;
   std::vector<RowHost> rows;
   std::vector<std::vector<int64_t>> sess_rows;
   std::vector<int64_t> sess_stored, sess_naive;
@@ -297,7 +300,10 @@ bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->
 void wait_prev(tm_store *s, cudaStream_t st) {
   ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
   for (auto &sl : s->slots)
-    if (sl.used) ck(cudaStreamWaitEvent(st, sl.done, 0), "cudaStreamWaitEvent");
+    if (sl.used) {
+      ck(cudaStreamWaitEvent(st, sl.done, 0), "cudaStreamWaitEvent");
+      sl.used = false;  // ordered behind this operation from now on (it records `last`)
+    }
 }
 
 void mark_done(tm_store *s, cudaStream_t st) { ck(cudaEventRecord(s->last, st), "cudaEventRecord"); }
@@ -537,7 +543,13 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     if (mem != TM_MEM_HOST && mem != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
     // ---- validate (trie.py:128-131); group entries into per-session chains (batch order
     // inside a chain: sequential semantics), chains ordered longest first
-    std::vector<int32_t> chain_of_sid(s->n_sess, -1);
+    // session -> chain slot for this batch (stamped, so a 1-entry call on a store with
+    // millions of sessions does not clear a million-entry table)
+    if ((int64_t)s->chain_stamp.size() < s->n_sess) {
+      s->chain_stamp.resize(s->n_sess, 0);
+      s->chain_slot.resize(s->n_sess, -1);
+    }
+    const uint64_t stamp = ++s->batch_stamp;
     std::vector<int64_t> chain_tokens;
     std::vector<int32_t> chain_len;
     std::vector<int32_t> chain_idx(n);
@@ -557,9 +569,10 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         if (run_origin[r] > 1) fail(TM_EINVAL, "bad origin");
       if (mem == TM_MEM_DEVICE && tok_off[k] % tms::kAlignWords)
         fail(TM_EINVAL, "device token offsets must be multiples of 32");
-      int32_t c = chain_of_sid[sid];
+      int32_t c = s->chain_stamp[sid] == stamp ? s->chain_slot[sid] : -1;
       if (c < 0) {
-        c = chain_of_sid[sid] = (int32_t)chain_tokens.size();
+        s->chain_stamp[sid] = stamp;
+        c = s->chain_slot[sid] = (int32_t)chain_tokens.size();
         chain_tokens.push_back(0);
         chain_len.push_back(0);
       }
@@ -669,8 +682,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       ck(tms::launch_record(s->v, ra, s->num_sms, s->stream), "record");
     }
     // ---- results back (chain order), into the host mirror in batch order
-    ck(cudaMemcpyAsync(h + o_crow, d + o_crow, 8 * n, cudaMemcpyDeviceToHost, s->stream), "D2H rows");
-    ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, s->stream), "D2H results");
+    ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
     int64_t ctr[4];
     ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
     mark_done(s, s->stream);

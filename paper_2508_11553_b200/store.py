@@ -191,6 +191,12 @@ class DeviceStore:
             _ptr(r.parent), _ptr(r.parent_local), _ptr(r.added), self._stream_arg(stream)))
         return r
 
+    def record_one(self, sid: int, tokens: np.ndarray, runs) -> RecordResult:
+        """Single-sequence record (the per-request path): no repacking."""
+        st, org, ver = runs
+        return self.record_packed(np.array([sid], np.int32), tokens, np.zeros(1, np.int64),
+                                  np.array([len(tokens)], np.int64), np.array([0, len(st)], np.int64), st, org, ver)
+
     def record(self, sids, seqs, runs) -> RecordResult:
         """seqs: list of int sequences; runs: list of (starts, origins, versions)."""
         lens = np.fromiter((len(s) for s in seqs), np.int64, len(seqs))
@@ -243,10 +249,13 @@ class DeviceStore:
         check(self.lib.tm_rows_total(self.h, len(rows), _ptr(rows), C.byref(t)))
         return t.value
 
-    def export(self, rows) -> Packed:
+    def export(self, rows, total: int | None = None) -> Packed:
+        """Packed trajectories of ``rows`` in host numpy arrays (``total``: their summed
+        length when the caller already knows it, saving a round trip)."""
         rows = np.ascontiguousarray(rows, np.int64)
         n = len(rows)
-        total = self.rows_total(rows) if n else 0
+        if total is None:
+            total = self.rows_total(rows) if n else 0
         off = np.zeros(n + 1, np.int64)
         tok = np.empty(total, np.int32)
         msk = np.empty(total, np.uint8)

@@ -17,6 +17,7 @@ extensions a new one, and ids survive later branching.
 
 from __future__ import annotations
 
+import array
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -62,13 +63,56 @@ class TrieNode:
         return bool(self.leaf_marks)
 
 
-def _origins_to_codes(origins: Sequence[SpanOrigin]) -> np.ndarray:
-    if isinstance(origins, np.ndarray):
-        return origins.astype(np.int64)
+def _as_int32(values) -> np.ndarray:
+    """Token ids -> int32 array at C speed (array.array), rejecting ids outside int32."""
+    if isinstance(values, np.ndarray):
+        if values.size and (values.min() < -(2**31) or values.max() >= 2**31):
+            raise ValueError("token ids must fit in int32")
+        return np.ascontiguousarray(values, np.int32)
     try:
-        return np.fromiter((ORIGIN_CODE[o] for o in origins), np.int64, len(origins))
-    except KeyError:
-        return np.fromiter((1 if o in (1, True, "model_output") else 0 for o in origins), np.int64, len(origins))
+        return np.frombuffer(array.array("i", values), np.int32)
+    except OverflowError:
+        raise ValueError("token ids must fit in int32") from None
+
+
+def meta_runs(origins, versions):
+    """Per-token (origin, version) -> run starts / origin codes / versions.
+
+    Runs are found at C speed: origin changes with list.index (two values), version
+    changes from an int64 view (skipped when every token has the same version)."""
+    n = len(origins)
+    if isinstance(origins, np.ndarray) or not n:
+        o = np.asarray([ORIGIN_CODE.get(x, x) for x in origins] if not isinstance(origins, np.ndarray) else origins,
+                       np.int64)
+        return runs_from_per_token(o, np.asarray(versions, np.int64))
+    first = origins[0]
+    o_starts, o_vals = [0], [first]
+    cur, i = first, 0
+    other = {SpanOrigin.AGENT_INPUT: SpanOrigin.MODEL_OUTPUT, SpanOrigin.MODEL_OUTPUT: SpanOrigin.AGENT_INPUT}
+    if cur not in other:  # not SpanOrigin members: generic path
+        return runs_from_per_token(np.asarray([1 if x in (1, True, "model_output") else 0 for x in origins], np.int64),
+                                   np.asarray(versions, np.int64))
+    while True:
+        nxt = other[cur]
+        try:
+            i = origins.index(nxt, i)
+        except ValueError:
+            break
+        o_starts.append(i)
+        o_vals.append(nxt)
+        cur = nxt
+    if isinstance(versions, list) and versions.count(versions[0]) == n:
+        v_starts, v_vals = [0], [versions[0]]
+    else:
+        v = np.frombuffer(array.array("q", versions), np.int64) if isinstance(versions, list) else np.asarray(versions, np.int64)
+        cut = np.flatnonzero(v[1:] != v[:-1]) + 1
+        v_starts = [0] + cut.tolist()
+        v_vals = v[[0] + cut.tolist()].tolist()
+    starts = sorted(set(o_starts) | set(v_starts))
+    oi = np.searchsorted(np.asarray(o_starts), starts, side="right") - 1
+    vi = np.searchsorted(np.asarray(v_starts), starts, side="right") - 1
+    codes = np.asarray([ORIGIN_CODE[x] for x in o_vals], np.uint8)[oi]
+    return np.asarray(starts, np.int32), codes, np.asarray(v_vals, np.int32)[vi]
 
 
 class SessionTrie:
@@ -80,6 +124,7 @@ class SessionTrie:
         self.sid = self.store.new_session()
         self._marks: dict[int, set[str]] = {}
         self._rows: list[int] = []  # local ordinal -> global row
+        self._lens: list[int] = []  # local ordinal -> sequence length
 
     # -- record -------------------------------------------------------------------
     def lpm_insert(self, tokens: Sequence[TokenId], origins: Sequence[SpanOrigin], versions: Sequence[ModelVersion],
@@ -89,18 +134,18 @@ class SessionTrie:
             raise ValueError("cannot insert an empty sequence")
         if not (len(tokens) == len(origins) == len(versions)):
             raise ValueError("tokens, origins, versions must be parallel")
-        runs = runs_from_per_token(_origins_to_codes(origins), np.asarray(versions, np.int64))
-        return self.insert_runs(tokens, runs, completion_id)
+        return self.insert_runs(tokens, meta_runs(origins, versions), completion_id)
 
     def insert_runs(self, tokens, runs, completion_id: str | None = None) -> InsertResult:
         """lpm_insert with metadata already as (starts, origins 0/1, versions) runs."""
-        r = self.store.record([self.sid], [tokens], [runs])
-        return self._absorb(r, 0, completion_id)
+        r = self.store.record_one(self.sid, _as_int32(tokens), runs)
+        return self._absorb(r, 0, completion_id, len(tokens))
 
-    def _absorb(self, r, k: int, completion_id):
+    def _absorb(self, r, k: int, completion_id, length: int):
         local = int(r.local[k])
         if local == len(self._rows):
             self._rows.append(int(r.row[k]))
+            self._lens.append(int(length))
         if completion_id is not None:
             self._marks.setdefault(local, set()).add(completion_id)
         return InsertResult(int(r.matched[k]), local, int(r.added[k]))
@@ -134,7 +179,7 @@ class SessionTrie:
 
     def path_trajectory(self, node_id: int) -> Trajectory:
         """Rebuild the trajectory for the root->node path (trie.py:203-208)."""
-        p = self.store.export([self._global(node_id)])
+        p = self.store.export([self._global(node_id)], total=self._lens[node_id])
         return Trajectory.from_packed(self.session_id, p.tokens, p.loss_mask, p.versions)
 
     def lex_node_ids(self) -> list[int]:
@@ -150,7 +195,7 @@ class SessionTrie:
         ids = self.marked_nodes()
         if not ids:
             return []
-        p = self.store.export([self._rows[k] for k in ids])
+        p = self.store.export([self._rows[k] for k in ids], total=sum(self._lens[k] for k in ids))
         out = []
         for i, k in enumerate(ids):
             a, b = p.offsets[i], p.offsets[i + 1]

@@ -1,0 +1,50 @@
+"""Per-call latency of the drop-in API (single lpm_insert / path_trajectory / extract)
+next to the reference's own Python implementation (a C restatement is not the right
+comparison for per-call overhead; the pure-Python oracle restates trie.py)."""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    from oracle.radix import RadixOracle
+    from paper_2508_11553_b200 import DeviceStore, SessionTrie, SpanOrigin
+
+    store = DeviceStore(0)
+    rng = np.random.default_rng(0)
+    for L in (16, 512, 4096, 32768):
+        trie = SessionTrie("lat", store=store)
+        ora = RadixOracle()
+        base = rng.integers(0, 151936, L).tolist()
+        org = [SpanOrigin.AGENT_INPUT] * (L // 2) + [SpanOrigin.MODEL_OUTPUT] * (L - L // 2)
+        o01 = [0] * (L // 2) + [1] * (L - L // 2)
+        ver = [0] * L
+        seqs = [base[: L - 8] + rng.integers(0, 151936, 8).tolist() for _ in range(50)]
+        trie.lpm_insert(seqs[0], org, ver, "w")
+        t0 = time.perf_counter()
+        for s in seqs[1:]:
+            trie.lpm_insert(s, org, ver, "c")
+        t_ins = (time.perf_counter() - t0) / (len(seqs) - 1)
+        t0 = time.perf_counter()
+        for s in seqs:
+            ora.insert(s, o01, ver, "c")
+        t_ora = (time.perf_counter() - t0) / len(seqs)
+        t0 = time.perf_counter()
+        for k in range(20):
+            trie.path_trajectory(k)
+        t_path = (time.perf_counter() - t0) / 20
+        t0 = time.perf_counter()
+        ext = trie.extract()
+        t_ext = time.perf_counter() - t0
+        print(f"L={L:6d}  lpm_insert {t_ins*1e6:8.1f} us (python trie restatement {t_ora*1e6:8.1f} us)  "
+              f"path_trajectory {t_path*1e6:8.1f} us  extract({len(ext)} rows) {t_ext*1e3:7.2f} ms")
+
+
+if __name__ == "__main__":
+    main()
