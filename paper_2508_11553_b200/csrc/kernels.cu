@@ -8,6 +8,8 @@
 //  k_rehash        branch-index growth
 #include "kernels.cuh"
 
+#include <algorithm>
+
 #include "launch.h"
 
 #include <cstdlib>
@@ -425,6 +427,16 @@ __global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
 constexpr int kExportNT = 256;
 constexpr int kExportTile = 4096;
 
+struct ExportPiece {        // one ancestor's share of an output tile
+  int64_t vb;                // owner's arena virtual base
+  int64_t run0;              // owner's first metadata run ...
+  int32_t pa, pb;            // positions [pa, pb) of the output row
+  int32_t nrun, first_run;   // ... its run count, and the run containing pa
+  int32_t len;               // owner's length (end of its last run)
+  int32_t pad;
+};
+constexpr int kMaxPieces = 16;  // per tile; deeper chains fall back to an in-kernel walk
+
 struct ExportArgs {
   int64_t n;
   const int64_t *rows;
@@ -435,6 +447,9 @@ struct ExportArgs {
   uint8_t *mask;
   int32_t *versions;
   unsigned long long *resp;  // n (atomicMax), may be null
+  int32_t *tile_row;         // ntiles: output row of each tile (planner output)
+  int32_t *npieces;          // ntiles: pieces per tile, or -1 (walk in-kernel)
+  ExportPiece *pieces;       // ntiles * kMaxPieces
 };
 
 // Copy / fill helpers for one piece [pa, pb) of an output row starting at word o.  When
@@ -486,45 +501,104 @@ __device__ __forceinline__ void fill_meta(uint8_t *__restrict__ mask, int32_t *_
   for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
 }
 
-__global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
-  for (int64_t t = blockIdx.x; t < e.ntiles; t += gridDim.x) {
+// Export planner: one thread per tile resolves the dependent lookups (tile -> row,
+// parent chain, first run of each piece) for every tile in parallel, so the copy
+// kernel's CTAs start streaming immediately instead of chasing pointers per tile.
+__global__ void k_export_plan(DevView v, ExportArgs e) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = e.n;  // largest i with tile_off[i] <= t
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
       if (e.tile_off[mid] <= t) lo = mid; else hi = mid;
     }
-    const int64_t i = lo;
-    const int64_t row = e.rows[i];
-    const int64_t a = (t - e.tile_off[i]) * kExportTile;
+    e.tile_row[t] = (int32_t)lo;
+    const int64_t row = e.rows[lo];
+    const int64_t a = (t - e.tile_off[lo]) * kExportTile;
     const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
-    const int64_t o = e.out_off[i];
     int64_t cur = row, upper = v.row_len[row];
-    long long respmax = 0;
-    while (cur >= 0 && upper > a) {  // ancestors own [m_x, upper)
+    int np = 0;
+    ExportPiece *out = e.pieces + t * kMaxPieces;
+    while (cur >= 0 && upper > a) {
       const int64_t mx = v.row_m[cur];
       const int64_t pa = max(mx, a), pb = min(upper, b);
       if (pa < pb) {
-        copy_tokens(e.tokens, v.arena + v.row_vb[cur], o, pa, pb);
-        const int64_t r0 = v.row_run0[cur];
-        const int nr = v.row_nrun[cur];
-        const int64_t lenx = v.row_len[cur];
-        int lo2 = 0, hi2 = nr;  // last run with start <= pa
+        if (np == kMaxPieces) { np = -1; break; }
+        ExportPiece p;
+        p.vb = v.row_vb[cur];
+        p.run0 = v.row_run0[cur];
+        p.pa = (int32_t)pa;
+        p.pb = (int32_t)pb;
+        p.nrun = v.row_nrun[cur];
+        p.len = v.row_len[cur];
+        int lo2 = 0, hi2 = p.nrun;  // last run with start <= pa
         while (hi2 - lo2 > 1) {
           int mid = (lo2 + hi2) >> 1;
-          if (v.run_start[r0 + mid] <= pa) lo2 = mid; else hi2 = mid;
+          if (v.run_start[p.run0 + mid] <= pa) lo2 = mid; else hi2 = mid;
         }
-        for (int k = lo2; k < nr; k++) {
-          const int64_t rs = v.run_start[r0 + k];
-          if (rs >= pb) break;
-          const int64_t re = (k + 1 < nr) ? v.run_start[r0 + k + 1] : lenx;
-          const int64_t xa = max(rs, pa), xb = min(re, pb);
-          const uint8_t org = v.run_origin[r0 + k];
-          fill_meta(e.mask, e.versions, o, xa, xb, org, v.run_version[r0 + k]);
-          if (org == 0 && xb > respmax) respmax = xb;
-        }
+        p.first_run = lo2;
+        p.pad = 0;
+        out[np++] = p;
       }
       upper = mx;
       cur = v.row_parent[cur];
+    }
+    e.npieces[t] = np;
+  }
+}
+
+__device__ __forceinline__ void export_piece(const DevView &v, const ExportArgs &e, const ExportPiece &p, int64_t o,
+                                             long long &respmax) {
+  copy_tokens(e.tokens, v.arena + p.vb, o, p.pa, p.pb);
+  for (int k = p.first_run; k < p.nrun; k++) {
+    const int64_t rs = v.run_start[p.run0 + k];
+    if (rs >= p.pb) break;
+    const int64_t re = (k + 1 < p.nrun) ? v.run_start[p.run0 + k + 1] : p.len;
+    const int64_t xa = max(rs, (int64_t)p.pa), xb = min(re, (int64_t)p.pb);
+    const uint8_t org = v.run_origin[p.run0 + k];
+    fill_meta(e.mask, e.versions, o, xa, xb, org, v.run_version[p.run0 + k]);
+    if (org == 0 && xb > respmax) respmax = xb;
+  }
+}
+
+__global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
+  __shared__ ExportPiece sp[kMaxPieces];
+  for (int64_t t = blockIdx.x; t < e.ntiles; t += gridDim.x) {
+    const int64_t i = e.tile_row[t];
+    const int np = e.npieces[t];
+    const int64_t o = e.out_off[i];
+    long long respmax = 0;
+    if (np >= 0) {
+      if (threadIdx.x < np) sp[threadIdx.x] = e.pieces[t * kMaxPieces + threadIdx.x];
+      __syncthreads();
+      for (int k = 0; k < np; k++) export_piece(v, e, sp[k], o, respmax);
+      __syncthreads();
+    } else {  // chain deeper than kMaxPieces inside this tile: walk it here
+      const int64_t row = e.rows[i];
+      const int64_t a = (t - e.tile_off[i]) * kExportTile;
+      const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
+      int64_t cur = row, upper = v.row_len[row];
+      while (cur >= 0 && upper > a) {
+        const int64_t mx = v.row_m[cur];
+        const int64_t pa = max(mx, a), pb = min(upper, b);
+        if (pa < pb) {
+          ExportPiece p;
+          p.vb = v.row_vb[cur];
+          p.run0 = v.row_run0[cur];
+          p.pa = (int32_t)pa;
+          p.pb = (int32_t)pb;
+          p.nrun = v.row_nrun[cur];
+          p.len = v.row_len[cur];
+          int lo2 = 0, hi2 = p.nrun;
+          while (hi2 - lo2 > 1) {
+            int mid = (lo2 + hi2) >> 1;
+            if (v.run_start[p.run0 + mid] <= pa) lo2 = mid; else hi2 = mid;
+          }
+          p.first_run = lo2;
+          export_piece(v, e, p, o, respmax);
+        }
+        upper = mx;
+        cur = v.row_parent[cur];
+      }
     }
     if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[i], (unsigned long long)respmax);
   }
@@ -778,12 +852,16 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
 
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {
   ExportArgs e{h.n, h.rows, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions,
-               (unsigned long long *)h.resp};
+               (unsigned long long *)h.resp, h.tile_row, h.npieces, reinterpret_cast<ExportPiece *>(h.pieces)};
+  if (h.ntiles < 1) return cudaSuccess;
+  const int pgrid = (int)std::min<int64_t>((h.ntiles + 255) / 256, (int64_t)num_sms * 8);
+  k_export_plan<<<pgrid, 256, 0, s>>>(v, e);
   int64_t grid = h.ntiles < (int64_t)num_sms * 8 ? h.ntiles : (int64_t)num_sms * 8;
-  if (grid < 1) return cudaSuccess;
   k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
   return cudaGetLastError();
 }
+
+int64_t export_plan_bytes(int64_t ntiles) { return ntiles * (8 + (int64_t)kMaxPieces * (int64_t)sizeof(ExportPiece)); }
 
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s) {

@@ -18,7 +18,11 @@ struct ExportArgsHost {
   uint8_t *mask;
   int32_t *versions;
   int64_t *resp;
+  int32_t *tile_row;  // planner scratch: ntiles ints, ntiles ints, ntiles * kMaxPieces pieces
+  int32_t *npieces;
+  void *pieces;
 };
+int64_t export_plan_bytes(int64_t ntiles);
 
 // fills b.root (if root != null) and b.bucket_items (plan_items_ints(n) ints); counts go to b.sched
 struct JsonArgsHost {
