@@ -272,7 +272,7 @@ def run_c5(args):
                      "traffic": None,
                      "note": "N>1: remote query bytes cross NVLink (tools/p2p_probe: SM peer reads 780 GB/s one "
                              "direction, 670 GB/s both directions at once); history bytes come from local HBM"},
-        "gpu_launches": args.steps * 2,
+        "gpu_launches": args.steps * 2,  # k_route + k_walk_routed per batch
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -440,7 +440,7 @@ def main():
                      "event_ms_avg_per_launch": walk_ms / max(walk_n, 1),
                      "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps * 2,
+        "gpu_launches": int(walk_n + plan_n),  # our kernels in the timed region (CUDA-event bracketed)
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
