@@ -128,6 +128,7 @@ __device__ __forceinline__ void sched_exit(Sched *sc) {
     if (atomicAdd(&sc->exit, 1u) == gridDim.x - 1) {
       for (int i = 0; i < kPlanNB; i++) sc->count[i] = 0;
       sc->work = 0;
+      sc->work2 = 0;
       sc->exit = 0;
       __threadfence();
     }
@@ -239,46 +240,77 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
     idx[atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1)] = (int32_t)i;
 }
 
-// Owner side.  Items are ordered (length bucket, requester): the global longest-first
-// order over all requesters' queries owned here; rank -> item via a prefix table.
+// Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
+// and the other ranks' (query bytes over NVLink).  1/np of the CTAs start on the local
+// queue and the rest on the remote one, each falling back to the other when its queue
+// runs dry, so HBM and the links are busy at the same time instead of in phases.
 template <int NT, int U>
 __global__ void __launch_bounds__(NT) k_walk_routed(DevView v, RoutedArgs a) {
   __shared__ WalkShared sh;
   __shared__ long long s_item;
-  __shared__ int s_pre[kPlanNB * kMaxRanks + 1];  // prefix over (bucket, peer)
-  __shared__ int s_bs[kPlanNB * kMaxRanks];       // bstart of (bucket, peer)
+  __shared__ int s_cell;
+  __shared__ int s_pre[kPlanNB * kMaxRanks + 2];  // cells: local (b) then remote (b, p != rank)
+  __shared__ int s_bs[kPlanNB * kMaxRanks];
+  __shared__ int s_peer[kPlanNB * kMaxRanks];
+  __shared__ int s_nloc;  // cells in the local queue
   const int np = a.nranks;
-  for (int c = threadIdx.x; c < kPlanNB * np; c += NT) {
-    const int bk = c / np, p = c % np;
+  const int ncell = kPlanNB * np;
+  // cell c: local cells first (bucket order), then remote cells (bucket, peer) order
+  for (int c = threadIdx.x; c < ncell; c += NT) {
+    int bk, p;
+    if (c < kPlanNB) { bk = c; p = a.rank; }
+    else { const int r = c - kPlanNB; bk = r / (np - 1); const int q = r % (np - 1); p = q < a.rank ? q : q + 1; }
     const RouteDesc *d = reinterpret_cast<const RouteDesc *>(a.peer[p]);
-    s_pre[c] = d->bcount[a.rank * kPlanNB + bk];  // counts, scanned below
+    s_pre[c] = d->bcount[a.rank * kPlanNB + bk];
     s_bs[c] = d->bstart[a.rank * kPlanNB + bk];
+    s_peer[c] = p;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // separate exclusive scans for the two queues
     int acc = 0;
-    for (int c = 0; c < kPlanNB * np; c++) { int t = s_pre[c]; s_pre[c] = acc; acc += t; }
-    s_pre[kPlanNB * np] = acc;
+    for (int c = 0; c < kPlanNB; c++) { int t = s_pre[c]; s_pre[c] = acc; acc += t; }
+    s_pre[ncell] = acc;  // local total
+    acc = 0;
+    for (int c = kPlanNB; c < ncell; c++) { int t = s_pre[c]; s_pre[c] = acc; acc += t; }
+    s_pre[ncell + 1] = acc;  // remote total
+    s_nloc = kPlanNB;
   }
   __syncthreads();
-  const int total = s_pre[kPlanNB * np];
+  const long long tot[2] = {s_pre[ncell], s_pre[ncell + 1]};
+  int q = (np > 1 && blockIdx.x % np != 0) ? 1 : 0;  // queue this CTA prefers
+  bool dry[2] = {false, false};
   for (;;) {
-    if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
+    if (threadIdx.x == 0) {
+      long long it = -1;
+      int cell = -1;
+      for (int tries = 0; tries < 2 && it < 0; tries++) {
+        const int qq = tries ? 1 - q : q;
+        if (dry[qq]) continue;
+        const long long x = (long long)atomicAdd(qq ? &a.sched->work2 : &a.sched->work, 1ull);
+        if (x >= tot[qq]) { dry[qq] = true; continue; }
+        int lo = qq ? kPlanNB : 0, hi = qq ? ncell : kPlanNB;  // last cell with prefix <= x
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (s_pre[mid] <= x) lo = mid; else hi = mid;
+        }
+        it = x;
+        cell = lo;
+      }
+      s_item = it;
+      s_cell = cell;
+    }
     __syncthreads();
     const long long it = s_item;
-    if (it >= total) {
+    const int cell = s_cell;
+    __syncthreads();
+    if (it < 0) {
       sched_exit(a.sched);
       return;
     }
-    int lo = 0, hi = kPlanNB * np;  // last cell with prefix <= it
-    while (hi - lo > 1) {
-      int mid = (lo + hi) >> 1;
-      if (s_pre[mid] <= it) lo = mid; else hi = mid;
-    }
-    const int p = lo % np;
+    const int p = s_peer[cell];
     const char *reg = a.peer[p];
     const RouteDesc *d = reinterpret_cast<const RouteDesc *>(reg);
-    const int32_t qi = reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[lo] + (it - s_pre[lo])];
+    const int32_t qi = reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[cell] + (it - s_pre[cell])];
     const int64_t g = reinterpret_cast<const int64_t *>(reg + d->sid_off)[qi];
     const int64_t off = reinterpret_cast<const int64_t *>(reg + d->qoff_off)[qi];
     const int L = (int)reinterpret_cast<const int64_t *>(reg + d->len_off)[qi];

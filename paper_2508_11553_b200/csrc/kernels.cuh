@@ -47,6 +47,7 @@ constexpr int kPlanNB = 128;
 struct Sched {
   int count[kPlanNB];
   unsigned long long work;
+  unsigned long long work2;  // second queue (routed walk: remote queries)
   unsigned int exit;
 };
 
