@@ -229,11 +229,13 @@ def run_c5(args):
     with Clocks(local) as clk:
         time.sleep(0.3)
         t_wall = time.perf_counter()
+        store.profile_begin()
         e0.record(stream)
         for _ in range(args.steps):
             router.match(wl.n_queries)
         e1.record(stream)
         torch.cuda.synchronize()
+        walk_ms, walk_n = store.profile_end("walk")
         while time.perf_counter() - t_wall < 1.0:
             for _ in range(10):
                 router.match(wl.n_queries)
@@ -263,6 +265,8 @@ def run_c5(args):
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,
         "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * args.steps / elapsed / 1e9,
+        "routed_walk_ms_avg_rank0": walk_ms / max(walk_n, 1),
+        "nvlink_query_GBps_during_walk_rank0": 4.0 * remote_toks / world / (walk_ms / max(walk_n, 1)) / 1e6,
         "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
                      "achieved": (4.0 * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
                      "peak": 770.0 if world > 1 else peak, "unit": "GB/s",

@@ -13,7 +13,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtmstore.so")
+# TM_LIB selects another build of the same C ABI (e.g. libtmstore_debug.so: device bounds checks)
+LIB_PATH = os.environ.get("TM_LIB") or os.path.join(HERE, "libtmstore.so")
 
 TM_OK, TM_EINVAL, TM_ENOENT, TM_ENOMEM, TM_ECUDA = 0, 1, 2, 3, 4
 TM_MEM_HOST, TM_MEM_DEVICE = 0, 1

@@ -88,8 +88,10 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
   int lo = sh.lo;
   __syncthreads();
   while (r >= 0) {
+    TM_DCHECK(v, r < v.row_cap, kErrRow);
     const int Lr = v.row_len[r];
     const int hi = min(Lr, L);
+    TM_DCHECK(v, v.row_vb[r] + v.row_m[r] >= 0 && v.row_vb[r] + ((Lr + 3) & ~3) <= v.arena_cap, kErrArena);
     const int32_t *a = v.arena + v.row_vb[r];
     const int j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
     if (threadIdx.x == 0) {
@@ -372,6 +374,12 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
   const int64_t row = b.c_row[e];
   const bool isnew = b.o_dup[e] < 0;
   if (threadIdx.x == 0) {
+    TM_DCHECK(v, row >= 0 && row < v.row_cap, kErrRow);
+    if (isnew && L > m) {
+      TM_DCHECK(v, b.c_vb[e] + (m & ~31ll) >= 0 && b.c_vb[e] + ((L + 31) & ~31ll) <= v.arena_cap, kErrArena);
+      TM_DCHECK(v, b.c_run0[e] >= 0 && b.c_run0[e] + (b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) <= v.run_cap,
+                kErrRun);
+    }
     if (isnew) {
       const int64_t par = b.o_parent[e];
       const int32_t local = v.s_nrows[sid];
@@ -554,6 +562,7 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
       const int64_t mx = v.row_m[cur];
       const int64_t pa = max(mx, a), pb = min(upper, b);
       if (pa < pb) {
+        TM_DCHECK(v, cur < v.row_cap && v.row_vb[cur] + pb <= v.arena_cap, kErrArena);
         if (np == kMaxPieces) { np = -1; break; }
         ExportPiece p;
         p.vb = v.row_vb[cur];

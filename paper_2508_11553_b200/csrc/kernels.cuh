@@ -38,8 +38,36 @@ struct DevView {
   int64_t *s_stored;
   int64_t *s_naive;
   // allocation counters (device-resident, advanced by the commit planner)
-  int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=error flags
+  int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=first device error code
+  // capacities (device-side bounds checks)
+  int64_t arena_cap, row_cap, run_cap;
 };
+
+// Device error codes (ctr[3]; first one wins; the host turns a nonzero code into TM_ECUDA).
+enum : long long {
+  kErrTableFull = 1,   // branch index probe wrapped the whole table (never expected: load <= 1/2)
+  kErrArena = 2,       // arena access outside its capacity
+  kErrRow = 3,         // row id outside the row table
+  kErrRun = 4,         // metadata run outside the run table
+};
+
+__device__ __forceinline__ void dev_error(const DevView &v, long long code) {
+  atomicCAS(reinterpret_cast<unsigned long long *>(&v.ctr[3]), 0ull, (unsigned long long)code);
+}
+
+// TM_DCHECK: bounds checks compiled into the debug build (-DTM_DEBUG, libtmstore_debug.so)
+// — compute-sanitizer is not available on this pool, so the debug library records the
+// first violated invariant in ctr[3] instead of faulting.
+#ifdef TM_DEBUG
+#define TM_DCHECK(v, cond, code) \
+  do {                             \
+    if (!(cond)) dev_error(v, code); \
+  } while (0)
+#else
+#define TM_DCHECK(v, cond, code) \
+  do {                             \
+  } while (0)
+#endif
 
 // Walk scheduler block (one per store, zeroed once at creation): planner bucket counts,
 // the walk's work counter and an exit counter; the last walk CTA re-zeroes it.
@@ -132,19 +160,27 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t owner, uint64_t dt, uint64_
   return mix64(owner * 0x9e3779b97f4a7c15ull ^ mix64(dt + 0x632be59bd9b4e019ull)) & mask;
 }
 
+// Probes are bounded by the table size (always on): a full table reports an error
+// instead of spinning forever.
 __device__ __forceinline__ int64_t ht_find(const DevView &v, uint64_t owner, uint64_t dt) {
   uint64_t s = slot_of(owner, dt, v.ht_mask);
-  for (;;) {
+  for (uint64_t probes = 0; probes <= v.ht_mask; probes++) {
     uint64_t k0 = v.hk0[s];
     if (k0 == kEmpty) return -1;
-    if (k0 == owner && v.hk1[s] == dt) return v.hval[s];
+    if (k0 == owner && v.hk1[s] == dt) {
+      const int64_t r = v.hval[s];
+      TM_DCHECK(v, r >= 0 && r < v.row_cap, kErrRow);
+      return r;
+    }
     s = (s + 1) & v.ht_mask;
   }
+  dev_error(v, kErrTableFull);
+  return -1;
 }
 
 __device__ __forceinline__ void ht_insert(const DevView &v, uint64_t owner, uint64_t dt, int64_t val) {
   uint64_t s = slot_of(owner, dt, v.ht_mask);
-  for (;;) {
+  for (uint64_t probes = 0; probes <= v.ht_mask; probes++) {
     unsigned long long prev = atomicCAS((unsigned long long *)&v.hk0[s], (unsigned long long)kEmpty,
                                         (unsigned long long)owner);
     if (prev == kEmpty) {
@@ -154,6 +190,7 @@ __device__ __forceinline__ void ht_insert(const DevView &v, uint64_t owner, uint
     }
     s = (s + 1) & v.ht_mask;
   }
+  dev_error(v, kErrTableFull);
 }
 
 __device__ __forceinline__ int4 ldg_stream(const int4 *p) {

@@ -178,6 +178,7 @@ void ensure_rows(tm_store *s, int64_t need) {
   dev_grow(s->v.row_run0, n, nc, s->stream);
   dev_grow(s->v.row_nrun, n, nc, s->stream);
   s->row_cap = nc;
+  s->v.row_cap = nc;
 }
 
 void ensure_runs(tm_store *s, int64_t need) {
@@ -187,6 +188,7 @@ void ensure_runs(tm_store *s, int64_t need) {
   dev_grow(s->v.run_version, s->n_runs, nc, s->stream);
   dev_grow(s->v.run_origin, s->n_runs, nc, s->stream);
   s->run_cap = nc;
+  s->v.run_cap = nc;
 }
 
 void ensure_arena(tm_store *s, int64_t need) {
@@ -194,6 +196,7 @@ void ensure_arena(tm_store *s, int64_t need) {
   int64_t nc = std::max<int64_t>(round_up(need, 1 << 20), s->arena_cap * 2);
   dev_grow(s->v.arena, s->arena_used, nc, s->stream);
   s->arena_cap = nc;
+  s->v.arena_cap = nc;
 }
 
 void ensure_sessions(tm_store *s, int64_t need) {
@@ -293,6 +296,16 @@ void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaSt
     for (auto &x : th) x.join();
   }
   for (auto &e : ev) cudaEventDestroy(e);
+}
+
+// a device-side error code (kernels.cuh kErr*) becomes a loud host error
+void check_device_error(tm_store *s) {
+  int64_t code = 0;
+  ck(cudaMemcpy(&code, s->v.ctr + 3, sizeof(code), cudaMemcpyDeviceToHost), "D2H error flag");
+  if (code) {
+    static const char *names[] = {"", "branch index full", "arena bounds", "row bounds", "run bounds"};
+    fail(TM_ECUDA, std::string("device check failed: ") + (code > 0 && code < 5 ? names[code] : "unknown"));
+  }
 }
 
 bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->rows.size() && s->rows[r].sid >= 0; }
@@ -444,7 +457,11 @@ void load_dev(tm_store *s, FileR &r, T *d, int64_t n) {
 extern "C" {
 
 const char *tm_last_error(void) { return g_err.c_str(); }
+#ifdef TM_DEBUG
+const char *tm_version(void) { return "tmstore 0.1.0 (sm_100a, debug checks)"; }
+#else
 const char *tm_version(void) { return "tmstore 0.1.0 (sm_100a)"; }
+#endif
 
 int tm_store_create(const tm_config *cfg, tm_store **out) {
   if (!out) {
@@ -684,9 +701,12 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     // ---- results back (chain order), into the host mirror in batch order
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
     int64_t ctr[4];
+    int64_t dev_err = 0;
     ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
+    ck(cudaMemcpyAsync(&dev_err, s->v.ctr + 3, sizeof(dev_err), cudaMemcpyDeviceToHost, s->stream), "D2H err");
     mark_done(s, s->stream);
     ck(cudaStreamSynchronize(s->stream), "record sync");
+    if (dev_err) check_device_error(s);
     const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
     const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
@@ -794,6 +814,7 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
       ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, st), "D2H");
       mark_done(s, st);
       ck(cudaStreamSynchronize(st), "match sync");
+      check_device_error(s);
       memcpy(out_matched, h + o_m, 8 * n);
       if (out_parent) memcpy(out_parent, h + o_par, 8 * n);
       if (out_dup) memcpy(out_dup, h + o_dup, 8 * n);
@@ -886,6 +907,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       if (out_resp_start) ck(cudaMemcpyAsync(out_resp_start, e.resp, 8 * n, cudaMemcpyDeviceToHost, st), "D2H resp");
       mark_done(s, st);
       ck(cudaStreamSynchronize(st), "export sync");
+      check_device_error(s);
     } else {
       mark_done(s, st);
     }
@@ -1272,6 +1294,7 @@ int tm_synchronize(tm_store *s) {
   return guarded(s, [&] {
     ck(cudaStreamSynchronize(s->stream), "sync");
     ck(cudaEventSynchronize(s->last), "sync");
+    check_device_error(s);
     for (auto &sl : s->slots)
       if (sl.used) ck(cudaEventSynchronize(sl.done), "sync");
   });
