@@ -187,12 +187,18 @@ class SessionTrie:
         base = {g: k for k, g in enumerate(self._rows)}
         return [base[int(g)] for g in self.store.session_rows(self.sid, "lex")]
 
-    def marked_nodes(self) -> list[int]:
+    def marked_node_ids(self) -> list[int]:
+        """Node ids carrying a completion mark, in lexicographic order."""
         return [k for k in self.lex_node_ids() if self._marks.get(k)]
+
+    def marked_nodes(self) -> list[TrieNode]:
+        """Marked nodes of the radix view in path order (trie.py:200-201)."""
+        nodes = self.nodes
+        return [nodes[k] for k in self.marked_node_ids()]
 
     def extract(self) -> list[tuple[int, Trajectory]]:
         """One trajectory per marked node, in lexicographic order (trie.py:210-216)."""
-        ids = self.marked_nodes()
+        ids = self.marked_node_ids()
         if not ids:
             return []
         p = self.store.export([self._rows[k] for k in ids], total=sum(self._lens[k] for k in ids))

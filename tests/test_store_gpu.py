@@ -65,6 +65,9 @@ def test_golden_cases_through_session_trie(store, trie_cases):
             assert t.tokens == p["tokens"]
             assert [int(m) for m in t.loss_mask] == p["loss_mask"] and t.version_tags == p["versions"]
         assert trie.check_well_formed() == []
+        marked = trie.marked_nodes()
+        assert [n.node_id for n in marked] == [e["row"] for e in case["extract"]]
+        assert all(n.is_marked for n in marked)
 
 
 def test_golden_cases_as_one_batch(store, trie_cases):
@@ -202,3 +205,50 @@ def test_errors_map_to_reference_exceptions(store):
         trie.path_trajectory(5)
     with pytest.raises(KeyError):
         store.session_stats(10**6)
+
+
+def test_concurrent_threads_match_oracle(store):
+    """Many Python threads recording and matching at once (the FastAPI threadpool /
+    WorkerPool pattern, trajectory.py:231): per-session results equal the oracle's and a
+    session shared by several threads holds exactly the distinct prefixes."""
+    import threading
+
+    from paper_2508_11553_b200 import SessionTrie, SpanOrigin, TrajectoryManager
+
+    rng = np.random.default_rng(11)
+    n_threads, per = 8, 40
+    work = []
+    for t in range(n_threads):
+        sids, seqs, origins, versions = _random_sessions(np.random.default_rng(100 + t), 3, per, 50, 120)
+        work.append((sids, seqs, origins, versions))
+    tries = [[SessionTrie(f"t{t}-s{s}", store=store) for s in range(3)] for t in range(n_threads)]
+    got = [[None] * per for _ in range(n_threads)]
+    tm = TrajectoryManager(type("E", (), {"current_version": 0})(), store=store)
+    shared_seqs = [[int(x) for x in rng.integers(0, 30, int(rng.integers(1, 60)))] for _ in range(n_threads * 10)]
+
+    def run(t):
+        sids, seqs, origins, versions = work[t]
+        for k in range(per):
+            org = [SpanOrigin.MODEL_OUTPUT if o else SpanOrigin.AGENT_INPUT for o in origins[k]]
+            r = tries[t][sids[k]].lpm_insert(seqs[k], org, versions[k], f"c{k}")
+            got[t][k] = (r.matched_prefix_length, r.node_id, r.added_tokens)
+            if k % 4 == 0:  # interleave shared-session records through the manager
+                for s in shared_seqs[t * 10: t * 10 + 3]:
+                    tm.record("shared", s[: max(1, len(s) // 2)], s[max(1, len(s) // 2):], [0] * (len(s) - max(1, len(s) // 2)), 0, f"r{t}-{k}")
+
+    ths = [threading.Thread(target=run, args=(t,)) for t in range(n_threads)]
+    [th.start() for th in ths]
+    [th.join() for th in ths]
+    for t in range(n_threads):
+        sids, seqs, origins, versions = work[t]
+        ora = CRadixStore()
+        om, orow, opar, oadd = ora.insert_batch(*pack_records(sids, seqs, origins, versions))
+        assert got[t] == list(zip(om.tolist(), orow.tolist(), oadd.tolist()))
+    recorded = []
+    for t in range(n_threads):
+        for k in range(0, per, 4):
+            recorded += [tuple(s) for s in shared_seqs[t * 10: t * 10 + 3]]
+    st = tm.storage_stats("shared")
+    assert st.stored_tokens == len({q[:i] for q in recorded for i in range(1, len(q) + 1)})
+    assert st.naive_tokens == sum(len(q) for q in recorded)
+    assert tm.trie_for("shared").check_well_formed() == []
