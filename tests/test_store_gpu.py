@@ -252,3 +252,38 @@ def test_concurrent_threads_match_oracle(store):
     assert st.stored_tokens == len({q[:i] for q in recorded for i in range(1, len(q) + 1)})
     assert st.naive_tokens == sum(len(q) for q in recorded)
     assert tm.trie_for("shared").check_well_formed() == []
+
+
+def test_edge_cases_long_sequences_and_extremes(store):
+    """Maximum-ish sizes and extreme values: a 1M-token history with a branch at its last
+    position, int32-extreme token ids, a batch of 2,000 identical inserts, a query equal to
+    a strict prefix, and out-of-range token ids rejected with ValueError."""
+    from paper_2508_11553_b200 import SessionTrie, SpanOrigin
+
+    rng = np.random.default_rng(5)
+    trie = SessionTrie("long", store=store)
+    L = 1 << 20
+    h = rng.integers(-(2**31), 2**31 - 1, L, dtype=np.int64).astype(np.int32)
+    h[:4] = [-(2**31), 2**31 - 1, 0, -1]
+    ins = lambda toks, c: trie.lpm_insert(toks, [SpanOrigin.MODEL_OUTPUT] * len(toks), [7] * len(toks), c)  # noqa: E731
+    r0 = ins(h, "a")
+    assert (r0.matched_prefix_length, r0.added_tokens) == (0, L)
+    b = h.copy()
+    b[-1] ^= 1
+    r1 = ins(b, "b")
+    assert (r1.matched_prefix_length, r1.added_tokens) == (L - 1, 1)
+    r2 = ins(h[: L // 2], "c")
+    assert (r2.matched_prefix_length, r2.added_tokens) == (L // 2, 0)
+    assert trie.stats().stored_tokens == L + 1
+    t = trie.path_trajectory(r1.node_id)
+    assert t.tokens == b.tolist() and t.version_tags == [7] * L
+    m, p, d = store.match([trie.sid], h, [0], [L])
+    assert m[0] == L and d[0] == trie.row_of(r0.node_id)
+    # 2,000 identical inserts in one batch: one row, naive counts all of them
+    sid = store.new_session()
+    seq = rng.integers(0, 100, 300).tolist()
+    res = store.record([sid] * 2000, [seq] * 2000, [(np.array([0]), np.array([1], np.uint8), np.array([0]))] * 2000)
+    assert res.local.tolist() == [0] * 2000 and res.added.tolist() == [300] + [0] * 1999
+    assert store.session_stats(sid) == (300, 600_000, 1)
+    with pytest.raises(ValueError):
+        trie.lpm_insert([2**31], [SpanOrigin.AGENT_INPUT], [0])
