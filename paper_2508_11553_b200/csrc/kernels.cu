@@ -741,32 +741,68 @@ __device__ __forceinline__ void put(char *dst, const char *s, int n) {
   for (int k = 0; k < n; k++) dst[k] = s[k];
 }
 
+// Copy `n` staged bytes from shared memory to out[base ...) with 4-byte aligned global
+// stores (byte stores only for the unaligned head and tail): a warp writes 128
+// contiguous bytes per instruction.
+__device__ __forceinline__ void stage_out(char *__restrict__ out, long long base, const char *buf, int n) {
+  const int head = (int)min((long long)n, (4 - (base & 3)) & 3);
+  if ((int)threadIdx.x < head) out[base + threadIdx.x] = buf[threadIdx.x];
+  const int nw = (n - head) >> 2;
+  uint32_t *dst = reinterpret_cast<uint32_t *>(out + base + head);
+  for (int w = threadIdx.x; w < nw; w += kJsonNT) {
+    const char *s = buf + head + 4 * w;
+    dst[w] = (uint32_t)(uint8_t)s[0] | ((uint32_t)(uint8_t)s[1] << 8) | ((uint32_t)(uint8_t)s[2] << 16) |
+             ((uint32_t)(uint8_t)s[3] << 24);
+  }
+  const int t0 = head + 4 * nw;
+  if ((int)threadIdx.x < n - t0) out[base + t0 + threadIdx.x] = buf[t0 + threadIdx.x];
+}
+
 __global__ void __launch_bounds__(kJsonNT) k_json_write(JsonArgs j) {
+  constexpr int kHalf = kExportTile / 2;   // a tile is printed in two halves ...
+  constexpr int kPer = kHalf / kJsonNT;    // ... of 8 positions per thread
   __shared__ long long sm[kJsonNT / 32];
+  __shared__ int s_total;
+  __shared__ char buf[kHalf * 12];         // widest half-section: 2048 x ("-2147483648,")
   for (int64_t t = blockIdx.x; t < j.ntiles; t += gridDim.x) {
     const int64_t i = json_row_of(j, t);
     const int64_t L = j.out_off[i + 1] - j.out_off[i];
     const int64_t a = (t - j.tile_off[i]) * kExportTile, b = min(a + (int64_t)kExportTile, L);
     const int64_t base = j.out_off[i];
-    // this thread's consecutive positions [pa, pb)
-    const int64_t pa = a + (int64_t)threadIdx.x * kJsonPer, pb = min(pa + kJsonPer, b);
     for (int sec = 0; sec < 2; sec++) {  // 0 tokens, 1 versions
       const int32_t *vals = sec ? j.versions : j.tokens;
-      long long mine = 0;
-      for (int64_t p = pa; p < pb; p++) mine += dec_width(vals[base + p]) + 1;
-      long long off = j.toff[3 * t + (sec ? 2 : 0)] + block_excl_scan(mine, sm);
-      for (int64_t p = pa; p < pb; p++) {
-        const int32_t v = vals[base + p];
-        const int w = dec_width(v);
-        dec_write(j.out + off, v, w);
-        if (p + 1 < L) j.out[off + w] = ',';
-        off += w + 1;
+      long long dst = j.toff[3 * t + (sec ? 2 : 0)];
+      for (int64_t h0 = a; h0 < b; h0 += kHalf) {
+        const int64_t pa = h0 + (int64_t)threadIdx.x * kPer, pb = min(pa + kPer, min(h0 + kHalf, b));
+        long long mine = 0;
+        for (int64_t p = pa; p < pb; p++) mine += dec_width(vals[base + p]) + (p + 1 < L ? 1 : 0);
+        const long long excl = block_excl_scan(mine, sm);
+        if ((int)threadIdx.x == kJsonNT - 1) s_total = (int)(excl + mine);
+        int off = (int)excl;
+        for (int64_t p = pa; p < pb; p++) {
+          const int32_t v = vals[base + p];
+          const int w = dec_width(v);
+          dec_write(buf + off, v, w);
+          if (p + 1 < L) buf[off + w] = ',';
+          off += w + 1;
+        }
+        __syncthreads();
+        const int n = s_total;
+        stage_out(j.out, dst, buf, n);
+        dst += n;
+        __syncthreads();
       }
     }
-    const long long moff = j.toff[3 * t + 1];
-    for (int64_t p = a + threadIdx.x; p < b; p += kJsonNT) {
-      j.out[moff + 2 * (p - a)] = j.mask[base + p] ? '1' : '0';
-      if (p + 1 < L) j.out[moff + 2 * (p - a) + 1] = ',';
+    // loss mask: "d," per position (no comma after the row's last)
+    for (int64_t h0 = a; h0 < b; h0 += kHalf) {
+      const int64_t h1 = min(h0 + kHalf, b);
+      for (int64_t p = h0 + threadIdx.x; p < h1; p += kJsonNT) {
+        buf[2 * (p - h0)] = j.mask[base + p] ? '1' : '0';
+        if (p + 1 < L) buf[2 * (p - h0) + 1] = ',';
+      }
+      __syncthreads();
+      stage_out(j.out, j.toff[3 * t + 1] + 2 * (h0 - a), buf, (int)(2 * (h1 - h0) - (h1 == L ? 1 : 0)));
+      __syncthreads();
     }
     if (t == j.tile_off[i] && threadIdx.x == 0) {  // fixed parts of the row
       const long long r0 = j.roff[4 * i], ts = j.roff[4 * i + 1], ms = j.roff[4 * i + 2], vs = j.roff[4 * i + 3];
@@ -776,8 +812,7 @@ __global__ void __launch_bounds__(kJsonNT) k_json_write(JsonArgs j) {
       put(j.out + ts - 11, ",\"tokens\":[", 11);
       put(j.out + ms - 15, "],\"loss_mask\":[", 15);
       put(j.out + vs - 14, "],\"versions\":[", 14);
-      const long long vend = vs + (j.roff[4 * (i + 1)] - 3 - vs);
-      put(j.out + vend, "]}\n", 3);
+      put(j.out + j.roff[4 * (i + 1)] - 3, "]}\n", 3);
     }
   }
 }
