@@ -46,5 +46,42 @@ def main():
               f"path_trajectory {t_path*1e6:8.1f} us  extract({len(ext)} rows) {t_ext*1e3:7.2f} ms")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def ingest_throughput(threads=16, per=100, L=4096):
+    """Records/s when `threads` finalizers record concurrently: per-record vs micro-batched."""
+    import threading
+
+    from paper_2508_11553_b200 import DeviceStore, TrajectoryManager
+
+    class E:
+        current_version = 0
+
+    rng = np.random.default_rng(1)
+    base = [rng.integers(0, 151936, L).tolist() for _ in range(threads)]
+    for batched in (False, True):
+        store = DeviceStore(0)
+        tm = TrajectoryManager(E(), store=store, batched_ingest=batched)
+
+        def worker(t):
+            ctx = base[t]
+            for k in range(per):
+                out = rng.integers(0, 151936, 64).tolist()
+                tm.record(f"s{t}", ctx, out, [0] * 64, 0, f"r{t}-{k}")
+                ctx = ctx[: L - 64 * 0] if k % 2 else ctx  # alternate branches / extensions
+
+        ths = [threading.Thread(target=worker, args=(t,)) for t in range(threads)]
+        t0 = time.perf_counter()
+        [x.start() for x in ths]
+        [x.join() for x in ths]
+        dt = time.perf_counter() - t0
+        tm.close()
+        print(f"ingest {'batched' if batched else 'per-record'}: {threads * per / dt:10.0f} records/s "
+              f"({threads} threads x {per} records of {L}+64 tokens)")
+        store.close()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ingest":
+    ingest_throughput()
