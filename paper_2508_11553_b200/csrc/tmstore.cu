@@ -344,7 +344,7 @@ int guarded(tm_store *s, F &&f) {
 // Stage host sequences into the pinned buffer with 128-byte aligned starts and copy
 // them to the device token scratch.  Returns device offsets (host vector).
 void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off, const int64_t *tok_len,
-                  std::vector<int64_t> &doff, const std::vector<int64_t> *perm) {
+                  std::vector<int64_t> &doff, const std::vector<int64_t> *perm, cudaStream_t st) {
   doff.resize(n);
   // Fast path: every sequence already starts on a 128-byte boundary -> one direct
   // H2D copy of the caller's buffer (pinned buffers go at full PCIe rate).  Padding
@@ -358,7 +358,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
   if (aligned) {
     for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm ? (*perm)[k] : k];
     void *d = s->dtok.need(sizeof(int32_t) * (size_t)(round_up(std::max<int64_t>(end, 1), tms::kAlignWords) + tms::kAlignWords));
-    if (end > 0) ck(cudaMemcpyAsync(d, tokens, sizeof(int32_t) * end, cudaMemcpyHostToDevice, s->stream), "H2D tokens");
+    if (end > 0) ck(cudaMemcpyAsync(d, tokens, sizeof(int32_t) * end, cudaMemcpyHostToDevice, st), "H2D tokens");
     return;
   }
   int64_t total = 0;
@@ -376,7 +376,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
     memset(h + doff[k] + L, 0, sizeof(int32_t) * (size_t)pad);
   }
   void *d = s->dtok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
-  if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, s->stream), "H2D tokens");
+  if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, st), "H2D tokens");
 }
 
 void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, int64_t r, std::vector<int64_t> &out) {
@@ -632,7 +632,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm[k]];
       tok_base = tokens;
     } else {
-      stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm);
+      stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm, s->stream);
       tok_base = (const int32_t *)s->dtok.p;
     }
     Layout lay;
@@ -772,11 +772,7 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
       for (int64_t k = 0; k < n; k++)
         if (sids[k] < 0 || sids[k] >= s->n_sess) fail(TM_ENOENT, "unknown session " + std::to_string(sids[k]));
       std::vector<int64_t> doff;
-      // stage on the chosen stream
-      cudaStream_t keep = s->stream;
-      s->stream = st;
-      stage_tokens(s, n, tokens, tok_off, tok_len, doff, nullptr);
-      s->stream = keep;
+      stage_tokens(s, n, tokens, tok_off, tok_len, doff, nullptr, st);
       char *h = (char *)s->pin.need(lay.bytes);
       memcpy(h + o_sid, sids, 4 * n);
       memcpy(h + o_off, doff.data(), 8 * n);

@@ -69,8 +69,7 @@ def ingest_throughput(threads=16, per=100, L=4096):
             ctx = base[t]
             for k in range(per):
                 out = rng.integers(0, 151936, 64).tolist()
-                tm.record(f"s{t}", ctx, out, [0] * 64, 0, f"r{t}-{k}")
-                ctx = ctx[: L - 64 * 0] if k % 2 else ctx  # alternate branches / extensions
+                tm.record(f"s{t}", ctx, out, [0] * 64, 0, f"r{t}-{k}")  # branches off a shared context
 
         ths = [threading.Thread(target=worker, args=(t,)) for t in range(threads)]
         t0 = time.perf_counter()
@@ -84,4 +83,5 @@ def ingest_throughput(threads=16, per=100, L=4096):
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ingest":
-    ingest_throughput()
+    for L in (256, 4096):
+        ingest_throughput(L=L)
