@@ -287,3 +287,33 @@ def test_edge_cases_long_sequences_and_extremes(store):
     assert store.session_stats(sid) == (300, 600_000, 1)
     with pytest.raises(ValueError):
         trie.lpm_insert([2**31], [SpanOrigin.AGENT_INPUT], [0])
+
+
+def test_hypothesis_naive_oracle_property(store):
+    """pkg/tests/test_trie.py:148-174 on the GPU trie: matched == max LCP (the NaiveStore
+    oracle), storage == distinct prefixes, every sequence reconstructible, well formed."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    from paper_2508_11553_b200 import SessionTrie, SpanOrigin
+
+    seqs_st = st.lists(st.lists(st.integers(0, 5), min_size=1, max_size=12), min_size=1, max_size=25)
+
+    @given(seqs=seqs_st)
+    @settings(max_examples=120, deadline=None)
+    def prop(seqs):
+        trie = SessionTrie("h", store=store)
+        seen = []
+        for n, seq in enumerate(seqs):
+            want = max([next((i for i, (a, b) in enumerate(zip(s, seq)) if a != b), min(len(s), len(seq)))
+                        for s in seen] or [0])
+            r = trie.lpm_insert(seq, [SpanOrigin.MODEL_OUTPUT] * len(seq), [0] * len(seq), f"c{n}")
+            assert r.matched_prefix_length == want
+            seen.append(tuple(seq))
+        st_ = trie.stats()
+        assert st_.stored_tokens == len({s[:i] for s in seen for i in range(1, len(s) + 1)})
+        assert st_.naive_tokens == sum(map(len, seen))
+        assert {tuple(t.tokens) for _, t in trie.extract()} == set(seen)
+        assert trie.check_well_formed() == []
+
+    prop()
