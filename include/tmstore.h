@@ -144,6 +144,10 @@ int tm_row_info(tm_store *store, int64_t row, int32_t *sid, int32_t *local, int6
 int tm_store_stats(tm_store *store, int64_t *rows, int64_t *arena_used, int64_t *arena_cap,
                    int64_t *max_depth);
 
+/* Observability counters since creation: record calls, records, recorded tokens,
+ * match calls, queries, export calls, exported rows, exported tokens (8 int64). */
+int tm_store_counters(tm_store *store, int64_t *out8);
+
 /* The store's CUDA stream (cudaStream_t) for callers that want to order work after it. */
 int tm_store_stream(tm_store *store, void **out_stream);
 

@@ -42,6 +42,7 @@ SIGNATURES = {
     "tm_row_info": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "tm_store_stats": (C.c_int, [_P, _P, _P, _P, _P]),
     "tm_store_stream": (C.c_int, [_P, _P]),
+    "tm_store_counters": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
     "tm_store_save": (C.c_int, [_P, C.c_char_p]),

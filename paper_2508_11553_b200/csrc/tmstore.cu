@@ -6,6 +6,7 @@
 // staging for host-memory calls, and one CUDA stream.  Every entry point locks the
 // store mutex; ctypes callers release the GIL around the call.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstddef>
@@ -116,6 +117,9 @@ struct tm_store {
   int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
   int64_t arena_used = 0, n_runs = 0, n_sess = 0;
   int64_t n_real_rows = 0;  // rows minus reserved-but-unused slots
+  // observability counters (tm_store_counters)
+  int64_t c_record_calls = 0, c_records = 0, c_record_tokens = 0, c_match_calls = 0, c_queries = 0,
+          c_export_calls = 0, c_export_rows = 0, c_export_tokens = 0;
   std::vector<uint64_t> chain_stamp;  // record: per-session batch stamp and chain slot
   std::vector<int32_t> chain_slot;
   uint64_t batch_stamp = 0;
@@ -320,6 +324,12 @@ void wait_prev(tm_store *s, cudaStream_t st) {
 }
 
 void mark_done(tm_store *s, cudaStream_t st) { ck(cudaEventRecord(s->last, st), "cudaEventRecord"); }
+
+// NVTX range around every C-ABI call (visible in nsys / ncu timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 int guarded(tm_store *s, F &&f) {
@@ -554,6 +564,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                     const int32_t *run_start, const uint8_t *run_origin, const int32_t *run_version,
                     int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
                     int32_t *out_parent_local, int64_t *out_added, void *stream) {
+  NvtxRange nvtx_("tm_record_batch");
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
@@ -739,17 +750,23 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     }
     s->arena_used = ctr[0];
     s->n_runs = ctr[2];
+    s->c_record_calls++;
+    s->c_records += n;
+    for (int64_t e = 0; e < n; e++) s->c_record_tokens += tok_len[e];
   });
 }
 
 int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
                    const int64_t *tok_off, const int64_t *tok_len, int64_t *out_matched, int64_t *out_parent,
                    int64_t *out_dup, void *stream) {
+  NvtxRange nvtx_("tm_match_batch");
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
     const bool dev = mem == TM_MEM_DEVICE;
+    s->c_match_calls++;
+    s->c_queries += n;
     tm_store::MatchSlot *slot = nullptr;
     if (dev) {  // read-only, device buffers: may overlap other device matches, not mutations
       slot = &s->slots[s->next_slot++ % tm_store::kSlots];
@@ -835,6 +852,7 @@ int tm_rows_total(tm_store *s, int64_t n, const int64_t *rows, int64_t *out_tota
 int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out, int64_t *out_offsets,
                    int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
                    void *stream) {
+  NvtxRange nvtx_("tm_export_rows");
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (mem_out != TM_MEM_HOST && mem_out != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
@@ -850,6 +868,9 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       tile[k + 1] = tile[k] + (L + T - 1) / T;
     }
     const int64_t total = out_offsets[n];
+    s->c_export_calls++;
+    s->c_export_rows += n;
+    s->c_export_tokens += total;
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
     wait_prev(s, st);
     Layout lay;
@@ -912,6 +933,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
 
 int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *sid_json, const int64_t *sid_off,
                      int32_t mem_out, char *out, int64_t cap, int64_t *out_bytes, void *stream) {
+  NvtxRange nvtx_("tm_export_ndjson");
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (mem_out != TM_MEM_HOST && mem_out != TM_MEM_DEVICE) fail(TM_EINVAL, "bad memory kind");
@@ -1084,6 +1106,14 @@ int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *are
   });
 }
 
+int tm_store_counters(tm_store *s, int64_t *out8) {
+  return guarded(s, [&] {
+    const int64_t c[8] = {s->c_record_calls, s->c_records, s->c_record_tokens, s->c_match_calls,
+                          s->c_queries, s->c_export_calls, s->c_export_rows, s->c_export_tokens};
+    memcpy(out8, c, sizeof(c));
+  });
+}
+
 int tm_store_stream(tm_store *s, void **out_stream) {
   return guarded(s, [&] { *out_stream = (void *)s->stream; });
 }
@@ -1126,6 +1156,7 @@ int tm_route_desc_bytes(int64_t *out_bytes) {
 }
 
 int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, void *stream) {
+  NvtxRange nvtx_("tm_route_prepare");
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks) fail(TM_EINVAL, "nranks out of range");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
@@ -1148,6 +1179,7 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
 
 int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
                     void *stream) {
+  NvtxRange nvtx_("tm_match_routed");
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
@@ -1171,6 +1203,7 @@ int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer
 
 
 int tm_store_save(tm_store *s, const char *path) {
+  NvtxRange nvtx_("tm_store_save");
   return guarded(s, [&] {
     wait_prev(s, s->stream);
     ck(cudaStreamSynchronize(s->stream), "snapshot sync");
@@ -1206,6 +1239,7 @@ int tm_store_save(tm_store *s, const char *path) {
 }
 
 int tm_store_load(tm_store *s, const char *path) {
+  NvtxRange nvtx_("tm_store_load");
   return guarded(s, [&] {
     if (s->n_sess || !s->rows.empty()) fail(TM_EINVAL, "restore needs an empty store");
     FILE *f = fopen(path, "rb");

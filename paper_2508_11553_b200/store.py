@@ -114,6 +114,14 @@ class DeviceStore:
         check(self.lib.tm_store_stats(self.h, C.byref(r), C.byref(u), C.byref(c), C.byref(d)))
         return dict(rows=r.value, arena_used=u.value, arena_cap=c.value, max_depth=d.value)
 
+    def counters(self) -> dict:
+        """Calls / items / tokens seen by this store (observability)."""
+        c = np.zeros(8, np.int64)
+        check(self.lib.tm_store_counters(self.h, _ptr(c)))
+        keys = ("record_calls", "records", "record_tokens", "match_calls", "queries", "export_calls", "export_rows",
+                "export_tokens")
+        return dict(zip(keys, c.tolist()))
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(self.lib.tm_store_stream(self.h, C.byref(s)))
