@@ -39,6 +39,7 @@ def main():
         for k in range(20):
             trie.path_trajectory(k)
         t_path = (time.perf_counter() - t0) / 20
+        trie.extract()  # warm: first call at a new size grows the staging buffers
         t0 = time.perf_counter()
         ext = trie.extract()
         t_ext = time.perf_counter() - t0
