@@ -389,32 +389,52 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
   if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, st), "H2D tokens");
 }
 
-void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, int64_t r, std::vector<int64_t> &out) {
-  // kids[local] = children of that row sorted by (m, prefix-first, tnext).  Order of
-  // the subtree of r:
-  //   for each branch depth d < len(r), ascending: [prefix row at d] + [children whose
-  //   token at d is below r's token at d] ... then r itself, then its extensions,
-  //   then, deepest depth first, the children whose token at d is above r's.
-  const RowHost &R = s->rows[r];
-  const auto &ch = kids[R.local];
+// Lexicographic order of the subtree of row r.  kids[local] =
+// children of that row sorted by (m, prefix-first, tnext).  For each branch depth d <
+// len(r), ascending: [prefix row at d] + [subtrees of children whose token at d is below
+// r's] ... then r itself, its extensions, and, deepest depth first, the subtrees of the
+// children whose token at d is above r's.  Iterative (an explicit action stack): chains of
+// thousands of turns must not exhaust the native stack.
+void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, int64_t root, std::vector<int64_t> &out) {
+  struct Act {
+    int64_t row;
+    bool recurse;
+  };
+  std::vector<Act> stack{{root, true}};
+  std::vector<Act> acts;
   std::vector<int64_t> hi_list;
   std::vector<size_t> hi_mark;
-  size_t i = 0;
-  while (i < ch.size() && s->rows[ch[i]].m < R.len) {
-    const int32_t d = s->rows[ch[i]].m;
-    hi_mark.push_back(hi_list.size());
-    for (; i < ch.size() && s->rows[ch[i]].m == d; i++) {
-      const RowHost &C = s->rows[ch[i]];
-      if (C.len == C.m) out.push_back(ch[i]);
-      else if (C.tnext < C.spar) lex_emit(s, kids, ch[i], out);
-      else hi_list.push_back(ch[i]);
+  while (!stack.empty()) {
+    const Act act = stack.back();
+    stack.pop_back();
+    if (!act.recurse) {
+      out.push_back(act.row);
+      continue;
     }
-  }
-  out.push_back(r);
-  for (; i < ch.size(); i++) lex_emit(s, kids, ch[i], out);
-  for (size_t g = hi_mark.size(); g-- > 0;) {
-    const size_t a = hi_mark[g], b = (g + 1 < hi_mark.size()) ? hi_mark[g + 1] : hi_list.size();
-    for (size_t k = a; k < b; k++) lex_emit(s, kids, hi_list[k], out);
+    const int64_t r = act.row;
+    const RowHost &R = s->rows[r];
+    const auto &ch = kids[R.local];
+    acts.clear();
+    hi_list.clear();
+    hi_mark.clear();
+    size_t i = 0;
+    while (i < ch.size() && s->rows[ch[i]].m < R.len) {
+      const int32_t d = s->rows[ch[i]].m;
+      hi_mark.push_back(hi_list.size());
+      for (; i < ch.size() && s->rows[ch[i]].m == d; i++) {
+        const RowHost &C = s->rows[ch[i]];
+        if (C.len == C.m) acts.push_back({ch[i], false});
+        else if (C.tnext < C.spar) acts.push_back({ch[i], true});
+        else hi_list.push_back(ch[i]);
+      }
+    }
+    acts.push_back({r, false});
+    for (; i < ch.size(); i++) acts.push_back({ch[i], true});
+    for (size_t g = hi_mark.size(); g-- > 0;) {
+      const size_t a0 = hi_mark[g], b0 = (g + 1 < hi_mark.size()) ? hi_mark[g + 1] : hi_list.size();
+      for (size_t k = a0; k < b0; k++) acts.push_back({hi_list[k], true});
+    }
+    for (size_t k = acts.size(); k-- > 0;) stack.push_back(acts[k]);
   }
 }
 
@@ -518,29 +538,28 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
 
 int tm_store_destroy(tm_store *s) {
   if (!s) return TM_OK;
-  {
-    DeviceGuard dg(s->device);
-    cudaStreamSynchronize(s->stream);
-    void *ptrs[] = {s->v.arena, s->v.row_vb, s->v.row_m, s->v.row_len, s->v.row_parent, s->v.row_sess,
-                    s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.run_start,
-                    s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
-                    s->v.s_stored, s->v.s_naive, s->v.ctr, s->sched};
-    for (void *p : ptrs)
-      if (p) cudaFree(p);
-    s->scratch.~DevBytes();
-    new (&s->scratch) DevBytes();
-    s->dtok.~DevBytes();
-    new (&s->dtok) DevBytes();
-    for (auto &sl : s->slots) {
-      cudaEventDestroy(sl.done);
-      if (sl.sched) cudaFree(sl.sched);
-      sl.scratch.~DevBytes();
-      new (&sl.scratch) DevBytes();
-    }
-    cudaEventDestroy(s->last);
-    cudaStreamDestroy(s->stream);
+  DeviceGuard dg(s->device);  // member destructors free device memory on the store's GPU
+  cudaStreamSynchronize(s->stream);
+  for (auto &sl : s->slots)
+    if (sl.used) cudaEventSynchronize(sl.done);
+  void *ptrs[] = {s->v.arena, s->v.row_vb, s->v.row_m, s->v.row_len, s->v.row_parent, s->v.row_sess,
+                  s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.run_start,
+                  s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
+                  s->v.s_stored, s->v.s_naive, s->v.ctr, s->sched};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  for (auto &sl : s->slots) {
+    cudaEventDestroy(sl.done);
+    if (sl.sched) cudaFree(sl.sched);
   }
-  delete s;
+  for (int k = 0; k < 4; k++)
+    for (auto &e : s->ev[k]) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  cudaEventDestroy(s->last);
+  cudaStreamDestroy(s->stream);
+  delete s;  // DevBytes / PinBytes members release scratch and pinned staging
   return TM_OK;
 }
 
