@@ -63,6 +63,8 @@ struct WalkOut {
 struct WalkShared {
   int red[32];
   long long row;
+  long long nvb;  // next row's virtual base / length (from the hint or one probe)
+  int nlen;
   int lo;
 };
 
@@ -87,18 +89,38 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
   int64_t r = sh.row;
   int lo = sh.lo;
   __syncthreads();
+  int Lr = 0;
+  int64_t vb = 0;
+  if (r >= 0) {
+    Lr = v.row_len[r];
+    vb = v.row_vb[r];
+  }
   while (r >= 0) {
     TM_DCHECK(v, r < v.row_cap, kErrRow);
-    const int Lr = v.row_len[r];
     const int hi = min(Lr, L);
-    TM_DCHECK(v, v.row_vb[r] + v.row_m[r] >= 0 && v.row_vb[r] + ((Lr + 3) & ~3) <= v.arena_cap, kErrArena);
-    const int32_t *a = v.arena + v.row_vb[r];
+    TM_DCHECK(v, vb + v.row_m[r] >= 0 && vb + ((Lr + 3) & ~3) <= v.arena_cap, kErrArena);
+    const int32_t *a = v.arena + vb;
+    // the extension hint is read before the compare so a turn-by-turn chain hops for free
+    int64_t ext = -1;
+    int32_t ext_tok = 0, ext_len = 0;
+    int64_t ext_vb = 0;
+    if (threadIdx.x == 0) {
+      ext = v.row_ext[r];
+      if (ext >= 0) { ext_tok = v.row_ext_tok[r]; ext_len = v.row_ext_len[r]; ext_vb = v.row_ext_vb[r]; }
+    }
     const int j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
     if (threadIdx.x == 0) {
       int64_t next = -1;
       if (j < L) {
         const int32_t t = q[j];
-        next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
+        if (j == Lr && ext >= 0 && t == ext_tok) {
+          next = ext;
+          sh.nlen = ext_len;
+          sh.nvb = ext_vb;
+        } else {
+          next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
+          if (next >= 0) { sh.nlen = v.row_len[next]; sh.nvb = v.row_vb[next]; }
+        }
         if (next < 0) {
           *o.m = j;
           *o.parent = r;
@@ -118,6 +140,8 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
     __syncthreads();
     r = sh.row;
     lo = sh.lo;
+    Lr = sh.nlen;
+    vb = sh.nvb;
     __syncthreads();
   }
 }
@@ -137,8 +161,10 @@ __device__ __forceinline__ void sched_exit(Sched *sc) {
   }
 }
 
+// 64-thread CTAs: ask for 6 resident per SM (<= 170 registers) so the walk keeps 6 CTAs
+// of loads in flight per SM
 template <int NT, int U>
-__global__ void __launch_bounds__(NT) k_walk(DevView v, Batch b) {
+__global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk(DevView v, Batch b) {
   __shared__ WalkShared sh;
   __shared__ long long s_item;
   __shared__ int s_base[kPlanNB + 1];
@@ -247,7 +273,7 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
 // queue and the rest on the remote one, each falling back to the other when its queue
 // runs dry, so HBM and the links are busy at the same time instead of in phases.
 template <int NT, int U>
-__global__ void __launch_bounds__(NT) k_walk_routed(DevView v, RoutedArgs a) {
+__global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v, RoutedArgs a) {
   __shared__ WalkShared sh;
   __shared__ long long s_item;
   __shared__ int s_cell;
@@ -393,6 +419,23 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
       v.row_depth[row] = par >= 0 ? v.row_depth[par] + 1 : 0;
       v.row_run0[row] = b.c_run0[e];
       v.row_nrun[row] = L > m ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
+      v.row_ext[row] = -1;
+      // skew-binary jump pointer (Myers): O(1) here, O(log depth) ancestor searches
+      int64_t jmp = -1;
+      if (par >= 0) {
+        const int64_t j1 = v.row_jump[par];
+        const int64_t j2 = j1 >= 0 ? v.row_jump[j1] : -1;
+        const int32_t d1 = j1 >= 0 ? v.row_depth[j1] : -1, d2 = j2 >= 0 ? v.row_depth[j2] : -1;
+        jmp = (j1 >= 0 && v.row_depth[par] - d1 == d1 - d2) ? j2 : par;
+        if (L > m && m == v.row_len[par] && v.row_ext[par] < 0) {  // the parent's extension hint
+          v.row_ext_tok[par] = b.tok[b.off[e] + m];
+          v.row_ext_len[par] = (int32_t)L;
+          v.row_ext_vb[par] = b.c_vb[e];
+          __threadfence();
+          v.row_ext[par] = row;
+        }
+      }
+      v.row_jump[row] = jmp;
       v.s_stored[sid] += L - m;
       const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
       if (L > m) ht_insert(v, owner, dt_key(m, b.tok[b.off[e] + m], false), row);
@@ -556,6 +599,13 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
     const int64_t a = (t - e.tile_off[lo]) * kExportTile;
     const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
     int64_t cur = row, upper = v.row_len[row];
+    // climb to the owner of position b-1 with jump pointers (O(log depth)); its range
+    // ends at or after b, so the tile's first piece ends at b
+    while (v.row_m[cur] > b - 1) {
+      const int64_t jp = v.row_jump[cur];
+      cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
+      upper = b;
+    }
     int np = 0;
     ExportPiece *out = e.pieces + t * kMaxPieces;
     while (cur >= 0 && upper > a) {

@@ -24,6 +24,12 @@ struct DevView {
   int32_t *row_depth;
   int64_t *row_run0;   // first metadata run
   int32_t *row_nrun;
+  // navigation hints (written once, at the child's commit)
+  int64_t *row_ext;      // first child extending this row exactly at its end (-1: none) ...
+  int32_t *row_ext_tok;  // ... its first own token,
+  int32_t *row_ext_len;  // ... its length,
+  int64_t *row_ext_vb;   // ... its virtual base: a multi-turn walk hops without a hash probe
+  int64_t *row_jump;     // skew-binary jump pointer to an ancestor (O(log depth) ancestor search)
   // metadata runs (absolute start positions within the row's sequence)
   int32_t *run_start;
   int32_t *run_version;

@@ -181,6 +181,11 @@ void ensure_rows(tm_store *s, int64_t need) {
   dev_grow(s->v.row_depth, n, nc, s->stream);
   dev_grow(s->v.row_run0, n, nc, s->stream);
   dev_grow(s->v.row_nrun, n, nc, s->stream);
+  dev_grow(s->v.row_ext, n, nc, s->stream);
+  dev_grow(s->v.row_ext_tok, n, nc, s->stream);
+  dev_grow(s->v.row_ext_len, n, nc, s->stream);
+  dev_grow(s->v.row_ext_vb, n, nc, s->stream);
+  dev_grow(s->v.row_jump, n, nc, s->stream);
   s->row_cap = nc;
   s->v.row_cap = nc;
 }
@@ -442,7 +447,7 @@ void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, 
 
 // ---- snapshot / restore -----------------------------------------------------------------
 namespace {
-constexpr char kMagic[8] = {'T', 'M', 'S', 'T', 'O', 'R', 'E', '1'};
+constexpr char kMagic[8] = {'T', 'M', 'S', 'T', 'O', 'R', 'E', '2'};
 
 struct FileW {
   FILE *f;
@@ -543,7 +548,8 @@ int tm_store_destroy(tm_store *s) {
   for (auto &sl : s->slots)
     if (sl.used) cudaEventSynchronize(sl.done);
   void *ptrs[] = {s->v.arena, s->v.row_vb, s->v.row_m, s->v.row_len, s->v.row_parent, s->v.row_sess,
-                  s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.run_start,
+                  s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.row_ext,
+                  s->v.row_ext_tok, s->v.row_ext_len, s->v.row_ext_vb, s->v.row_jump, s->v.run_start,
                   s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
                   s->v.s_stored, s->v.s_naive, s->v.ctr, s->sched};
   for (void *p : ptrs)
@@ -1244,6 +1250,9 @@ int tm_store_save(tm_store *s, const char *path) {
       save_dev(s, w, s->v.row_parent, nrows); save_dev(s, w, s->v.row_sess, nrows);
       save_dev(s, w, s->v.row_local, nrows); save_dev(s, w, s->v.row_depth, nrows);
       save_dev(s, w, s->v.row_run0, nrows); save_dev(s, w, s->v.row_nrun, nrows);
+      save_dev(s, w, s->v.row_ext, nrows); save_dev(s, w, s->v.row_ext_tok, nrows);
+      save_dev(s, w, s->v.row_ext_len, nrows); save_dev(s, w, s->v.row_ext_vb, nrows);
+      save_dev(s, w, s->v.row_jump, nrows);
       save_dev(s, w, s->v.run_start, s->n_runs); save_dev(s, w, s->v.run_version, s->n_runs);
       save_dev(s, w, s->v.run_origin, s->n_runs);
       save_dev(s, w, s->v.s_nrows, s->n_sess); save_dev(s, w, s->v.s_stored, s->n_sess);
@@ -1292,6 +1301,9 @@ int tm_store_load(tm_store *s, const char *path) {
       load_dev(s, r, s->v.row_parent, nrows); load_dev(s, r, s->v.row_sess, nrows);
       load_dev(s, r, s->v.row_local, nrows); load_dev(s, r, s->v.row_depth, nrows);
       load_dev(s, r, s->v.row_run0, nrows); load_dev(s, r, s->v.row_nrun, nrows);
+      load_dev(s, r, s->v.row_ext, nrows); load_dev(s, r, s->v.row_ext_tok, nrows);
+      load_dev(s, r, s->v.row_ext_len, nrows); load_dev(s, r, s->v.row_ext_vb, nrows);
+      load_dev(s, r, s->v.row_jump, nrows);
       load_dev(s, r, s->v.run_start, nruns); load_dev(s, r, s->v.run_version, nruns);
       load_dev(s, r, s->v.run_origin, nruns);
       load_dev(s, r, s->v.s_nrows, nsess); load_dev(s, r, s->v.s_stored, nsess);
