@@ -427,11 +427,12 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
         const int64_t j2 = j1 >= 0 ? v.row_jump[j1] : -1;
         const int32_t d1 = j1 >= 0 ? v.row_depth[j1] : -1, d2 = j2 >= 0 ? v.row_depth[j2] : -1;
         jmp = (j1 >= 0 && v.row_depth[par] - d1 == d1 - d2) ? j2 : par;
-        if (L > m && m == v.row_len[par] && v.row_ext[par] < 0) {  // the parent's extension hint
+        // the parent's extension hint; its only readers are this CTA's later entries (same
+        // session chain) and later launches, so program order suffices
+        if (L > m && m == v.row_len[par] && v.row_ext[par] < 0) {
           v.row_ext_tok[par] = b.tok[b.off[e] + m];
           v.row_ext_len[par] = (int32_t)L;
           v.row_ext_vb[par] = b.c_vb[e];
-          __threadfence();
           v.row_ext[par] = row;
         }
       }
