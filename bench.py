@@ -54,6 +54,8 @@ def parse():
                     help="c4 (default): per-rank 10k x 32k shard, host-routed; c5: 1M-session store sharded "
                          "by session hash with GPU-originated batches routed over NVLink (fused P2P K1)")
     ap.add_argument("--c5-sessions", type=int, default=1_000_000)
+    ap.add_argument("--routing", default="fused", choices=["fused", "nccl"],
+                    help="c5 exchange: fused P2P K1 (product) or NCCL all-to-all + local match (baseline)")
     ap.add_argument("--mixed", default=None,
                     help="lo,hi: log-uniform history lengths (config-5 shard) instead of fixed --hist")
     return ap.parse_args()
@@ -212,8 +214,9 @@ def run_c5(args):
     router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
     wl.fill_queries(router)
     torch.cuda.synchronize()
+    route = router.match if args.routing == "fused" else router.match_nccl
     for _ in range(max(3, args.warmup)):
-        router.match(wl.n_queries)
+        route(wl.n_queries)
     torch.cuda.synchronize()
     m = router.out_matched[: wl.n_queries].cpu().numpy()
     bad = np.flatnonzero(m != wl.q_depth)
@@ -232,13 +235,13 @@ def run_c5(args):
         store.profile_begin()
         e0.record(stream)
         for _ in range(args.steps):
-            router.match(wl.n_queries)
+            route(wl.n_queries)
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
         while time.perf_counter() - t_wall < 1.0:
             for _ in range(10):
-                router.match(wl.n_queries)
+                route(wl.n_queries)
             torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
@@ -260,7 +263,9 @@ def run_c5(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": "c5", "sessions_total": args.c5_sessions, "history_tokens": "log-uniform [1024, 131072]",
                    "batch_queries_per_rank": wl.n_queries, "owner": "splitmix64(gsid) mod N",
-                   "routing": "fused P2P K1: owners read requester HBM over NVLink, write results back",
+                   "routing": ("fused P2P K1: owners read requester HBM over NVLink, write results back"
+                               if args.routing == "fused" else
+                               "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"),
                    "cross_shard_frac": float(remote.mean()), "shard_build_s": build_s,
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,

@@ -171,6 +171,8 @@ int tm_ipc_open(tm_store *store, const void *handle64, void **out_ptr);
 int tm_ipc_close(tm_store *store, void *ptr);
 int tm_route_prepare(tm_store *store, void *region, int64_t n, const int64_t *offsets, int32_t nranks,
                      void *stream);
+/* Per-owner query counts of a prepared region (kMaxRanks = 16 int32; synchronous). */
+int tm_route_counts(tm_store *store, const void *region, int32_t *out_counts16, void *stream);
 /* g2l: device int32[global sessions] -> this store's session id (-1 if not owned).
  * peer_regions: host array of nranks device pointers (this rank's own region at [rank]). */
 int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,

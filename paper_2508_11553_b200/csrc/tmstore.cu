@@ -1202,6 +1202,15 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
   });
 }
 
+int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *stream) {
+  return guarded(s, [&] {
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    ck(cudaMemcpyAsync(out_counts, (const char *)region + offsetof(tms::RouteDesc, count), sizeof(int32_t) * tms::kMaxRanks,
+                       cudaMemcpyDeviceToHost, st), "D2H route counts");
+    ck(cudaStreamSynchronize(st), "route counts sync");
+  });
+}
+
 int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
                     void *stream) {
   NvtxRange nvtx_("tm_match_routed");

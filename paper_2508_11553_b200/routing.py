@@ -139,6 +139,55 @@ class Router:
         if self.nranks > 1:
             self._barrier()
 
+    def match_nccl(self, n: int):
+        """BASELINE for comparison, not the product path: the same exchange done with
+        NCCL collectives only — all-to-all of the query tokens to their owners, a local
+        match there, all-to-all of the results back (with the host reading the split
+        sizes in between).  Results land in out_matched / out_parent / out_dup."""
+        import torch
+        import torch.distributed as dist
+
+        dev = self.gsid.device
+        st = torch.cuda.current_stream(self.store.device).cuda_stream
+        st = C.c_void_p(1 if st == 0 else st)
+        lib, h = self.store.lib, self.store.h
+        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, st))
+        cnt = np.zeros(16, np.int32)
+        check(lib.tm_route_counts(h, C.c_void_p(self.base), cnt.ctypes.data_as(C.c_void_p), st))
+        counts = cnt[: self.nranks].astype(np.int64)
+        idx = torch.as_tensor(_CudaArray(self.base + self.offsets[4], (n,), "<i4"), device=dev).long()
+        lens = self.qlen[:n][idx]
+        pad = (lens + 31) // 32 * 32
+        starts = self.qoff[:n][idx]
+        tok_per_owner = torch.zeros(self.nranks, dtype=torch.int64, device=dev)
+        owner_of_q = torch.repeat_interleave(torch.arange(self.nranks, device=dev), torch.as_tensor(counts, device=dev))
+        tok_per_owner.index_add_(0, owner_of_q, pad)
+        gather = torch.repeat_interleave(starts, pad) + (
+            torch.arange(int(pad.sum()), device=dev) - torch.repeat_interleave(torch.cumsum(pad, 0) - pad, pad))
+        send_tok = self.tokens[gather]
+        meta = torch.stack([torch.as_tensor(counts, device=dev), tok_per_owner], 1).contiguous()
+        rmeta = torch.empty_like(meta)
+        dist.all_to_all_single(rmeta, meta, group=self.group)
+        rm = rmeta.cpu().numpy()
+        q_in, t_in = rm[:, 0].tolist(), rm[:, 1].tolist()
+        q_out, t_out = counts.tolist(), tok_per_owner.tolist()
+        recv_tok = torch.empty(sum(t_in), dtype=torch.int32, device=dev)
+        dist.all_to_all_single(recv_tok, send_tok, t_in, t_out, group=self.group)
+        send_ql = torch.stack([self.gsid[:n][idx], lens], 1).contiguous()
+        recv_ql = torch.empty((sum(q_in), 2), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv_ql, send_ql, q_in, q_out, group=self.group)
+        rl = recv_ql[:, 1]
+        rpad = (rl + 31) // 32 * 32
+        roff = torch.cumsum(rpad, 0) - rpad
+        sids = self.g2l[recv_ql[:, 0]]
+        res = torch.empty((sum(q_in), 3), dtype=torch.int64, device=dev)
+        self.store.match_device(sids, recv_tok, roff, rl, res[:, 0], res[:, 1], res[:, 2])
+        back = torch.empty((n, 3), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(back, res.contiguous(), q_out, q_in, group=self.group)
+        self.out_matched[:n][idx] = back[:, 0]
+        self.out_parent[:n][idx] = back[:, 1]
+        self.out_dup[:n][idx] = back[:, 2]
+
     def close(self):
         lib, h = self.store.lib, self.store.h
         for p, ptr in enumerate(self.peers):

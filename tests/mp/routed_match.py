@@ -32,6 +32,12 @@ torch.cuda.synchronize()
 m = router.out_matched[: wl.n_queries].cpu().numpy()
 par = router.out_parent[: wl.n_queries].cpu().numpy()
 ok = np.array_equal(m, wl.q_depth) and bool(np.all((par >= 0) | (m == 0)))
+# the NCCL-only baseline exchange must agree exactly with the fused path
+router.out_matched.fill_(-7)
+router.match_nccl(wl.n_queries)
+torch.cuda.synchronize()
+ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
+ok = ok and np.array_equal(router.out_parent[: wl.n_queries].cpu().numpy(), par)
 remote = float(np.mean(wl.owner[wl.q_g] != rank))
 flag = torch.tensor([1 if ok else 0], device=dev)
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
