@@ -180,10 +180,11 @@ class Router:
         rpad = (rl + 31) // 32 * 32
         roff = torch.cumsum(rpad, 0) - rpad
         sids = self.g2l[recv_ql[:, 0]]
-        res = torch.empty((sum(q_in), 3), dtype=torch.int64, device=dev)
-        self.store.match_device(sids, recv_tok, roff, rl, res[:, 0], res[:, 1], res[:, 2])
+        m_, p_, d_ = (torch.empty(sum(q_in), dtype=torch.int64, device=dev) for _ in range(3))
+        self.store.match_device(sids, recv_tok, roff.contiguous(), rl.contiguous(), m_, p_, d_)
+        res = torch.stack([m_, p_, d_], 1).contiguous()
         back = torch.empty((n, 3), dtype=torch.int64, device=dev)
-        dist.all_to_all_single(back, res.contiguous(), q_out, q_in, group=self.group)
+        dist.all_to_all_single(back, res, q_out, q_in, group=self.group)
         self.out_matched[:n][idx] = back[:, 0]
         self.out_parent[:n][idx] = back[:, 1]
         self.out_dup[:n][idx] = back[:, 2]
