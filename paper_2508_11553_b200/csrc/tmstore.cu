@@ -45,14 +45,25 @@ void ck(cudaError_t e, const char *what) {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// Grow a device array to new_n elements (at least need_n): try the doubled size first and
+// fall back to exactly what is needed when HBM is tight (a 100 GB arena cannot double).
+// Returns the capacity actually allocated.
 template <class T>
-void dev_grow(T *&p, int64_t old_n, int64_t new_n, cudaStream_t s) {
+int64_t dev_grow(T *&p, int64_t old_n, int64_t new_n, cudaStream_t s, int64_t need_n = -1) {
   T *q = nullptr;
-  ck(cudaMalloc((void **)&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1)), "cudaMalloc(grow)");
+  int64_t got = new_n;
+  if (cudaMalloc((void **)&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1)) != cudaSuccess) {
+    cudaGetLastError();  // clear the allocation failure
+    q = nullptr;
+    if (need_n < 0 || need_n >= new_n) fail(TM_ENOMEM, "cudaMalloc(grow): out of device memory");
+    ck(cudaMalloc((void **)&q, sizeof(T) * (size_t)std::max<int64_t>(need_n, 1)), "cudaMalloc(grow, exact)");
+    got = need_n;
+  }
   if (p && old_n > 0) ck(cudaMemcpyAsync(q, p, sizeof(T) * (size_t)old_n, cudaMemcpyDeviceToDevice, s), "grow copy");
   ck(cudaStreamSynchronize(s), "grow sync");
   if (p) cudaFree(p);
   p = q;
+  return got;
 }
 
 // growable byte buffers (device scratch / pinned staging)
@@ -202,8 +213,8 @@ void ensure_runs(tm_store *s, int64_t need) {
 
 void ensure_arena(tm_store *s, int64_t need) {
   if (need <= s->arena_cap) return;
-  int64_t nc = std::max<int64_t>(round_up(need, 1 << 20), s->arena_cap * 2);
-  dev_grow(s->v.arena, s->arena_used, nc, s->stream);
+  const int64_t exact = round_up(need, 1 << 20);
+  const int64_t nc = dev_grow(s->v.arena, s->arena_used, std::max<int64_t>(exact, s->arena_cap * 2), s->stream, exact);
   s->arena_cap = nc;
   s->v.arena_cap = nc;
 }
