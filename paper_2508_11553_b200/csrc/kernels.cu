@@ -68,10 +68,15 @@ struct WalkShared {
   int lo;
 };
 
-// Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).
+constexpr int kTmaStages = 4;
+constexpr int kTmaChunk = 256;  // int4 per stream per stage (4 KB)
+using Ring = TmaRing<64, kTmaStages, kTmaChunk>;
+
+// Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).  rg != null:
+// compare through the TMA ring (64-thread CTAs only).
 template <int NT, int U>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
-                                           WalkOut o, WalkShared &sh) {
+                                           WalkOut o, WalkShared &sh, Ring *rg = nullptr) {
   if (threadIdx.x == 0) {
     int64_t r = -1;
     if (root_hint) r = *root_hint;
@@ -108,7 +113,13 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
       ext = v.row_ext[r];
       if (ext >= 0) { ext_tok = v.row_ext_tok[r]; ext_len = v.row_ext_len[r]; ext_vb = v.row_ext_vb[r]; }
     }
-    const int j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+    int j;
+    if constexpr (NT == 64) {
+      j = rg ? block_first_mismatch_tma<64, kTmaStages, kTmaChunk>(q, a, lo, hi, sh.red, *rg)
+             : block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+    } else {
+      j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+    }
     if (threadIdx.x == 0) {
       int64_t next = -1;
       if (j < L) {
@@ -198,6 +209,26 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk(DevView v, Batch 
     WalkOut o{b.o_m + w, b.o_parent + w, b.o_dup + w, b.o_tnext ? b.o_tnext + w : nullptr,
               b.o_spar ? b.o_spar + w : nullptr};
     walk_query<NT, U>(v, b.tok + b.off[w], (int)b.len[w], b.sids[w], b.root ? b.root + w : nullptr, o, sh);
+  }
+}
+
+// K1 with the TMA-staged compare (TM_WALK_VARIANT=tma): same scheduling as k_walk.
+__global__ void __launch_bounds__(64) k_walk_tma(DevView v, Batch b) {
+  __shared__ WalkShared sh;
+  __shared__ long long s_item;
+  __shared__ Ring rg;
+  tma_ring_init(rg);
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(&b.sched->work, 1ull);
+    __syncthreads();
+    const int64_t w = s_item;
+    if (w >= b.n) {
+      sched_exit(b.sched);
+      return;
+    }
+    WalkOut o{b.o_m + w, b.o_parent + w, b.o_dup + w, b.o_tnext ? b.o_tnext + w : nullptr,
+              b.o_spar ? b.o_spar + w : nullptr};
+    walk_query<64, 8>(v, b.tok + b.off[w], (int)b.len[w], b.sids[w], b.root ? b.root + w : nullptr, o, sh, &rg);
   }
 }
 
@@ -950,6 +981,7 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
       else if (!strcmp(e, "64x8")) variant = 7;
       else if (!strcmp(e, "256x4")) variant = 8;
       else if (!strcmp(e, "64x4")) variant = 9;
+      else if (!strcmp(e, "tma")) variant = 10;
     }
   }
   switch (variant) {
@@ -962,6 +994,18 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
     case 7: return walk_variant<64, 8>(v, b, num_sms, s);
     case 8: return walk_variant<256, 4>(v, b, num_sms, s);
     case 9: return walk_variant<64, 4>(v, b, num_sms, s);
+    case 10: {
+      static int occ = 0;
+      if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_tma, 64, 0);
+        if (occ < 1) occ = 1;
+      }
+      int64_t grid = (int64_t)num_sms * occ;
+      if (grid > b.n) grid = b.n;
+      if (grid < 1) grid = 1;
+      k_walk_tma<<<(int)grid, 64, 0, s>>>(v, b);
+      return cudaGetLastError();
+    }
     default: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
   }
 }

@@ -270,4 +270,119 @@ __device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ 
   }
 }
 
+// ---- TMA (cp.async.bulk) staged compare ---------------------------------------------------
+// Same contract as block_first_mismatch, but the query and history chunks are moved into a
+// ring of shared-memory stages by the bulk-copy engine (one elected thread issues, an
+// mbarrier per stage counts the landed bytes), and the CTA compares out of shared memory.
+// Registers stay free of load buffers; S stages of 2 x CHV int4 are in flight per CTA.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{ .reg .pred P; WAIT%=: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra WAIT%=; }" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NT, int S, int CHV>
+struct TmaRing {
+  int4 q[S][CHV];
+  int4 a[S][CHV];
+  uint64_t bar[S];
+  uint32_t chunks;  // chunks consumed by this CTA so far (stage / phase bookkeeping)
+};
+
+template <int NT, int S, int CHV>
+__device__ __forceinline__ void tma_ring_init(TmaRing<NT, S, CHV> &rg) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) mbar_init(&rg.bar[s], 1);
+    rg.chunks = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <int NT, int S, int CHV>
+__device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
+                                                        int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg) {
+  static_assert(CHV % NT == 0, "chunk must split evenly over the CTA");
+  if (lo >= hi) return hi;
+  const int4 *q4 = reinterpret_cast<const int4 *>(q);
+  const int4 *a4 = reinterpret_cast<const int4 *>(a);
+  const int v0 = lo >> 2, v1 = (hi + 3) >> 2;
+  const int nch = (v1 - v0 + CHV - 1) / CHV;
+  const uint32_t base = rg.chunks;  // uniform: read before anyone updates it
+  auto issue = [&](int c) {
+    const int s = (int)((base + c) % S);
+    const int i0 = v0 + c * CHV;
+    const int n = min(CHV, v1 - i0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage -> async writes
+    mbar_expect_tx(&rg.bar[s], 2u * 16u * (uint32_t)n);
+    bulk_g2s(rg.q[s], q4 + i0, 16u * (uint32_t)n, &rg.bar[s]);
+    bulk_g2s(rg.a[s], a4 + i0, 16u * (uint32_t)n, &rg.bar[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < S && c < nch; c++) issue(c);
+  int result = hi;
+  int c = 0;
+  for (; c < nch; c++) {
+    const int s = (int)((base + c) % S);
+    mbar_wait(&rg.bar[s], ((base + c) / S) & 1);
+    const int i0 = v0 + c * CHV;
+    int first = 0x7fffffff;
+#pragma unroll
+    for (int k = CHV / NT - 1; k >= 0; k--) {
+      const int li = k * NT + threadIdx.x;
+      const int idx = i0 + li;
+      if (idx >= v1) continue;
+      const int4 x = rg.q[s][li], y = rg.a[s][li];
+      const int p = idx * 4;
+      unsigned ne = (x.x != y.x ? 1u : 0u) | (x.y != y.y ? 2u : 0u) | (x.z != y.z ? 4u : 0u) | (x.w != y.w ? 8u : 0u);
+      unsigned valid = 0xfu;
+      if (p < lo) valid &= (0xfu << (lo - p)) & 0xfu;
+      if (p + 4 > hi) valid &= (hi - p) <= 0 ? 0u : (0xfu >> (4 - (hi - p)));
+      ne &= valid;
+      if (ne) first = min(first, p + __ffs(ne) - 1);
+    }
+    if (__syncthreads_or(first != 0x7fffffff)) {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      unsigned wmin = __reduce_min_sync(0xffffffffu, (unsigned)first);
+      if (lane == 0) s_red[warp] = (int)wmin;
+      __syncthreads();
+      int r = 0x7fffffff;
+#pragma unroll
+      for (int w = 0; w < NT / 32; w++) r = min(r, s_red[w]);
+      result = r;
+      c++;
+      break;
+    }
+    if (threadIdx.x == 0 && c + S < nch) issue(c + S);
+  }
+  // drain chunks issued but not consumed (keeps stage phases aligned; no copy may land
+  // in a stage after it is reused)
+  const int issued = min(nch, c - 1 + S);  // prologue issued S, each consumed chunk one more
+  for (int d = c; d < issued; d++) mbar_wait(&rg.bar[(base + d) % S], ((base + d) / S) & 1);
+  __syncthreads();
+  if (threadIdx.x == 0) rg.chunks = base + (uint32_t)issued;
+  __syncthreads();
+  return result;
+}
+
 }  // namespace tms
