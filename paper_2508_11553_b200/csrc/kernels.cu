@@ -9,6 +9,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 #include "launch.h"
 
@@ -72,11 +73,13 @@ constexpr int kTmaStages = 4;
 constexpr int kTmaChunk = 256;  // int4 per stream per stage (4 KB)
 using Ring = TmaRing<64, kTmaStages, kTmaChunk>;
 
-// Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).  rg != null:
-// compare through the TMA ring (64-thread CTAs only).
-template <int NT, int U>
+struct NoRing {};
+
+// Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).  With a TmaRing
+// the compare goes through the TMA-staged path, otherwise through registers.
+template <int NT, int U, class R = NoRing>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
-                                           WalkOut o, WalkShared &sh, Ring *rg = nullptr) {
+                                           WalkOut o, WalkShared &sh, R *rg = nullptr) {
   if (threadIdx.x == 0) {
     int64_t r = -1;
     if (root_hint) r = *root_hint;
@@ -114,11 +117,10 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
       if (ext >= 0) { ext_tok = v.row_ext_tok[r]; ext_len = v.row_ext_len[r]; ext_vb = v.row_ext_vb[r]; }
     }
     int j;
-    if constexpr (NT == 64) {
-      j = rg ? block_first_mismatch_tma<64, kTmaStages, kTmaChunk>(q, a, lo, hi, sh.red, *rg)
-             : block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
-    } else {
+    if constexpr (std::is_same<R, NoRing>::value) {
       j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+    } else {
+      j = block_first_mismatch_tma(q, a, lo, hi, sh.red, *rg);
     }
     if (threadIdx.x == 0) {
       int64_t next = -1;
@@ -212,11 +214,13 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk(DevView v, Batch 
   }
 }
 
-// K1 with the TMA-staged compare (TM_WALK_VARIANT=tma): same scheduling as k_walk.
+// K1 with the TMA-staged compare: same scheduling as k_walk; S stages of CHV int4 per
+// stream in shared memory.
+template <int S, int CHV>
 __global__ void __launch_bounds__(64) k_walk_tma(DevView v, Batch b) {
   __shared__ WalkShared sh;
   __shared__ long long s_item;
-  __shared__ Ring rg;
+  __shared__ TmaRing<64, S, CHV> rg;
   tma_ring_init(rg);
   for (;;) {
     if (threadIdx.x == 0) s_item = (long long)atomicAdd(&b.sched->work, 1ull);
@@ -230,6 +234,20 @@ __global__ void __launch_bounds__(64) k_walk_tma(DevView v, Batch b) {
               b.o_spar ? b.o_spar + w : nullptr};
     walk_query<64, 8>(v, b.tok + b.off[w], (int)b.len[w], b.sids[w], b.root ? b.root + w : nullptr, o, sh, &rg);
   }
+}
+
+template <int S, int CHV>
+static cudaError_t walk_tma_variant(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_tma<S, CHV>, 64, 0);
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = (int64_t)num_sms * occ;
+  if (grid > b.n) grid = b.n;
+  if (grid < 1) grid = 1;
+  k_walk_tma<S, CHV><<<(int)grid, 64, 0, s>>>(v, b);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------------
@@ -982,6 +1000,10 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
       else if (!strcmp(e, "256x4")) variant = 8;
       else if (!strcmp(e, "64x4")) variant = 9;
       else if (!strcmp(e, "tma")) variant = 10;
+      else if (!strcmp(e, "tma3")) variant = 11;
+      else if (!strcmp(e, "tma8x128")) variant = 12;
+      else if (!strcmp(e, "tma6x128")) variant = 13;
+      else if (!strcmp(e, "tma2x512")) variant = 14;
     }
   }
   switch (variant) {
@@ -994,18 +1016,11 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
     case 7: return walk_variant<64, 8>(v, b, num_sms, s);
     case 8: return walk_variant<256, 4>(v, b, num_sms, s);
     case 9: return walk_variant<64, 4>(v, b, num_sms, s);
-    case 10: {
-      static int occ = 0;
-      if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_tma, 64, 0);
-        if (occ < 1) occ = 1;
-      }
-      int64_t grid = (int64_t)num_sms * occ;
-      if (grid > b.n) grid = b.n;
-      if (grid < 1) grid = 1;
-      k_walk_tma<<<(int)grid, 64, 0, s>>>(v, b);
-      return cudaGetLastError();
-    }
+    case 10: return walk_tma_variant<4, 256>(v, b, num_sms, s);
+    case 11: return walk_tma_variant<3, 256>(v, b, num_sms, s);
+    case 12: return walk_tma_variant<8, 128>(v, b, num_sms, s);
+    case 13: return walk_tma_variant<6, 128>(v, b, num_sms, s);
+    case 14: return walk_tma_variant<2, 512>(v, b, num_sms, s);
     default: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
   }
 }

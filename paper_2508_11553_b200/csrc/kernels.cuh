@@ -322,6 +322,7 @@ __device__ __forceinline__ void tma_ring_init(TmaRing<NT, S, CHV> &rg) {
 template <int NT, int S, int CHV>
 __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
                                                         int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg) {
+  static_assert(NT == 64, "the TMA compare is written for 64-thread CTAs");
   static_assert(CHV % NT == 0, "chunk must split evenly over the CTA");
   if (lo >= hi) return hi;
   const int4 *q4 = reinterpret_cast<const int4 *>(q);
