@@ -517,11 +517,13 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
   }
 }
 
-template <int NT, int U>
+template <int NT, int U, bool TMA = false>
 __global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
   const Batch &b = a.b;
   __shared__ WalkShared sh;
   __shared__ long long s_item;
+  __shared__ TmaRing<64, 2, 256> rg;
+  if constexpr (TMA) tma_ring_init(rg);
   for (;;) {
     if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
     __syncthreads();
@@ -534,7 +536,8 @@ __global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
     const int64_t c = a.chain_order[it];
     for (int64_t e = a.chain_beg[c]; e < a.chain_beg[c + 1]; e++) {
       WalkOut o{b.o_m + e, b.o_parent + e, b.o_dup + e, b.o_tnext + e, b.o_spar + e};
-      walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh);
+      if constexpr (TMA) walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh, &rg);
+      else walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh);
       if (threadIdx.x == 0) {  // allocate (the reserved row id is already in c_row)
         long long words, runs, isnew;
         entry_need(b, e, words, runs, isnew);
@@ -1032,17 +1035,17 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
   }
 }
 
-template <int NT, int U>
+template <int NT, int U, bool TMA = false>
 static cudaError_t record_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<NT, U>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<NT, U, TMA>, NT, 0);
     if (occ < 1) occ = 1;
   }
   int64_t grid = (int64_t)num_sms * occ;
   if (grid > a.nchains) grid = a.nchains;
   if (grid < 1) grid = 1;
-  k_record<NT, U><<<(int)grid, NT, 0, s>>>(v, a);
+  k_record<NT, U, TMA><<<(int)grid, NT, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 
@@ -1057,12 +1060,14 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
       if (!strcmp(e, "64x8")) variant = 1;
       else if (!strcmp(e, "32x8")) variant = 2;
       else if (!strcmp(e, "32x4")) variant = 3;
+      else if (!strcmp(e, "tma")) variant = 4;
     }
   }
   switch (variant) {
     case 1: return record_variant<64, 8>(v, a, num_sms, s);
     case 2: return record_variant<32, 8>(v, a, num_sms, s);
     case 3: return record_variant<32, 4>(v, a, num_sms, s);
+    case 4: return record_variant<64, 4, true>(v, a, num_sms, s);
     default: return record_variant<64, 4>(v, a, num_sms, s);
   }
 }
