@@ -442,7 +442,7 @@ def main():
         "config": c4_config(args, world, wl, mixed),
         "tokens_compared_per_s": toks_per_s,
         "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
-        "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": "k_walk_tma", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0,
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": traffic,
                      "kernel_time_basis": "timed region / batches (batches overlap on 2 streams; includes planner)",

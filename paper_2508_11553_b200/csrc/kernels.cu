@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
       __syncthreads();
       continue;
     }
-    walk_query<NT, U>(v, reinterpret_cast<const int32_t *>(reg + d->tok_off) + off, L, sid, nullptr, o, sh, &rg);
+    const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
+    if (p != a.rank) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, &rg);  // remote query: TMA over NVLink
+    else walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);                   // local: register double buffer
   }
 }
 
