@@ -321,21 +321,29 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
 // and the other ranks' (query bytes over NVLink).  1/np of the CTAs start on the local
 // queue and the rest on the remote one, each falling back to the other when its queue
 // runs dry, so HBM and the links are busy at the same time instead of in phases.
+// Dynamic shared memory: [TmaRing (only when nranks > 1)][3 x kPlanNB x nranks + 2 ints
+// of routing tables], sized by routed_smem_bytes so a single rank keeps full occupancy.
+using RoutedRing = TmaRing<64, kTmaStages, kTmaChunk>;
+
+__host__ __device__ constexpr size_t routed_smem_bytes(int nranks) {
+  return (nranks > 1 ? (sizeof(RoutedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
+}
+
 template <int NT, int U>
 __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v, RoutedArgs a) {
+  extern __shared__ __align__(16) char dyn[];
   __shared__ WalkShared sh;
-  // TMA-staged compare: bulk copies pull remote query chunks over NVLink (a 2-stage ring:
-  // the routing tables already take 24 KB of the 48 KB static shared memory)
-  __shared__ TmaRing<64, 2, 256> rg;
-  tma_ring_init(rg);
   __shared__ long long s_item;
   __shared__ int s_cell;
-  __shared__ int s_pre[kPlanNB * kMaxRanks + 2];  // cells: local (b) then remote (b, p != rank)
-  __shared__ int s_bs[kPlanNB * kMaxRanks];
-  __shared__ int s_peer[kPlanNB * kMaxRanks];
   __shared__ int s_nloc;  // cells in the local queue
   const int np = a.nranks;
   const int ncell = kPlanNB * np;
+  // TMA-staged compare for remote queries: bulk copies pull query chunks over NVLink
+  RoutedRing *rg = np > 1 ? reinterpret_cast<RoutedRing *>(dyn) : nullptr;
+  if (np > 1) tma_ring_init(*rg);
+  int *s_pre = reinterpret_cast<int *>(dyn + (np > 1 ? (sizeof(RoutedRing) + 15) / 16 * 16 : 0));  // ncell + 2
+  int *s_bs = s_pre + ncell + 2;
+  int *s_peer = s_bs + ncell;
   // cell c: local cells first (bucket order), then remote cells (bucket, peer) order
   for (int c = threadIdx.x; c < ncell; c += NT) {
     int bk, p;
@@ -405,8 +413,8 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
       continue;
     }
     const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
-    if (p != a.rank) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, &rg);  // remote query: TMA over NVLink
-    else walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);                   // local: register double buffer
+    if (p != a.rank) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg);  // remote query: TMA over NVLink
+    else walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);                  // local: register double buffer
   }
 }
 
@@ -1111,12 +1119,14 @@ cudaError_t launch_route(char *region, int nranks, cudaStream_t s) {
 }
 
 cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk_routed<kWalkNT, kWalkU>, kWalkNT, 0);
-    if (occ < 1) occ = 1;
+  static int occ[kMaxRanks + 1] = {0};
+  const size_t smem = routed_smem_bytes(a.nranks);
+  if (!occ[a.nranks]) {
+    cudaFuncSetAttribute(k_walk_routed<kWalkNT, kWalkU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, kWalkU>, kWalkNT, smem);
+    if (occ[a.nranks] < 1) occ[a.nranks] = 1;
   }
-  k_walk_routed<kWalkNT, kWalkU><<<num_sms * occ, kWalkNT, 0, s>>>(v, a);
+  k_walk_routed<kWalkNT, kWalkU><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
 }
 
