@@ -317,3 +317,45 @@ def test_hypothesis_naive_oracle_property(store):
         assert trie.check_well_formed() == []
 
     prop()
+
+
+def test_cabi_error_paths(store, tmp_path):
+    """Every C-ABI failure is a status code mapped to the reference exception type; the
+    store stays usable afterwards."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2508_11553_b200 import DeviceStore
+    from paper_2508_11553_b200._lib import check
+
+    lib = store.lib
+    sid = store.new_session()
+    one = (np.array([0], np.int32), np.array([1], np.uint8), np.array([0], np.int32))
+    with pytest.raises(KeyError):  # unknown session
+        store.record([sid + 10_000], [[1, 2]], [one])
+    with pytest.raises(ValueError):  # runs not starting at 0
+        store.record([sid], [[1, 2]], [(np.array([1], np.int32), one[1], one[2])])
+    with pytest.raises(ValueError):  # run start beyond the sequence
+        store.record([sid], [[1, 2]], [(np.array([0, 5], np.int32), np.array([0, 1], np.uint8), np.array([0, 0], np.int32))])
+    with pytest.raises(ValueError):  # bad origin code
+        store.record([sid], [[1, 2]], [(one[0], np.array([3], np.uint8), one[2])])
+    with pytest.raises(KeyError):  # export of a row that does not exist
+        store.export([10**9])
+    with pytest.raises(KeyError):
+        store.row_info(-1)
+    dev = torch.device("cuda", 0)
+    tok = torch.arange(64, dtype=torch.int32, device=dev)
+    with pytest.raises(ValueError):  # device tokens must start on 128-byte boundaries
+        store.record_device([sid], tok, [3], [10], [0, 1], *one)
+    with pytest.raises(KeyError):  # snapshot that does not exist
+        DeviceStore.load(str(tmp_path / "missing"))
+    bad = tmp_path / "bad.snap"
+    bad.write_bytes(b"NOTASNAPSHOT" * 4)
+    with pytest.raises(ValueError):
+        DeviceStore.load(str(bad))
+    h = C.c_void_p()
+    assert lib.tm_store_create(None, None) != 0  # null out pointer
+    # still healthy
+    r = store.record([sid], [[5, 6, 7]], [one])
+    assert r.added.tolist() == [3]
