@@ -359,3 +359,33 @@ def test_cabi_error_paths(store, tmp_path):
     # still healthy
     r = store.record([sid], [[5, 6, 7]], [one])
     assert r.added.tolist() == [3]
+
+
+def test_growth_from_tiny_capacities_vs_oracle():
+    """Every table starts tiny (arena 64 K words, 64 rows / runs, 16 sessions, 1 K-slot
+    branch index) and grows — arena and row-table reallocation, branch-index rehash, dense
+    probe collisions — with results still equal to the oracle's."""
+    from paper_2508_11553_b200 import DeviceStore
+
+    st = DeviceStore(0, arena_words=1 << 16, row_capacity=64, run_capacity=64, session_capacity=16)
+    rng = np.random.default_rng(99)
+    n_sess = 300
+    sids, seqs, origins, versions = _random_sessions(rng, n_sess, 3000, 151936, 400)
+    g = [st.new_session() for _ in range(n_sess)]
+    ora = CRadixStore()
+    om, orow, opar, oadd = ora.insert_batch(*pack_records(sids, seqs, origins, versions), nthreads=4)
+    for a in range(0, len(sids), 700):  # several calls, each forcing growth
+        b = min(len(sids), a + 700)
+        sub = pack_records([g[s] for s in sids[a:b]], seqs[a:b], origins[a:b], versions[a:b])
+        r = st.record_packed(sub[0], sub[1], sub[2][:-1], np.diff(sub[2]), *sub[3:])
+        assert np.array_equal(r.matched, om[a:b]) and np.array_equal(r.local, orow[a:b])
+        assert np.array_equal(r.parent_local, opar[a:b])
+    info = st.stats()
+    assert info["arena_cap"] > (1 << 16) and info["rows"] == sum(ora.stats(s)[2] for s in range(n_sess))
+    for s in (0, 17, 299):
+        rows = st.session_rows(g[s])
+        p = st.export(rows)
+        for k in range(len(rows)):
+            t, m, v = ora.export_row(s, k)
+            assert np.array_equal(p.tokens[p.offsets[k]:p.offsets[k + 1]], t)
+    st.close()
