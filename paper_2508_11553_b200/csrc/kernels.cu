@@ -587,6 +587,19 @@ struct ExportPiece {        // one ancestor's share of an output tile
 };
 constexpr int kMaxPieces = 16;  // per tile; deeper chains fall back to an in-kernel walk
 
+struct TileHdr {            // planner output per tile: everything the copy CTA needs up front
+  int64_t o;                 // output word of the tile's row start
+  int32_t a, b;              // tile positions [a, b) of that row
+  int32_t row;               // output row index (resp-start atomics, fallback walk)
+  int32_t np;                // pieces, or -1: chain deeper than kMaxPieces, walk in-kernel
+  int64_t pad;
+};
+struct TilePlan {            // 672 bytes: fetched into shared memory with 42 16-byte cp.async
+  TileHdr h;
+  ExportPiece p[kMaxPieces];
+};
+static_assert(sizeof(TilePlan) % 16 == 0, "TilePlan is copied in 16-byte chunks");
+
 struct ExportArgs {
   int64_t n;
   const int64_t *rows;
@@ -597,9 +610,7 @@ struct ExportArgs {
   uint8_t *mask;
   int32_t *versions;
   unsigned long long *resp;  // n (atomicMax), may be null
-  int32_t *tile_row;         // ntiles: output row of each tile (planner output)
-  int32_t *npieces;          // ntiles: pieces per tile, or -1 (walk in-kernel)
-  ExportPiece *pieces;       // ntiles * kMaxPieces
+  TilePlan *plan;            // ntiles (planner output); pieces by descending position
 };
 
 // Copy / fill helpers for one piece [pa, pb) of an output row starting at word o.  When
@@ -614,16 +625,7 @@ __device__ __forceinline__ void copy_tokens(int32_t *__restrict__ out, const int
       for (int64_t p = 4 * vb + threadIdx.x; p < pb; p += kExportNT) out[o + p] = src[p];
       const int4 *s4 = reinterpret_cast<const int4 *>(src);
       int4 *d4 = reinterpret_cast<int4 *>(out + o);
-      int64_t q = va + threadIdx.x;
-      for (; q + 3 * kExportNT < vb; q += 4 * kExportNT) {
-        const int4 x0 = ldg_stream(s4 + q), x1 = ldg_stream(s4 + q + kExportNT);
-        const int4 x2 = ldg_stream(s4 + q + 2 * kExportNT), x3 = ldg_stream(s4 + q + 3 * kExportNT);
-        d4[q] = x0;
-        d4[q + kExportNT] = x1;
-        d4[q + 2 * kExportNT] = x2;
-        d4[q + 3 * kExportNT] = x3;
-      }
-      for (; q < vb; q += kExportNT) d4[q] = ldg_stream(s4 + q);
+      for (int64_t q = va + threadIdx.x; q < vb; q += kExportNT) d4[q] = ldg_stream(s4 + q);
       return;
     }
   }
@@ -651,6 +653,15 @@ __device__ __forceinline__ void fill_meta(uint8_t *__restrict__ mask, int32_t *_
   for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
 }
 
+__device__ __forceinline__ int first_run_of(const DevView &v, int64_t run0, int nrun, int64_t pa) {
+  int lo = 0, hi = nrun;  // last run with start <= pa
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (v.run_start[run0 + mid] <= pa) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 // Export planner: one thread per tile resolves the dependent lookups (tile -> row,
 // parent chain, first run of each piece) for every tile in parallel, so the copy
 // kernel's CTAs start streaming immediately instead of chasing pointers per tile.
@@ -661,7 +672,6 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
       int64_t mid = (lo + hi) >> 1;
       if (e.tile_off[mid] <= t) lo = mid; else hi = mid;
     }
-    e.tile_row[t] = (int32_t)lo;
     const int64_t row = e.rows[lo];
     const int64_t a = (t - e.tile_off[lo]) * kExportTile;
     const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
@@ -674,7 +684,7 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
       upper = b;
     }
     int np = 0;
-    ExportPiece *out = e.pieces + t * kMaxPieces;
+    ExportPiece *out = e.plan[t].p;
     while (cur >= 0 && upper > a) {
       const int64_t mx = v.row_m[cur];
       const int64_t pa = max(mx, a), pb = min(upper, b);
@@ -688,25 +698,26 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
         p.pb = (int32_t)pb;
         p.nrun = v.row_nrun[cur];
         p.len = v.row_len[cur];
-        int lo2 = 0, hi2 = p.nrun;  // last run with start <= pa
-        while (hi2 - lo2 > 1) {
-          int mid = (lo2 + hi2) >> 1;
-          if (v.run_start[p.run0 + mid] <= pa) lo2 = mid; else hi2 = mid;
-        }
-        p.first_run = lo2;
+        p.first_run = first_run_of(v, p.run0, p.nrun, pa);
         p.pad = 0;
         out[np++] = p;
       }
       upper = mx;
       cur = v.row_parent[cur];
     }
-    e.npieces[t] = np;
+    TileHdr h;
+    h.o = e.out_off[lo];
+    h.a = (int32_t)a;
+    h.b = (int32_t)b;
+    h.row = (int32_t)lo;
+    h.np = np;
+    h.pad = 0;
+    e.plan[t].h = h;
   }
 }
 
-__device__ __forceinline__ void export_piece(const DevView &v, const ExportArgs &e, const ExportPiece &p, int64_t o,
-                                             long long &respmax) {
-  copy_tokens(e.tokens, v.arena + p.vb, o, p.pa, p.pb);
+__device__ __forceinline__ void export_runs(const DevView &v, const ExportArgs &e, const ExportPiece &p, int64_t o,
+                                            long long &respmax) {
   for (int k = p.first_run; k < p.nrun; k++) {
     const int64_t rs = v.run_start[p.run0 + k];
     if (rs >= p.pb) break;
@@ -718,22 +729,75 @@ __device__ __forceinline__ void export_piece(const DevView &v, const ExportArgs 
   }
 }
 
-__global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
-  __shared__ ExportPiece sp[kMaxPieces];
-  for (int64_t t = blockIdx.x; t < e.ntiles; t += gridDim.x) {
-    const int64_t i = e.tile_row[t];
-    const int np = e.npieces[t];
-    const int64_t o = e.out_off[i];
+// pieces are ordered by descending position and partition the tile [a, b)
+__device__ __forceinline__ int piece_at(const ExportPiece *sp, int np, int32_t p) {
+  int k = 0;
+  while (k + 1 < np && sp[k].pa > p) k++;
+  return k;
+}
+
+constexpr int kExportSlots = kExportTile / 4 / kExportNT;  // int4 output slots per thread per tile
+constexpr int kExportCtas = 4;                             // resident CTAs per SM (64 registers)
+
+// K3 copy: persistent CTAs over planner tiles.  Tile-centric: the mask / version fills
+// (stores only) go first, then each thread issues the loads of all kExportSlots int4
+// slots it owns before storing them - 4 loads in flight per thread however the tile
+// splits into ancestor pieces.  The next tile's plan is fetched into the other half of
+// a double-buffered shared-memory table with cp.async while this tile is processed;
+// one barrier per tile.
+__device__ __forceinline__ void fetch_plan(TilePlan *dst, const TilePlan *src) {
+  constexpr int kChunks = (int)(sizeof(TilePlan) / 16);
+  if (threadIdx.x < kChunks) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<char *>(dst) + 16 * threadIdx.x);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(reinterpret_cast<const char *>(src) + 16 * threadIdx.x)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kExportNT, kExportCtas) k_export(DevView v, ExportArgs e) {
+  __shared__ TilePlan sp[2];
+  int64_t t = blockIdx.x;
+  if (t >= e.ntiles) return;
+  fetch_plan(&sp[0], &e.plan[t]);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  for (int it = 0; t < e.ntiles; t += gridDim.x, it ^= 1) {
+    const TileHdr h = sp[it].h;
+    const ExportPiece *P = sp[it].p;
+    if (t + gridDim.x < e.ntiles) fetch_plan(&sp[it ^ 1], &e.plan[t + gridDim.x]);  // overlaps this tile
+    const int64_t o = h.o;
     long long respmax = 0;
-    if (np >= 0) {
-      if (threadIdx.x < np) sp[threadIdx.x] = e.pieces[t * kMaxPieces + threadIdx.x];
-      __syncthreads();
-      for (int k = 0; k < np; k++) export_piece(v, e, sp[k], o, respmax);
-      __syncthreads();
-    } else {  // chain deeper than kMaxPieces inside this tile: walk it here
-      const int64_t row = e.rows[i];
-      const int64_t a = (t - e.tile_off[i]) * kExportTile;
-      const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
+    if (h.np > 0 && (o & 3) == 0) {
+      for (int k = 0; k < h.np; k++) export_runs(v, e, P[k], o, respmax);  // stores only
+      int4 x[kExportSlots];
+      uint32_t full = 0;  // slots inside one piece; the others straddle a piece boundary or the row end
+#pragma unroll
+      for (int j = 0; j < kExportSlots; j++) {
+        const int32_t p = h.a + 4 * ((int)threadIdx.x + j * kExportNT);
+        const ExportPiece &q = P[piece_at(P, h.np, p)];
+        const bool ok = p + 4 <= q.pb;  // (q.pb <= h.b)
+        full |= (uint32_t)ok << j;
+        x[j] = ldg_stream_if(reinterpret_cast<const int4 *>(v.arena + q.vb + p), ok);
+      }
+      int4 *d4 = reinterpret_cast<int4 *>(e.tokens + o) + (h.a >> 2) + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < kExportSlots; j++) stg_if(d4 + j * kExportNT, x[j], (full >> j) & 1);
+#pragma unroll 1
+      for (int j = 0; j < kExportSlots; j++) {
+        const int32_t p = h.a + 4 * ((int)threadIdx.x + j * kExportNT);
+        if (!(full & (1u << j)) && p < h.b)
+          for (int u = 0; u < 4 && p + u < h.b; u++)
+            e.tokens[o + p + u] = v.arena[P[piece_at(P, h.np, p + u)].vb + p + u];
+      }
+    } else if (h.np > 0) {  // unaligned row start
+      for (int k = 0; k < h.np; k++) {
+        copy_tokens(e.tokens, v.arena + P[k].vb, o, P[k].pa, P[k].pb);
+        export_runs(v, e, P[k], o, respmax);
+      }
+    } else if (h.np < 0) {  // chain deeper than kMaxPieces inside this tile: walk it here
+      const int64_t row = e.rows[h.row];
+      const int64_t a = h.a, b = h.b;
       int64_t cur = row, upper = v.row_len[row];
       while (cur >= 0 && upper > a) {
         const int64_t mx = v.row_m[cur];
@@ -746,19 +810,17 @@ __global__ void __launch_bounds__(kExportNT) k_export(DevView v, ExportArgs e) {
           p.pb = (int32_t)pb;
           p.nrun = v.row_nrun[cur];
           p.len = v.row_len[cur];
-          int lo2 = 0, hi2 = p.nrun;
-          while (hi2 - lo2 > 1) {
-            int mid = (lo2 + hi2) >> 1;
-            if (v.run_start[p.run0 + mid] <= pa) lo2 = mid; else hi2 = mid;
-          }
-          p.first_run = lo2;
-          export_piece(v, e, p, o, respmax);
+          p.first_run = first_run_of(v, p.run0, p.nrun, pa);
+          copy_tokens(e.tokens, v.arena + p.vb, o, p.pa, p.pb);
+          export_runs(v, e, p, o, respmax);
         }
         upper = mx;
         cur = v.row_parent[cur];
       }
     }
-    if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[i], (unsigned long long)respmax);
+    if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[h.row], (unsigned long long)respmax);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // next plan visible; this tile's plan no longer read
   }
 }
 
@@ -1083,17 +1145,19 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
 }
 
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {
-  ExportArgs e{h.n, h.rows, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions,
-               (unsigned long long *)h.resp, h.tile_row, h.npieces, reinterpret_cast<ExportPiece *>(h.pieces)};
   if (h.ntiles < 1) return cudaSuccess;
+  ExportArgs e{h.n, h.rows, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions,
+               (unsigned long long *)h.resp, reinterpret_cast<TilePlan *>(h.plan)};
   const int pgrid = (int)std::min<int64_t>((h.ntiles + 255) / 256, (int64_t)num_sms * 8);
   k_export_plan<<<pgrid, 256, 0, s>>>(v, e);
-  int64_t grid = h.ntiles < (int64_t)num_sms * 8 ? h.ntiles : (int64_t)num_sms * 8;
+  const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * kExportCtas);
   k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
   return cudaGetLastError();
 }
 
-int64_t export_plan_bytes(int64_t ntiles) { return ntiles * (8 + (int64_t)kMaxPieces * (int64_t)sizeof(ExportPiece)); }
+int64_t export_plan_bytes(int64_t ntiles) {
+  return ntiles * (int64_t)sizeof(TilePlan);
+}
 
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s) {

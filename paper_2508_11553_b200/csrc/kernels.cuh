@@ -207,6 +207,20 @@ __device__ __forceinline__ int4 ldg_stream(const int4 *p) {
   return r;
 }
 
+// predicated streaming load / store (no branch, so the value stays in registers)
+__device__ __forceinline__ int4 ldg_stream_if(const int4 *p, bool pred) {
+  int4 r = make_int4(0, 0, 0, 0);
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n"
+               " @p ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];\n}"
+               : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+               : "l"(p), "r"((int)pred));
+  return r;
+}
+__device__ __forceinline__ void stg_if(int4 *p, int4 x, bool pred) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n @p st.global.v4.s32 [%0], {%1,%2,%3,%4};\n}"
+               ::"l"(p), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w), "r"((int)pred) : "memory");
+}
+
 // First mismatch position in [lo, hi) between q[] and a[] (both indexed by absolute
 // position, 16-byte congruent), or hi.  Whole-block call; all threads get the result.
 // Each warp owns 32*U consecutive int4 per chunk; the next chunk is prefetched into

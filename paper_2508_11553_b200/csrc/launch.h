@@ -18,9 +18,7 @@ struct ExportArgsHost {
   uint8_t *mask;
   int32_t *versions;
   int64_t *resp;
-  int32_t *tile_row;  // planner scratch: ntiles ints, ntiles ints, ntiles * kMaxPieces pieces
-  int32_t *npieces;
-  void *pieces;
+  char *plan;  // planner scratch: export_plan_bytes(ntiles), 16-byte aligned
 };
 int64_t export_plan_bytes(int64_t ntiles);
 

@@ -914,8 +914,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
     size_t in_bytes = lay.bytes;
     size_t o_tok = 0, o_msk = 0, o_ver = 0, o_resp = 0;
     const int64_t ntiles_all = tile[n];
-    size_t o_trow = lay.add(4 * ntiles_all), o_np = lay.add(4 * ntiles_all),
-           o_pieces = lay.add((size_t)tms::export_plan_bytes(ntiles_all) - 8 * ntiles_all);
+    size_t o_plan = lay.add((size_t)tms::export_plan_bytes(ntiles_all));
     if (mem_out == TM_MEM_HOST) {
       o_tok = lay.add(4 * total);
       o_msk = lay.add(total);
@@ -934,9 +933,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
     e.out_off = (const int64_t *)(d + o_off);
     e.tile_off = (const int64_t *)(d + o_tile);
     e.ntiles = tile[n];
-    e.tile_row = (int32_t *)(d + o_trow);
-    e.npieces = (int32_t *)(d + o_np);
-    e.pieces = d + o_pieces;
+    e.plan = d + o_plan;
     if (mem_out == TM_MEM_HOST) {
       e.tokens = (int32_t *)(d + o_tok);
       e.mask = (uint8_t *)(d + o_msk);
@@ -992,8 +989,7 @@ int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *si
     size_t in_bytes = lay.bytes;
     size_t o_tok = lay.add(4 * total), o_msk = lay.add(total), o_ver = lay.add(4 * total), o_sums = lay.add(16 * ntiles),
            o_toff = lay.add(24 * ntiles), o_roff = lay.add(32 * (n + 1)), o_sidoff = lay.add(8 * (n + 1)),
-           o_sid = lay.add((size_t)sid_off[n]), o_trow = lay.add(4 * ntiles), o_np = lay.add(4 * ntiles),
-           o_pieces = lay.add((size_t)tms::export_plan_bytes(ntiles) - 8 * ntiles);
+           o_sid = lay.add((size_t)sid_off[n]), o_plan = lay.add((size_t)tms::export_plan_bytes(ntiles));
     char *d = (char *)s->scratch.need(lay.bytes);
     char *h = (char *)s->pin.need(std::max(in_bytes, (size_t)16 * ntiles));
     memcpy(h + o_rows, rows, 8 * n);
@@ -1010,9 +1006,7 @@ int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *si
     e.mask = (uint8_t *)(d + o_msk);
     e.versions = (int32_t *)(d + o_ver);
     e.resp = nullptr;
-    e.tile_row = (int32_t *)(d + o_trow);
-    e.npieces = (int32_t *)(d + o_np);
-    e.pieces = d + o_pieces;
+    e.plan = d + o_plan;
     {
       ProfScope ps(s, 2, st);
       ck(tms::launch_export(s->v, e, s->num_sms, st), "export");

@@ -166,6 +166,49 @@ def test_random_batches_vs_c_oracle(store, vocab, max_new, n_sess, n_ins):
     assert np.array_equal(dup_local, d_o)
 
 
+def test_export_deep_chains_and_straddled_tiles(store):
+    """K3 corner cases against the C oracle: chains with more ancestor pieces inside one
+    4096-position tile than the planner records (in-kernel walk), pieces whose
+    boundaries straddle 16-byte output slots, rows spanning several tiles, and output
+    offsets of every residue mod 4 (rows exported after a ragged-length row)."""
+    rng = np.random.default_rng(2508)
+    seqs = []
+    cur = rng.integers(0, 151936, 3).tolist()
+    for k in range(70):                          # 70-deep chain, 1-7 new tokens per step
+        cur = cur + rng.integers(0, 151936, int(rng.integers(1, 8))).tolist()
+        seqs.append(list(cur))
+        if k % 9 == 4:                           # side branches off the chain
+            cut = int(rng.integers(1, len(cur)))
+            seqs.append(cur[:cut] + rng.integers(0, 151936, int(rng.integers(1, 6))).tolist())
+    long = cur + rng.integers(0, 151936, 9001).tolist()     # multi-tile row on top of the chain
+    seqs.append(long)
+    seqs.append(long + rng.integers(0, 151936, 5).tolist())
+    seqs.append(long[:5000] + rng.integers(0, 151936, 4100).tolist())
+    origins = [(rng.random(len(q)) < 0.4).astype(int).tolist() for q in seqs]
+    versions = [np.sort(rng.integers(0, 4, len(q))).tolist() for q in seqs]
+    ora = CRadixStore()
+    ora.insert_batch(*pack_records([0] * len(seqs), seqs, origins, versions))
+    sid = store.new_session()
+    rec = pack_records([sid] * len(seqs), seqs, origins, versions)
+    store.record_packed(rec[0], rec[1], rec[2][:-1], np.diff(rec[2]), *rec[3:])
+    rows = np.asarray(store.session_rows(sid, "insert"))
+    nrows = len(rows)
+    expect = [ora.export_row(0, k) for k in range(nrows)]
+    for shift in range(4):  # a ragged row first puts every following row at offset residue `shift`
+        order = rng.permutation(nrows)
+        head = [k for k in range(nrows) if len(expect[k][0]) % 4 == shift][:1]
+        sel = head + order.tolist()
+        p = store.export(rows[sel])
+        for j, k in enumerate(sel):
+            a, b = p.offsets[j], p.offsets[j + 1]
+            t, m, v = expect[k]
+            assert np.array_equal(p.tokens[a:b], t), (shift, k)
+            assert np.array_equal(p.loss_mask[a:b], m), (shift, k)
+            assert np.array_equal(p.versions[a:b], v), (shift, k)
+            zeros = np.flatnonzero(m == 0)
+            assert p.resp_start[j] == (zeros[-1] + 1 if len(zeros) else 0)
+
+
 def test_device_match_path_and_alignment(store):
     """TM_MEM_DEVICE match on torch tensors equals the host-path result."""
     import torch
