@@ -43,6 +43,7 @@ SIGNATURES = {
     "tm_store_stats": (C.c_int, [_P, _P, _P, _P, _P]),
     "tm_store_stream": (C.c_int, [_P, _P]),
     "tm_store_counters": (C.c_int, [_P, _P]),
+    "tm_store_h2d_stats": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
     "tm_store_save": (C.c_int, [_P, C.c_char_p]),

@@ -1159,6 +1159,34 @@ int64_t export_plan_bytes(int64_t ntiles) {
   return ntiles * (int64_t)sizeof(TilePlan);
 }
 
+// Packed host->device token copy (hostpack.h): one thread per 4 positions reads 8 B of
+// the uint16 low plane and the aligned 4-byte word of the high plane that holds their
+// 2-bit high parts, and stores one int4.
+__global__ void k_unpack18(const uint16_t *__restrict__ lo, const uint8_t *__restrict__ hi, int32_t *__restrict__ out,
+                           int64_t q0, int64_t q1) {
+  for (int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = 4 * q;
+    const uint2 l = *reinterpret_cast<const uint2 *>(lo + p);
+    const int lane = (int)(p & 31);  // byte (lane & 7) + u of the group's 8 high-plane bytes
+    const uint32_t h = *reinterpret_cast<const uint32_t *>(hi + (p >> 5) * 8 + (lane & 7)) >> (2 * (lane >> 3));
+    int4 o;
+    o.x = (int)((l.x & 0xFFFFu) | ((h & 3u) << 16));
+    o.y = (int)((l.x >> 16) | (((h >> 8) & 3u) << 16));
+    o.z = (int)((l.y & 0xFFFFu) | (((h >> 16) & 3u) << 16));
+    o.w = (int)((l.y >> 16) | (((h >> 24) & 3u) << 16));
+    reinterpret_cast<int4 *>(out)[q] = o;
+  }
+}
+
+cudaError_t launch_unpack18(const uint16_t *lo, const uint8_t *hi, int32_t *out, int64_t p0, int64_t p1, int num_sms,
+                            cudaStream_t s) {
+  const int64_t nq = (p1 - p0) / 4;
+  if (nq <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((nq + 255) / 256, (int64_t)num_sms * 8);
+  k_unpack18<<<grid, 256, 0, s>>>(lo, hi, out, p0 / 4, p1 / 4);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s) {
   k_rehash<<<1024, 256, 0, s>>>(v, ok0, ok1, oval, ocap);

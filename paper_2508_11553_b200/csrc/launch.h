@@ -22,6 +22,11 @@ struct ExportArgsHost {
 };
 int64_t export_plan_bytes(int64_t ntiles);
 
+// expand 18-bit split planes (hostpack.h) into int32 tokens for positions [p0, p1)
+// (multiples of 32)
+cudaError_t launch_unpack18(const uint16_t *lo, const uint8_t *hi, int32_t *out, int64_t p0, int64_t p1, int num_sms,
+                            cudaStream_t s);
+
 // fills b.root (if root != null) and b.bucket_items (plan_items_ints(n) ints); counts go to b.sched
 struct JsonArgsHost {
   int64_t n;

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/tmstore.h"
+#include "hostpack.h"
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -140,6 +141,13 @@ struct tm_store {
   int64_t max_depth = 0;
   DevBytes scratch, dtok;
   PinBytes pin, ptok, d2h_slot[2];
+  // packed host->device token copies (hostpack.h): pinned + device 18-bit planes
+  PinBytes plo, phi;
+  DevBytes dlo, dhi;
+  cudaEvent_t pack_ev = nullptr;  // last DMA out of the pinned planes
+  bool pack_pending = false;
+  int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
+  int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0;
   // Device-memory match batches are read-only: they may overlap each other (a batch's
   // planner and grid ramp-up hide under the previous batch's tail) but not a mutation.
   // Each in-flight batch uses one slot (scratch + scheduler block + completion event).
@@ -369,21 +377,90 @@ int guarded(tm_store *s, F &&f) {
 
 // Stage host sequences into the pinned buffer with 128-byte aligned starts and copy
 // them to the device token scratch.  Returns device offsets (host vector).
+// Packed copy (hostpack.h) of host tokens into dtok: pieces sorted by destination,
+// disjoint, destinations multiples of 32.  Host threads pack chunk k+1 while the copy
+// engine moves chunk k and k_unpack18 expands it.  false: a token is outside [0, 2^18)
+// (nothing usable was written; the caller does the raw copy on the same stream).
+bool stage_packed(tm_store *s, const std::vector<tms::PackPiece> &pieces, int64_t end, int32_t *dtok, cudaStream_t st) {
+  end = round_up(std::max<int64_t>(end, 32), 32);
+  uint16_t *lo = (uint16_t *)s->plo.need(2 * (size_t)end);
+  uint8_t *hi = (uint8_t *)s->phi.need((size_t)end / 4);
+  uint16_t *dlo = (uint16_t *)s->dlo.need(2 * (size_t)end);
+  uint8_t *dhi = (uint8_t *)s->dhi.need((size_t)end / 4);
+  if (s->pack_pending) ck(cudaEventSynchronize(s->pack_ev), "pack staging free");
+  s->pack_pending = false;
+  int64_t total = 0;
+  for (const auto &p : pieces) total += p.len;
+  const int64_t chunk = std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(1) << 20, total / 16));
+  size_t a = 0;
+  while (a < pieces.size()) {
+    size_t b = a;
+    int64_t tok = 0;
+    while (b < pieces.size() && (b == a || tok < chunk)) tok += pieces[b++].len;
+    if (!tms::pack18(&pieces[a], (int64_t)(b - a), lo, hi)) {
+      ck(cudaEventRecord(s->pack_ev, st), "pack event");
+      s->pack_pending = true;
+      return false;
+    }
+    const int64_t p0 = pieces[a].dst, p1 = round_up(pieces[b - 1].dst + pieces[b - 1].len, 32);
+    ck(cudaMemcpyAsync(dlo + p0, lo + p0, 2 * (size_t)(p1 - p0), cudaMemcpyHostToDevice, st), "H2D low plane");
+    ck(cudaMemcpyAsync(dhi + p0 / 4, hi + p0 / 4, (size_t)(p1 - p0) / 4, cudaMemcpyHostToDevice, st), "H2D high plane");
+    ck(tms::launch_unpack18(dlo, dhi, dtok, p0, p1, s->num_sms, st), "unpack18");
+    a = b;
+  }
+  ck(cudaEventRecord(s->pack_ev, st), "pack event");
+  s->pack_pending = true;
+  return true;
+}
+
+void add_pieces(std::vector<tms::PackPiece> &out, const int32_t *src, int64_t dst, int64_t len) {
+  for (int64_t o = 0; o < len; o += tms::kPackPieceMax)
+    out.push_back({src + o, dst + o, std::min<int64_t>(tms::kPackPieceMax, len - o)});
+}
+
+bool use_packed(tm_store *s, int64_t tokens) {
+  return s->pack_min >= 0 && tokens >= s->pack_min && tms::pack18_supported();
+}
+
 void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off, const int64_t *tok_len,
                   std::vector<int64_t> &doff, const std::vector<int64_t> *perm, cudaStream_t st) {
   doff.resize(n);
-  // Fast path: every sequence already starts on a 128-byte boundary -> one direct
-  // H2D copy of the caller's buffer (pinned buffers go at full PCIe rate).  Padding
-  // words after a sequence are never compared (positions >= len are masked).
+  // Fast path: every sequence already starts on a 128-byte boundary -> the device copy
+  // keeps the caller's layout (one direct H2D of a pinned buffer goes at full PCIe rate).
+  // Padding words after a sequence are never compared (positions >= len are masked).
   bool aligned = true;
-  int64_t end = 0;
+  int64_t end = 0, ntok = 0;
   for (int64_t k = 0; k < n; k++) {
     aligned &= (tok_off[k] % tms::kAlignWords) == 0 && tok_off[k] >= 0;
     end = std::max<int64_t>(end, tok_off[k] + tok_len[k]);
+    ntok += tok_len[k];
   }
+  const bool packed = use_packed(s, ntok);
   if (aligned) {
     for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm ? (*perm)[k] : k];
-    void *d = s->dtok.need(sizeof(int32_t) * (size_t)(round_up(std::max<int64_t>(end, 1), tms::kAlignWords) + tms::kAlignWords));
+    int32_t *d = (int32_t *)s->dtok.need(sizeof(int32_t) * (size_t)(round_up(std::max<int64_t>(end, 1), tms::kAlignWords) + tms::kAlignWords));
+    if (packed) {
+      // the sequences' own ranges, merged (sequences may share words of the caller's buffer)
+      std::vector<std::pair<int64_t, int64_t>> iv;
+      iv.reserve(n);
+      for (int64_t k = 0; k < n; k++)
+        if (tok_len[k] > 0) iv.push_back({tok_off[k], tok_off[k] + tok_len[k]});
+      std::sort(iv.begin(), iv.end());
+      std::vector<tms::PackPiece> pieces;
+      for (size_t i = 0; i < iv.size();) {
+        int64_t a = iv[i].first, b = iv[i].second;
+        for (i++; i < iv.size() && iv[i].first < b; i++) b = std::max(b, iv[i].second);  // overlapping only
+        add_pieces(pieces, tokens + a, a, b - a);
+      }
+      if (stage_packed(s, pieces, end, d, st)) {
+        s->c_pack_calls++;
+        s->c_pack_tokens += ntok;
+        return;
+      }
+      s->c_pack_fallbacks++;
+    }
+    s->c_raw_calls++;
+    s->c_raw_tokens += ntok;
     if (end > 0) ck(cudaMemcpyAsync(d, tokens, sizeof(int32_t) * end, cudaMemcpyHostToDevice, st), "H2D tokens");
     return;
   }
@@ -393,6 +470,22 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
     doff[k] = total;
     total += round_up(std::max<int64_t>(tok_len[e], 1), tms::kAlignWords);
   }
+  int32_t *d = (int32_t *)s->dtok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
+  if (packed) {
+    std::vector<tms::PackPiece> pieces;
+    for (int64_t k = 0; k < n; k++) {
+      const int64_t e = perm ? (*perm)[k] : k;
+      add_pieces(pieces, tokens + tok_off[e], doff[k], tok_len[e]);
+    }
+    if (stage_packed(s, pieces, total, d, st)) {
+      s->c_pack_calls++;
+      s->c_pack_tokens += ntok;
+      return;
+    }
+    s->c_pack_fallbacks++;
+  }
+  s->c_raw_calls++;
+  s->c_raw_tokens += ntok;
   int32_t *h = (int32_t *)s->ptok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
   for (int64_t k = 0; k < n; k++) {
     int64_t e = perm ? (*perm)[k] : k;
@@ -401,7 +494,6 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
     int64_t pad = round_up(std::max<int64_t>(L, 1), tms::kAlignWords) - L;
     memset(h + doff[k] + L, 0, sizeof(int32_t) * (size_t)pad);
   }
-  void *d = s->dtok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
   if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, st), "H2D tokens");
 }
 
@@ -520,11 +612,13 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
   s->device = c.device;
   if (const char *e = getenv("TM_PLAN_MIN")) s->plan_min = atoll(e);
   if (const char *e = getenv("TM_PLAN_ROOTS")) s->plan_roots = atoi(e);
+  if (const char *e = getenv("TM_H2D_PACK_MIN")) s->pack_min = atoll(e);
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
     ck(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, c.device), "attr");
     ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&s->last, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&s->pack_ev, cudaEventDisableTiming), "event");
     ck(cudaMalloc((void **)&s->v.ctr, sizeof(int64_t) * 4), "ctr");
     ck(cudaMalloc((void **)&s->sched, sizeof(tms::Sched)), "sched");
     ck(cudaMemsetAsync(s->sched, 0, sizeof(tms::Sched), s->stream), "sched");
@@ -575,6 +669,7 @@ int tm_store_destroy(tm_store *s) {
       cudaEventDestroy(e.second);
     }
   cudaEventDestroy(s->last);
+  cudaEventDestroy(s->pack_ev);
   cudaStreamDestroy(s->stream);
   delete s;  // DevBytes / PinBytes members release scratch and pinned staging
   return TM_OK;
@@ -1133,6 +1228,13 @@ int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *are
     if (arena_used) *arena_used = s->arena_used;
     if (arena_cap) *arena_cap = s->arena_cap;
     if (max_depth) *max_depth = s->max_depth;
+  });
+}
+
+int tm_store_h2d_stats(tm_store *s, int64_t *out5) {
+  return guarded(s, [&] {
+    const int64_t c[5] = {s->c_pack_calls, s->c_pack_tokens, s->c_raw_calls, s->c_raw_tokens, s->c_pack_fallbacks};
+    memcpy(out5, c, sizeof(c));
   });
 }
 

@@ -122,6 +122,13 @@ class DeviceStore:
                 "export_tokens")
         return dict(zip(keys, c.tolist()))
 
+    def h2d_stats(self) -> dict:
+        """How host-memory token inputs crossed PCIe: packed 18-bit planes or raw int32
+        (tm_store_h2d_stats)."""
+        c = np.zeros(5, np.int64)
+        check(self.lib.tm_store_h2d_stats(self.h, _ptr(c)))
+        return dict(zip(("packed_calls", "packed_tokens", "raw_calls", "raw_tokens", "pack_fallbacks"), c.tolist()))
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(self.lib.tm_store_stream(self.h, C.byref(s)))
