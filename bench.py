@@ -8,8 +8,9 @@ batch through the K1 match kernel.
 
   value      queries/s with queries resident in HBM (device-timed, CUDA events on the
              launching stream, max over ranks)
-  e2e        the same through the C-ABI host-buffer call (pinned H2D of the query
-             tokens + D2H of the results inside the timed region)
+  e2e        the same through the C-ABI host-buffer call (the query tokens cross PCIe
+             inside the timed region - as 18-bit planes packed by the library's host
+             threads - and the results come back)
   roofline   K1 algorithmic bytes (8 B per compared token, c_q = min(m+1,|q|,|parent|))
              / K1 device time, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the C restatement of the reference radix tree (oracle/, "port"),
@@ -406,6 +407,7 @@ def main():
     pin_np = pin_tok.numpy()
     q_off = wl.q_off[:-1].copy()
     store.match(wl.q_sess, pin_np, q_off, wl.q_len)  # warm
+    tok_bytes0 = store.h2d_stats()["token_bytes"]
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
@@ -418,7 +420,9 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_elapsed = float(t.item())
     e2e_value = world * wl.n_queries * args.e2e_steps / e2e_elapsed
-    h2d = int(wl.q_off[-2] + wl.q_len[-1]) * 4 + wl.n_queries * (4 + 8 + 8)
+    # token bytes that crossed PCIe (packed 18-bit planes when the library packs them, see
+    # DESIGN.md "PCIe path") + the per-query session ids, offsets and lengths
+    h2d = (store.h2d_stats()["token_bytes"] - tok_bytes0) // args.e2e_steps + wl.n_queries * (4 + 8 + 8)
     d2h = wl.n_queries * 24
 
     peak, peak_kind = peaks()

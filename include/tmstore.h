@@ -148,11 +148,12 @@ int tm_store_stats(tm_store *store, int64_t *rows, int64_t *arena_used, int64_t 
  * match calls, queries, export calls, exported rows, exported tokens (8 int64). */
 int tm_store_counters(tm_store *store, int64_t *out8);
 
-/* Host->device token copies of host-memory calls (5 int64): calls sent as packed 18-bit
+/* Host->device token copies of host-memory calls (6 int64): calls sent as packed 18-bit
  * planes, their tokens, calls sent as raw int32, their tokens, packed attempts that fell
- * back to raw (a token outside [0, 2^18)).  Replaces nothing in the reference (its trie
- * is host-resident); TM_H2D_PACK_MIN (tokens per call, default 8M, <0 off) selects. */
-int tm_store_h2d_stats(tm_store *store, int64_t *out5);
+ * back to raw (a token outside [0, 2^18)), token bytes actually copied.  Replaces nothing
+ * in the reference (its trie is host-resident); TM_H2D_PACK_MIN (tokens per call,
+ * default 8M, <0 off) selects. */
+int tm_store_h2d_stats(tm_store *store, int64_t *out6);
 
 /* The store's CUDA stream (cudaStream_t) for callers that want to order work after it. */
 int tm_store_stream(tm_store *store, void **out_stream);

@@ -123,6 +123,8 @@ bool pack_tail(const int32_t *src, int64_t n, uint16_t *lo, uint8_t *hi) {
   return bad == 0;
 }
 
+}  // namespace
+
 __attribute__((target("avx2"))) bool pack_piece(const PackPiece &p, uint16_t *lo, uint8_t *hi) {
   const int64_t full = p.len / 32;
   __m256i bad = _mm256_setzero_si256();
@@ -133,8 +135,6 @@ __attribute__((target("avx2"))) bool pack_piece(const PackPiece &p, uint16_t *lo
   _mm_sfence();  // this thread's non-temporal stores land before it reports the piece done
   return ok;
 }
-
-}  // namespace
 
 bool pack18_supported() {
   static const bool ok = __builtin_cpu_supports("avx2");
@@ -151,13 +151,5 @@ int host_threads() {
 }
 
 void parallel_for(int64_t n, const std::function<void(int64_t)> &fn) { pool().run(n, fn); }
-
-bool pack18(const PackPiece *pieces, int64_t np, uint16_t *lo, uint8_t *hi) {
-  std::atomic<bool> ok{true};
-  parallel_for(np, [&](int64_t i) {
-    if (!pack_piece(pieces[i], lo, hi)) ok.store(false, std::memory_order_relaxed);
-  });
-  return ok.load();
-}
 
 }  // namespace tms

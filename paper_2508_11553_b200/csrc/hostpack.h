@@ -22,8 +22,9 @@ struct PackPiece {
 constexpr int64_t kPackPieceMax = 1 << 15;  // tokens per piece (work unit of one pool thread)
 
 bool pack18_supported();
-// Pack pieces [0, np) into lo / hi; false if any token is outside [0, 2^18).
-bool pack18(const PackPiece *pieces, int64_t np, uint16_t *lo, uint8_t *hi);
+// Pack one piece into lo / hi (non-temporal stores, fenced); false if any token is
+// outside [0, 2^18).
+bool pack_piece(const PackPiece &p, uint16_t *lo, uint8_t *hi);
 // Host thread pool shared by all stores of the process (TM_HOST_THREADS, default: all cores).
 int host_threads();
 void parallel_for(int64_t n, const std::function<void(int64_t)> &fn);

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -147,7 +149,8 @@ struct tm_store {
   cudaEvent_t pack_ev = nullptr;  // last DMA out of the pinned planes
   bool pack_pending = false;
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
-  int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0;
+  int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0,
+          c_h2d_bytes = 0;  // token bytes actually copied host->device
   // Device-memory match batches are read-only: they may overlap each other (a batch's
   // planner and grid ramp-up hide under the previous batch's tail) but not a mutation.
   // Each in-flight batch uses one slot (scratch + scheduler block + completion event).
@@ -378,9 +381,12 @@ int guarded(tm_store *s, F &&f) {
 // Stage host sequences into the pinned buffer with 128-byte aligned starts and copy
 // them to the device token scratch.  Returns device offsets (host vector).
 // Packed copy (hostpack.h) of host tokens into dtok: pieces sorted by destination,
-// disjoint, destinations multiples of 32.  Host threads pack chunk k+1 while the copy
-// engine moves chunk k and k_unpack18 expands it.  false: a token is outside [0, 2^18)
-// (nothing usable was written; the caller does the raw copy on the same stream).
+// disjoint, destinations multiples of 32.  One pool job packs every piece (threads take
+// pieces in order); whenever a chunk of pieces is complete the calling thread - between
+// its own pieces - enqueues that chunk's plane copies and its k_unpack18, so the copy
+// engine streams chunk k while the pool packs chunk k+1.  false: a token is outside
+// [0, 2^18) (the caller then does the raw copy on the same stream, which overwrites
+// whatever the packed chunks wrote).
 bool stage_packed(tm_store *s, const std::vector<tms::PackPiece> &pieces, int64_t end, int32_t *dtok, cudaStream_t st) {
   end = round_up(std::max<int64_t>(end, 32), 32);
   uint16_t *lo = (uint16_t *)s->plo.need(2 * (size_t)end);
@@ -391,25 +397,49 @@ bool stage_packed(tm_store *s, const std::vector<tms::PackPiece> &pieces, int64_
   s->pack_pending = false;
   int64_t total = 0;
   for (const auto &p : pieces) total += p.len;
-  const int64_t chunk = std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(1) << 20, total / 16));
-  size_t a = 0;
-  while (a < pieces.size()) {
-    size_t b = a;
-    int64_t tok = 0;
-    while (b < pieces.size() && (b == a || tok < chunk)) tok += pieces[b++].len;
-    if (!tms::pack18(&pieces[a], (int64_t)(b - a), lo, hi)) {
-      ck(cudaEventRecord(s->pack_ev, st), "pack event");
-      s->pack_pending = true;
-      return false;
+  const int64_t chunk = std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(1) << 19, total / 24));
+  std::vector<size_t> cbeg{0};  // chunk c = pieces [cbeg[c], cbeg[c+1])
+  std::vector<int32_t> chunk_of(pieces.size());
+  for (size_t i = 0, tok = 0; i < pieces.size(); i++) {
+    if (tok >= (size_t)chunk) {
+      cbeg.push_back(i);
+      tok = 0;
     }
-    const int64_t p0 = pieces[a].dst, p1 = round_up(pieces[b - 1].dst + pieces[b - 1].len, 32);
-    ck(cudaMemcpyAsync(dlo + p0, lo + p0, 2 * (size_t)(p1 - p0), cudaMemcpyHostToDevice, st), "H2D low plane");
-    ck(cudaMemcpyAsync(dhi + p0 / 4, hi + p0 / 4, (size_t)(p1 - p0) / 4, cudaMemcpyHostToDevice, st), "H2D high plane");
-    ck(tms::launch_unpack18(dlo, dhi, dtok, p0, p1, s->num_sms, st), "unpack18");
-    a = b;
+    chunk_of[i] = (int32_t)cbeg.size() - 1;
+    tok += pieces[i].len;
   }
+  const size_t nchunks = cbeg.size();
+  cbeg.push_back(pieces.size());
+  std::unique_ptr<std::atomic<int64_t>[]> left(new std::atomic<int64_t>[nchunks]);
+  for (size_t c = 0; c < nchunks; c++) left[c].store((int64_t)(cbeg[c + 1] - cbeg[c]));
+  std::atomic<bool> bad{false};
+  size_t issued = 0;
+  int64_t bytes = 0;
+  cudaError_t err = cudaSuccess;
+  const std::thread::id caller = std::this_thread::get_id();
+  auto issue_ready = [&] {  // calling thread only
+    while (issued < nchunks && err == cudaSuccess && !bad.load(std::memory_order_relaxed) &&
+           left[issued].load(std::memory_order_acquire) == 0) {
+      const tms::PackPiece &a = pieces[cbeg[issued]], &b = pieces[cbeg[issued + 1] - 1];
+      const int64_t p0 = a.dst, p1 = round_up(b.dst + b.len, 32);
+      err = cudaMemcpyAsync(dlo + p0, lo + p0, 2 * (size_t)(p1 - p0), cudaMemcpyHostToDevice, st);
+      if (err == cudaSuccess) err = cudaMemcpyAsync(dhi + p0 / 4, hi + p0 / 4, (size_t)(p1 - p0) / 4, cudaMemcpyHostToDevice, st);
+      if (err == cudaSuccess) err = tms::launch_unpack18(dlo, dhi, dtok, p0, p1, s->num_sms, st);
+      bytes += (p1 - p0) * 9 / 4;
+      issued++;
+    }
+  };
+  tms::parallel_for((int64_t)pieces.size(), [&](int64_t i) {
+    if (!tms::pack_piece(pieces[i], lo, hi)) bad.store(true, std::memory_order_relaxed);
+    left[chunk_of[i]].fetch_sub(1, std::memory_order_acq_rel);
+    if (std::this_thread::get_id() == caller) issue_ready();
+  });
+  issue_ready();  // the chunks finished by other threads after the caller's last piece
+  ck(err, "packed H2D");
   ck(cudaEventRecord(s->pack_ev, st), "pack event");
   s->pack_pending = true;
+  if (bad.load()) return false;
+  s->c_h2d_bytes += bytes;
   return true;
 }
 
@@ -461,6 +491,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
     }
     s->c_raw_calls++;
     s->c_raw_tokens += ntok;
+    s->c_h2d_bytes += 4 * end;
     if (end > 0) ck(cudaMemcpyAsync(d, tokens, sizeof(int32_t) * end, cudaMemcpyHostToDevice, st), "H2D tokens");
     return;
   }
@@ -486,6 +517,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
   }
   s->c_raw_calls++;
   s->c_raw_tokens += ntok;
+  s->c_h2d_bytes += 4 * total;
   int32_t *h = (int32_t *)s->ptok.need(sizeof(int32_t) * (size_t)std::max<int64_t>(total, 32));
   for (int64_t k = 0; k < n; k++) {
     int64_t e = perm ? (*perm)[k] : k;
@@ -1231,10 +1263,11 @@ int tm_store_stats(tm_store *s, int64_t *rows, int64_t *arena_used, int64_t *are
   });
 }
 
-int tm_store_h2d_stats(tm_store *s, int64_t *out5) {
+int tm_store_h2d_stats(tm_store *s, int64_t *out6) {
   return guarded(s, [&] {
-    const int64_t c[5] = {s->c_pack_calls, s->c_pack_tokens, s->c_raw_calls, s->c_raw_tokens, s->c_pack_fallbacks};
-    memcpy(out5, c, sizeof(c));
+    const int64_t c[6] = {s->c_pack_calls, s->c_pack_tokens, s->c_raw_calls, s->c_raw_tokens, s->c_pack_fallbacks,
+                          s->c_h2d_bytes};
+    memcpy(out6, c, sizeof(c));
   });
 }
 

@@ -125,9 +125,10 @@ class DeviceStore:
     def h2d_stats(self) -> dict:
         """How host-memory token inputs crossed PCIe: packed 18-bit planes or raw int32
         (tm_store_h2d_stats)."""
-        c = np.zeros(5, np.int64)
+        c = np.zeros(6, np.int64)
         check(self.lib.tm_store_h2d_stats(self.h, _ptr(c)))
-        return dict(zip(("packed_calls", "packed_tokens", "raw_calls", "raw_tokens", "pack_fallbacks"), c.tolist()))
+        keys = ("packed_calls", "packed_tokens", "raw_calls", "raw_tokens", "pack_fallbacks", "token_bytes")
+        return dict(zip(keys, c.tolist()))
 
     def stream(self) -> int:
         s = C.c_void_p()
