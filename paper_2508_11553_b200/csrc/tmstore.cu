@@ -149,6 +149,8 @@ struct tm_store {
   cudaEvent_t pack_ev = nullptr;  // last DMA out of the pinned planes
   bool pack_pending = false;
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
+  bool pack_auto = true;                // TM_H2D_PACK_MIN unset: pack only as the node's sole GPU client
+  int local_world = 1;                  // LOCAL_WORLD_SIZE (torchrun) at creation
   int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0,
           c_h2d_bytes = 0;  // token bytes actually copied host->device
   // Device-memory match batches are read-only: they may overlap each other (a batch's
@@ -448,8 +450,16 @@ void add_pieces(std::vector<tms::PackPiece> &out, const int32_t *src, int64_t ds
     out.push_back({src + o, dst + o, std::min<int64_t>(tms::kPackPieceMax, len - o)});
 }
 
+std::atomic<int> g_live_stores{0};
+
+// Packing halves the PCIe bytes but doubles the host-memory traffic (read 4 B, write
+// 2.25 B, DMA-read 2.25 B per token instead of DMA-read 4 B).  It pays while PCIe is the
+// bottleneck - one GPU client per node - and loses once several GPUs' copies share the
+// host memory bandwidth, so by default it is used only when this
+// is the node's sole GPU client (one rank, one live store).
 bool use_packed(tm_store *s, int64_t tokens) {
-  return s->pack_min >= 0 && tokens >= s->pack_min && tms::pack18_supported();
+  if (s->pack_min < 0 || tokens < s->pack_min || !tms::pack18_supported()) return false;
+  return !s->pack_auto || (s->local_world == 1 && g_live_stores.load() == 1);
 }
 
 void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off, const int64_t *tok_len,
@@ -644,7 +654,11 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
   s->device = c.device;
   if (const char *e = getenv("TM_PLAN_MIN")) s->plan_min = atoll(e);
   if (const char *e = getenv("TM_PLAN_ROOTS")) s->plan_roots = atoi(e);
-  if (const char *e = getenv("TM_H2D_PACK_MIN")) s->pack_min = atoll(e);
+  if (const char *e = getenv("TM_H2D_PACK_MIN")) {
+    s->pack_min = atoll(e);
+    s->pack_auto = false;
+  }
+  if (const char *e = getenv("LOCAL_WORLD_SIZE")) s->local_world = std::max(1, atoi(e));
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
     ck(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, c.device), "attr");
@@ -674,6 +688,7 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
     delete s;
     return rc;
   }
+  g_live_stores.fetch_add(1);
   *out = s;
   return TM_OK;
 }
@@ -703,6 +718,7 @@ int tm_store_destroy(tm_store *s) {
   cudaEventDestroy(s->last);
   cudaEventDestroy(s->pack_ev);
   cudaStreamDestroy(s->stream);
+  g_live_stores.fetch_sub(1);
   delete s;  // DevBytes / PinBytes members release scratch and pinned staging
   return TM_OK;
 }

@@ -155,3 +155,22 @@ def test_small_calls_stay_raw_by_default():
         assert h["packed_calls"] == 0 and h["raw_calls"] == 1
     finally:
         st.close()
+
+
+def test_auto_policy_stays_raw_with_several_gpu_clients():
+    """TM_H2D_PACK_MIN unset: packing doubles host-memory traffic, so it is skipped when
+    more than one store is live in the process (or LOCAL_WORLD_SIZE > 1)."""
+    from paper_2508_11553_b200 import DeviceStore
+
+    assert "TM_H2D_PACK_MIN" not in os.environ
+    a, b = DeviceStore(0), DeviceStore(0)
+    try:
+        s = a.new_session()
+        n = 9 << 20  # above the 8M-token default threshold
+        toks = (np.arange(n, dtype=np.int64) % 151936).astype(np.int32)
+        a.record_one(s, toks, (np.zeros(1, np.int32), np.zeros(1, np.uint8), np.zeros(1, np.int32)))
+        h = a.h2d_stats()
+        assert h["packed_calls"] == 0 and h["raw_calls"] == 1 and h["token_bytes"] == 4 * n
+    finally:
+        a.close()
+        b.close()
