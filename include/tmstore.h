@@ -91,6 +91,12 @@ int tm_record_batch(tm_store *store, int64_t n, int32_t mem, const int32_t *sids
                     int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
                     int32_t *out_parent_local, int64_t *out_added, void *stream);
 
+/* One record of host arrays (the per-request lpm_insert path, trie.py:120-179) without
+ * building batch arrays: out6 = matched, row, local, parent, parent_local, added.
+ * Same semantics and errors as tm_record_batch with n = 1. */
+int tm_record_one(tm_store *store, int32_t sid, const int32_t *tokens, int64_t ntok, const int32_t *run_start,
+                  const uint8_t *run_origin, const int32_t *run_version, int64_t nruns, int64_t *out6);
+
 /* Read-only longest-prefix match of a batch of queries (no mutation): the LPM walk
  * of lpm_insert (trie.py:136-158) without the record step.
  *   out_matched[n]   LCP length with the best stored sequence of the session

@@ -33,6 +33,7 @@ SIGNATURES = {
     "tm_session_create": (C.c_int, [_P, _P]),
     "tm_session_count": (C.c_int, [_P, _P]),
     "tm_record_batch": (C.c_int, [_P, _I64, _I32] + [_P] * 15),
+    "tm_record_one": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, _P, C.c_int64, _P]),
     "tm_match_batch": (C.c_int, [_P, _I64, _I32] + [_P] * 8),
     "tm_rows_total": (C.c_int, [_P, _I64, _P, _P]),
     "tm_export_rows": (C.c_int, [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P]),

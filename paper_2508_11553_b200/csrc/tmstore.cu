@@ -147,6 +147,7 @@ struct tm_store {
   PinBytes plo, phi;
   DevBytes dlo, dhi;
   cudaEvent_t pack_ev = nullptr;  // last DMA out of the pinned planes
+  int64_t *pin_ctr = nullptr;     // pinned copy of the device counters (arena, rows, runs, error)
   bool pack_pending = false;
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
   bool pack_auto = true;                // TM_H2D_PACK_MIN unset: pack only as the node's sole GPU client
@@ -332,13 +333,24 @@ void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaSt
 }
 
 // a device-side error code (kernels.cuh kErr*) becomes a loud host error
+[[noreturn]] void raise_device_error(int64_t code) {
+  static const char *names[] = {"", "branch index full", "arena bounds", "row bounds", "run bounds"};
+  fail(TM_ECUDA, std::string("device check failed: ") + (code > 0 && code < 5 ? names[code] : "unknown"));
+}
+
 void check_device_error(tm_store *s) {
   int64_t code = 0;
   ck(cudaMemcpy(&code, s->v.ctr + 3, sizeof(code), cudaMemcpyDeviceToHost), "D2H error flag");
-  if (code) {
-    static const char *names[] = {"", "branch index full", "arena bounds", "row bounds", "run bounds"};
-    fail(TM_ECUDA, std::string("device check failed: ") + (code > 0 && code < 5 ? names[code] : "unknown"));
-  }
+  if (code) raise_device_error(code);
+}
+
+// host-memory calls: queue the counters' readback into pinned memory before the final
+// sync (no extra round trip), then check the error word after it
+void enqueue_ctr_readback(tm_store *s, cudaStream_t st) {
+  ck(cudaMemcpyAsync(s->pin_ctr, s->v.ctr, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H counters");
+}
+void check_ctr_error(const tm_store *s) {
+  if (s->pin_ctr[3]) raise_device_error(s->pin_ctr[3]);
 }
 
 bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->rows.size() && s->rows[r].sid >= 0; }
@@ -665,6 +677,7 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
     ck(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&s->last, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&s->pack_ev, cudaEventDisableTiming), "event");
+    ck(cudaHostAlloc((void **)&s->pin_ctr, 64, cudaHostAllocDefault), "pinned counters");
     ck(cudaMalloc((void **)&s->v.ctr, sizeof(int64_t) * 4), "ctr");
     ck(cudaMalloc((void **)&s->sched, sizeof(tms::Sched)), "sched");
     ck(cudaMemsetAsync(s->sched, 0, sizeof(tms::Sched), s->stream), "sched");
@@ -717,6 +730,7 @@ int tm_store_destroy(tm_store *s) {
     }
   cudaEventDestroy(s->last);
   cudaEventDestroy(s->pack_ev);
+  if (s->pin_ctr) cudaFreeHost(s->pin_ctr);
   cudaStreamDestroy(s->stream);
   g_live_stores.fetch_sub(1);
   delete s;  // DevBytes / PinBytes members release scratch and pinned staging
@@ -890,13 +904,11 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     }
     // ---- results back (chain order), into the host mirror in batch order
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
-    int64_t ctr[4];
-    int64_t dev_err = 0;
-    ck(cudaMemcpyAsync(ctr, s->v.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream), "D2H ctr");
-    ck(cudaMemcpyAsync(&dev_err, s->v.ctr + 3, sizeof(dev_err), cudaMemcpyDeviceToHost, s->stream), "D2H err");
+    enqueue_ctr_readback(s, s->stream);
     mark_done(s, s->stream);
     ck(cudaStreamSynchronize(s->stream), "record sync");
-    if (dev_err) check_device_error(s);
+    check_ctr_error(s);
+    const int64_t *ctr = s->pin_ctr;
     const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
     const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
@@ -933,6 +945,20 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     s->c_records += n;
     for (int64_t e = 0; e < n; e++) s->c_record_tokens += tok_len[e];
   });
+}
+
+int tm_record_one(tm_store *s, int32_t sid, const int32_t *tokens, int64_t ntok, const int32_t *run_start,
+                  const uint8_t *run_origin, const int32_t *run_version, int64_t nruns, int64_t *out6) {
+  const int64_t off = 0, run_off[2] = {0, nruns};
+  int64_t m = 0, row = 0, par = 0, added = 0;
+  int32_t local = 0, par_local = 0;
+  const int rc = tm_record_batch(s, 1, TM_MEM_HOST, &sid, tokens, &off, &ntok, run_off, run_start, run_origin,
+                                 run_version, &m, &row, &local, &par, &par_local, &added, nullptr);
+  if (rc == TM_OK && out6) {
+    const int64_t o[6] = {m, row, local, par, par_local, added};
+    memcpy(out6, o, sizeof(o));
+  }
+  return rc;
 }
 
 int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, const int32_t *tokens,
@@ -1004,9 +1030,10 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
     if (mem == TM_MEM_HOST) {
       char *h = (char *)s->pin.need(lay.bytes);
       ck(cudaMemcpyAsync(h + o_m, d + o_m, out_end - o_m, cudaMemcpyDeviceToHost, st), "D2H");
+      enqueue_ctr_readback(s, st);
       mark_done(s, st);
       ck(cudaStreamSynchronize(st), "match sync");
-      check_device_error(s);
+      check_ctr_error(s);
       memcpy(out_matched, h + o_m, 8 * n);
       if (out_parent) memcpy(out_parent, h + o_par, 8 * n);
       if (out_dup) memcpy(out_dup, h + o_dup, 8 * n);
@@ -1064,8 +1091,11 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       o_ver = lay.add(4 * total);
       o_resp = lay.add(8 * n);
     }
+    // small host exports come back in ONE copy through the pinned staging (the outputs
+    // are contiguous in the layout) and one sync; large ones stream through d2h_pageable
+    const bool small_host = mem_out == TM_MEM_HOST && lay.bytes - o_tok <= (size_t(8) << 20);
     char *d = (char *)s->scratch.need(lay.bytes);
-    char *h = (char *)s->pin.need(in_bytes);
+    char *h = (char *)s->pin.need(small_host ? lay.bytes : in_bytes);
     memcpy(h + o_rows, rows, 8 * n);
     memcpy(h + o_off, out_offsets, 8 * (n + 1));
     memcpy(h + o_tile, tile.data(), 8 * (n + 1));
@@ -1093,14 +1123,25 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       ProfScope ps(s, 2, st);
       ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
     }
-    if (mem_out == TM_MEM_HOST) {
+    if (small_host) {
+      ck(cudaMemcpyAsync(h + o_tok, d + o_tok, lay.bytes - o_tok, cudaMemcpyDeviceToHost, st), "D2H export");
+      enqueue_ctr_readback(s, st);
+      mark_done(s, st);
+      ck(cudaStreamSynchronize(st), "export sync");
+      check_ctr_error(s);
+      if (out_tokens) memcpy(out_tokens, h + o_tok, 4 * (size_t)total);
+      if (out_mask) memcpy(out_mask, h + o_msk, (size_t)total);
+      if (out_versions) memcpy(out_versions, h + o_ver, 4 * (size_t)total);
+      if (out_resp_start) memcpy(out_resp_start, h + o_resp, 8 * (size_t)n);
+    } else if (mem_out == TM_MEM_HOST) {
       if (out_tokens) d2h_pageable(s, out_tokens, e.tokens, 4 * total, st);
       if (out_mask) d2h_pageable(s, out_mask, e.mask, total, st);
       if (out_versions) d2h_pageable(s, out_versions, e.versions, 4 * total, st);
       if (out_resp_start) ck(cudaMemcpyAsync(out_resp_start, e.resp, 8 * n, cudaMemcpyDeviceToHost, st), "D2H resp");
+      enqueue_ctr_readback(s, st);
       mark_done(s, st);
       ck(cudaStreamSynchronize(st), "export sync");
-      check_device_error(s);
+      check_ctr_error(s);
     } else {
       mark_done(s, st);
     }

@@ -63,14 +63,15 @@ class TrieNode:
         return bool(self.leaf_marks)
 
 
-def _as_int32(values) -> np.ndarray:
-    """Token ids -> int32 array at C speed (array.array), rejecting ids outside int32."""
+def _as_int32(values):
+    """Token ids -> an int32 buffer at C speed (array.array for lists, numpy arrays as
+    int32), rejecting ids outside int32."""
     if isinstance(values, np.ndarray):
         if values.size and (values.min() < -(2**31) or values.max() >= 2**31):
             raise ValueError("token ids must fit in int32")
         return np.ascontiguousarray(values, np.int32)
     try:
-        return np.frombuffer(array.array("i", values), np.int32)
+        return array.array("i", values)
     except OverflowError:
         raise ValueError("token ids must fit in int32") from None
 
