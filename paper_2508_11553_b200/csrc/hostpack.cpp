@@ -136,6 +136,31 @@ __attribute__((target("avx2"))) bool pack_piece(const PackPiece &p, uint16_t *lo
   return ok;
 }
 
+__attribute__((target("avx2"))) static void copy_stream_avx2(char *dst, const char *src, size_t n) {
+  size_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+  if (head > n) head = n;
+  memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256((const __m256i *)(src + i)), b = _mm256_loadu_si256((const __m256i *)(src + i + 32));
+    const __m256i c = _mm256_loadu_si256((const __m256i *)(src + i + 64)), d = _mm256_loadu_si256((const __m256i *)(src + i + 96));
+    _mm256_stream_si256((__m256i *)(dst + i), a);
+    _mm256_stream_si256((__m256i *)(dst + i + 32), b);
+    _mm256_stream_si256((__m256i *)(dst + i + 64), c);
+    _mm256_stream_si256((__m256i *)(dst + i + 96), d);
+  }
+  memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
+void copy_stream(void *dst, const void *src, size_t n) {
+  if (pack18_supported()) copy_stream_avx2((char *)dst, (const char *)src, n);
+  else memcpy(dst, src, n);
+}
+
 bool pack18_supported() {
   static const bool ok = __builtin_cpu_supports("avx2");
   return ok;

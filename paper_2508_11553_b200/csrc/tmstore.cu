@@ -299,13 +299,16 @@ struct ProfScope {
 // through a small bounce buffer (measured ~1.5-5 GB/s here), so pipeline 64 MB chunks
 // through two pinned slots and spread the pinned->pageable memcpy over host threads.
 void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaStream_t st) {
-  constexpr int64_t CH = 64ll << 20;
+  static const int64_t CH = [] {  // TM_D2H_CHUNK_MB (tuning only)
+    const char *e = getenv("TM_D2H_CHUNK_MB");
+    return (e ? std::max(1, atoi(e)) : 64) * (int64_t(1) << 20);
+  }();
   if (bytes <= (8ll << 20)) {
     ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "D2H sync");
     return;
   }
-  const int nthreads = std::max(1, std::min(8, (int)std::thread::hardware_concurrency()));
+  const int64_t nparts = 4 * (int64_t)tms::host_threads();
   const int64_t nch = (bytes + CH - 1) / CH;
   cudaEvent_t ev[2];
   for (auto &e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -321,13 +324,11 @@ void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaSt
     if (c + 1 < nch) issue(c + 1);
     const int64_t off = c * CH, len = std::min(CH, bytes - off);
     const char *slot = (const char *)s->d2h_slot[c & 1].p;
-    std::vector<std::thread> th;
-    const int64_t part = (len + nthreads - 1) / nthreads;
-    for (int k = 0; k < nthreads; k++) {
+    const int64_t part = (len + nparts - 1) / nparts;  // pool threads copy (and first-touch) the destination
+    tms::parallel_for(nparts, [&](int64_t k) {
       const int64_t a = k * part, b = std::min(len, a + part);
-      if (a < b) th.emplace_back([=] { memcpy((char *)dst + off + a, slot + a, (size_t)(b - a)); });
-    }
-    for (auto &x : th) x.join();
+      if (a < b) tms::copy_stream((char *)dst + off + a, slot + a, (size_t)(b - a));
+    });
   }
   for (auto &e : ev) cudaEventDestroy(e);
 }

@@ -332,6 +332,30 @@ def test_edge_cases_long_sequences_and_extremes(store):
         trie.lpm_insert([2**31], [SpanOrigin.AGENT_INPUT], [0])
 
 
+def test_large_host_exports_stream_through_pinned_chunks(store):
+    """Exports and NDJSON larger than the single-copy limit (8 MB) come back through the
+    chunked pinned pipeline (several chunks, odd sizes); every byte must match."""
+    from paper_2508_11553_b200 import Trajectory, trajectory_to_line
+
+    rng = np.random.default_rng(9)
+    sid = store.new_session()
+    L = (5 << 20) + 12345  # 20 MB of tokens: several 64 MB-or-less chunks across the three arrays
+    h = rng.integers(0, 151936, L).astype(np.int32)
+    org = (np.arange(L) // 100_000 % 2).astype(np.uint8)
+    ver = (np.arange(L) // 1_000_000).astype(np.int32)
+    starts = np.flatnonzero(np.r_[True, (org[1:] != org[:-1]) | (ver[1:] != ver[:-1])])
+    r = store.record_one(sid, h, (starts.astype(np.int32), org[starts], ver[starts]))
+    row = int(r.row[0])
+    p = store.export([row, row])
+    for k in range(2):
+        a, b = p.offsets[k], p.offsets[k + 1]
+        assert np.array_equal(p.tokens[a:b], h) and np.array_equal(p.loss_mask[a:b], org)
+        assert np.array_equal(p.versions[a:b], ver)
+    text = store.export_ndjson([row], ["s-large"])
+    t = Trajectory.from_packed("s-large", h, org, ver)
+    assert text == (trajectory_to_line(t) + "\n").encode()
+
+
 def test_hypothesis_naive_oracle_property(store):
     """pkg/tests/test_trie.py:148-174 on the GPU trie: matched == max LCP (the NaiveStore
     oracle), storage == distinct prefixes, every sequence reconstructible, well formed."""
