@@ -527,8 +527,8 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
   }
 }
 
-template <int NT, int U, bool TMA = false>
-__global__ void __launch_bounds__(NT) k_record(DevView v, RecordArgs a) {
+template <int NT, int U, bool TMA = false, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_record(DevView v, RecordArgs a) {
   const Batch &b = a.b;
   __shared__ WalkShared sh;
   __shared__ long long s_item;
@@ -1107,22 +1107,26 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
   }
 }
 
-template <int NT, int U, bool TMA = false>
+template <int NT, int U, bool TMA = false, int MINB = 1>
 static cudaError_t record_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<NT, U, TMA>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<NT, U, TMA, MINB>, NT, 0);
     if (occ < 1) occ = 1;
   }
   int64_t grid = (int64_t)num_sms * occ;
   if (grid > a.nchains) grid = a.nchains;
   if (grid < 1) grid = 1;
-  k_record<NT, U, TMA><<<(int)grid, NT, 0, s>>>(v, a);
+  k_record<NT, U, TMA, MINB><<<(int)grid, NT, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 
-// TM_RECORD_VARIANT (tuning only): "64x4" (default: 78 regs -> more resident chains;
-// c2 record 0.26 ms vs 0.35 for 64x8), "64x8", "32x8", "32x4"
+// Default: chains are serial inside, so K2 runs best with every chain resident at once and
+// as many bytes in flight per chain as that allows.  Up to 7 chains per SM: 128-thread
+// CTAs (<= 72 registers, 7 per SM; c2, 1,000 chains: 0.234 ms vs 0.255 for 64x4); more
+// chains: 64-thread CTAs, 14 per SM (c3, 4,000 chains: 0.065 ms vs 0.073-0.086).
+// TM_RECORD_VARIANT (tuning only): "64x4", "64x8", "32x8", "32x4", "tma", "128x4",
+// "128x2", "256x2", "64x4m"
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
   static int variant = -1;
   if (variant < 0) {
@@ -1130,9 +1134,14 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
     variant = 0;
     if (e) {
       if (!strcmp(e, "64x8")) variant = 1;
+      else if (!strcmp(e, "64x4")) variant = 9;
       else if (!strcmp(e, "32x8")) variant = 2;
       else if (!strcmp(e, "32x4")) variant = 3;
       else if (!strcmp(e, "tma")) variant = 4;
+      else if (!strcmp(e, "128x4")) variant = 5;
+      else if (!strcmp(e, "128x2")) variant = 6;
+      else if (!strcmp(e, "256x2")) variant = 7;
+      else if (!strcmp(e, "64x4m")) variant = 8;
     }
   }
   switch (variant) {
@@ -1140,7 +1149,14 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
     case 2: return record_variant<32, 8>(v, a, num_sms, s);
     case 3: return record_variant<32, 4>(v, a, num_sms, s);
     case 4: return record_variant<64, 4, true>(v, a, num_sms, s);
-    default: return record_variant<64, 4>(v, a, num_sms, s);
+    case 5: return record_variant<128, 4, false, 7>(v, a, num_sms, s);
+    case 6: return record_variant<128, 2, false, 8>(v, a, num_sms, s);
+    case 7: return record_variant<256, 2, false, 4>(v, a, num_sms, s);
+    case 8: return record_variant<64, 4, false, 14>(v, a, num_sms, s);
+    case 9: return record_variant<64, 4>(v, a, num_sms, s);
+    default:
+      if (a.nchains <= (int64_t)num_sms * 7) return record_variant<128, 4, false, 7>(v, a, num_sms, s);
+      return record_variant<64, 4, false, 14>(v, a, num_sms, s);
   }
 }
 
