@@ -55,7 +55,7 @@ def parse():
                     help="c4 (default): per-rank 10k x 32k shard, host-routed; c5: 1M-session store sharded "
                          "by session hash with GPU-originated batches routed over NVLink (fused P2P K1)")
     ap.add_argument("--c5-sessions", type=int, default=1_000_000)
-    ap.add_argument("--routing", default="fused", choices=["fused", "nccl"],
+    ap.add_argument("--routing", default="fused", choices=["fused", "fused-nccl-barrier", "nccl"],
                     help="c5 exchange: fused P2P K1 (product) or NCCL all-to-all + local match (baseline)")
     ap.add_argument("--mixed", default=None,
                     help="lo,hi: log-uniform history lengths (config-5 shard) instead of fixed --hist")
@@ -215,7 +215,8 @@ def run_c5(args):
     router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
     wl.fill_queries(router)
     torch.cuda.synchronize()
-    route = router.match if args.routing == "fused" else router.match_nccl
+    route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
+             "nccl": router.match_nccl}[args.routing]
     for _ in range(max(3, args.warmup)):
         route(wl.n_queries)
     torch.cuda.synchronize()
@@ -240,10 +241,15 @@ def run_c5(args):
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
-        while time.perf_counter() - t_wall < 1.0:
-            for _ in range(10):
-                route(wl.n_queries)
-            torch.cuda.synchronize()
+        # keep the clocks sampler running for >= 1 s under load; every rank must make the
+        # same number of (collective) routed calls, so the count is agreed on first
+        left = torch.tensor([max(0.0, 1.0 - (time.perf_counter() - t_wall))], device=dev, dtype=torch.float64)
+        per = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(left, op=dist.ReduceOp.MAX)
+        dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        for _ in range(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1):
+            route(wl.n_queries)
+        torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -264,9 +270,11 @@ def run_c5(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": "c5", "sessions_total": args.c5_sessions, "history_tokens": "log-uniform [1024, 131072]",
                    "batch_queries_per_rank": wl.n_queries, "owner": "splitmix64(gsid) mod N",
-                   "routing": ("fused P2P K1: owners read requester HBM over NVLink, write results back"
-                               if args.routing == "fused" else
-                               "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"),
+                   "routing": {"fused": "fused P2P K1: owners read requester HBM over NVLink, write results back; "
+                                        "device-side epoch-flag barriers (no collective call per batch)",
+                               "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
+                               "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
+                                   args.routing],
                    "cross_shard_frac": float(remote.mean()), "shard_build_s": build_s,
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,
@@ -282,7 +290,8 @@ def run_c5(args):
                      "traffic": None,
                      "note": "N>1: remote query bytes cross NVLink (tools/p2p_probe: SM peer reads 780 GB/s one "
                              "direction, 670 GB/s both directions at once); history bytes come from local HBM"},
-        "gpu_launches": args.steps * 2,  # k_route + k_walk_routed per batch
+        # ours per batch: k_route + k_walk_routed (+ k_route_arrive + k_route_wait_done with device barriers)
+        "gpu_launches": args.steps * (4 if args.routing == "fused" else 2),
         "clocks": clk.summary(),
     }
     if rank == 0:

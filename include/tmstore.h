@@ -191,6 +191,16 @@ int tm_route_counts(tm_store *store, const void *region, int32_t *out_counts16, 
 int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
                     void *stream);
 
+/* tm_match_routed with the two cross-rank barriers done on the device instead of by the
+ * caller: a 32-thread kernel writes this rank's `arrive` epoch into every peer's region
+ * header (NVLink store, release), the owners' match kernel waits for all arrivals
+ * (acquire), its last CTA writes `done` into every requester's header, and a wait
+ * kernel on this rank's stream holds later work until every owner is done.  `epoch`:
+ * the same value on every rank, one larger per routed call (1, 2, ...).  A peer that
+ * never signals becomes a device error after 20 s (tm_synchronize reports it). */
+int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
+                         const int32_t *g2l, int64_t epoch, void *stream);
+
 /* Snapshot / restore (the reference store is in-memory only, trajectory.py:128): write
  * the arena, row table, metadata runs, session counters and the host row mirror to a
  * file; load them into an EMPTY store (any GPU), rebuilding the branch index. */

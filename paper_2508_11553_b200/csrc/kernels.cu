@@ -161,7 +161,7 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
 
 // The last CTA out leaves the scheduler block zeroed for the next launch, so a steady
 // stream of batches needs no memset.
-__device__ __forceinline__ void sched_exit(Sched *sc) {
+__device__ __forceinline__ bool sched_exit(Sched *sc) {  // thread 0: true in the last CTA out
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&sc->exit, 1u) == gridDim.x - 1) {
@@ -170,8 +170,10 @@ __device__ __forceinline__ void sched_exit(Sched *sc) {
       sc->work2 = 0;
       sc->exit = 0;
       __threadfence();
+      return true;
     }
   }
+  return false;
 }
 
 // 64-thread CTAs: ask for 6 resident per SM (<= 170 registers) so the walk keeps 6 CTAs
@@ -317,6 +319,58 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
     idx[atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1)] = (int32_t)i;
 }
 
+// ---- device-side cross-rank barriers (epoch flags in the RouteDesc headers) ----------
+__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr uint64_t kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;  // a dead peer becomes an error, not a hang
+
+// Spin until flags[0..nranks) >= epoch in this rank's own header.  false on timeout
+// (the error word is set; callers stop waiting so the stream drains).
+__device__ bool wait_flags(const DevView &v, const int64_t *flags, int nranks, int64_t epoch) {
+  const uint64_t t0 = globaltimer_ns();
+  for (int p = 0; p < nranks; p++) {
+    while (ld_acquire_sys(flags + p) < epoch) {
+      if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+        dev_error(v, kErrPeerTimeout);
+        return false;
+      }
+      __nanosleep(256);
+    }
+  }
+  return true;
+}
+
+// This rank's batch is bucketed (stream order: k_route ran before): tell every owner.
+__global__ void k_route_arrive(RoutedArgs a) {
+  if (threadIdx.x == 0) __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.nranks) {
+    RouteDesc *d = reinterpret_cast<RouteDesc *>(const_cast<char *>(a.peer[threadIdx.x]));
+    st_release_sys(&d->arrive[a.rank], a.epoch);
+  }
+}
+
+// Requester side: every owner has written this rank's results (they are visible to the
+// work queued after this kernel).
+__global__ void k_route_wait_done(DevView v, RoutedArgs a) {
+  if (threadIdx.x == 0) {
+    const RouteDesc *d = reinterpret_cast<const RouteDesc *>(a.peer[a.rank]);
+    wait_flags(v, d->done, a.nranks, a.epoch);
+    __threadfence_system();
+  }
+}
+
 // Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
 // and the other ranks' (query bytes over NVLink).  1/np of the CTAs start on the local
 // queue and the rest on the remote one, each falling back to the other when its queue
@@ -344,6 +398,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   int *s_pre = reinterpret_cast<int *>(dyn + (np > 1 ? (sizeof(RoutedRing) + 15) / 16 * 16 : 0));  // ncell + 2
   int *s_bs = s_pre + ncell + 2;
   int *s_peer = s_bs + ncell;
+  if (a.epoch > 0) {  // device-side barrier: every requester has bucketed its batch
+    if (threadIdx.x == 0)
+      wait_flags(v, reinterpret_cast<const RouteDesc *>(a.peer[a.rank])->arrive, np, a.epoch);
+    __syncthreads();
+  }
   // cell c: local cells first (bucket order), then remote cells (bucket, peer) order
   for (int c = threadIdx.x; c < ncell; c += NT) {
     int bk, p;
@@ -393,7 +452,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
     const int cell = s_cell;
     __syncthreads();
     if (it < 0) {
-      sched_exit(a.sched);
+      if (sched_exit(a.sched) && a.epoch > 0) {  // last CTA out: results are written, tell every requester
+        __threadfence_system();
+        for (int p = 0; p < np; p++)
+          st_release_sys(&reinterpret_cast<RouteDesc *>(const_cast<char *>(a.peer[p]))->done[a.rank], a.epoch);
+      }
       return;
     }
     const int p = s_peer[cell];
@@ -1223,6 +1286,16 @@ int export_tile_tokens() { return kExportTile; }
 
 cudaError_t launch_route(char *region, int nranks, cudaStream_t s) {
   k_route<<<1, kRouteNT, 0, s>>>(region, nranks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route_arrive(const RoutedArgs &a, cudaStream_t s) {
+  k_route_arrive<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaStream_t s) {
+  k_route_wait_done<<<1, 32, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 

@@ -55,6 +55,7 @@ enum : long long {
   kErrArena = 2,       // arena access outside its capacity
   kErrRow = 3,         // row id outside the row table
   kErrRun = 4,         // metadata run outside the run table
+  kErrPeerTimeout = 5, // a peer rank never signalled (routed match, device-side barrier)
 };
 
 __device__ __forceinline__ void dev_error(const DevView &v, long long code) {
@@ -102,6 +103,12 @@ struct RouteDesc {
   // process every requester's queries in one global longest-first order
   int32_t bcount[kMaxRanks * kPlanNB];
   int32_t bstart[kMaxRanks * kPlanNB];
+  // device-side barrier flags (epochs), written by the peers over NVLink: arrive[p] =
+  // peer p has bucketed its batch for epoch e; done[p] = owner p has finished every query
+  // of this rank's batch for epoch e (its results are visible).  Never rewritten by
+  // tm_route_prepare; zero at allocation.
+  int64_t arrive[kMaxRanks];
+  int64_t done[kMaxRanks];
 };
 
 struct RoutedArgs {
@@ -109,6 +116,7 @@ struct RoutedArgs {
   const char *peer[kMaxRanks];  // every rank's region as mapped on this GPU (own included)
   const int32_t *g2l;           // global session id -> local session id (-1: not owned)
   Sched *sched;
+  int64_t epoch;                // > 0: device-side barriers (wait for arrive, signal done)
 };
 
 // one batch of sequences resident on the device

@@ -335,8 +335,9 @@ void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaSt
 
 // a device-side error code (kernels.cuh kErr*) becomes a loud host error
 [[noreturn]] void raise_device_error(int64_t code) {
-  static const char *names[] = {"", "branch index full", "arena bounds", "row bounds", "run bounds"};
-  fail(TM_ECUDA, std::string("device check failed: ") + (code > 0 && code < 5 ? names[code] : "unknown"));
+  static const char *names[] = {"", "branch index full", "arena bounds", "row bounds", "run bounds",
+                                "peer rank timed out (routed match)"};
+  fail(TM_ECUDA, std::string("device check failed: ") + (code > 0 && code < 6 ? names[code] : "unknown"));
 }
 
 void check_device_error(tm_store *s) {
@@ -1409,9 +1410,9 @@ int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *
   });
 }
 
-int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                    void *stream) {
-  NvtxRange nvtx_("tm_match_routed");
+namespace {
+int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                 int64_t epoch, void *stream) {
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
@@ -1424,13 +1425,33 @@ int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer
     for (int p = 0; p < nranks; p++) a.peer[p] = (const char *)peer_regions[p];
     a.g2l = g2l;
     a.sched = slot->sched;
+    a.epoch = epoch;
+    if (epoch > 0) ck(tms::launch_route_arrive(a, st), "route arrive");
     {
       ProfScope ps(s, 0, st);
       ck(tms::launch_walk_routed(s->v, a, s->num_sms, st), "walk_routed");
     }
+    if (epoch > 0) ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
     ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
     slot->used = true;
   });
+}
+}  // namespace
+
+int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                    void *stream) {
+  NvtxRange nvtx_("tm_match_routed");
+  return match_routed(s, nranks, rank, peer_regions, g2l, 0, stream);
+}
+
+int tm_match_routed_sync(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                         int64_t epoch, void *stream) {
+  NvtxRange nvtx_("tm_match_routed_sync");
+  if (epoch <= 0) {
+    g_err = "epoch must be positive and increase by one per routed call";
+    return TM_EINVAL;
+  }
+  return match_routed(s, nranks, rank, peer_regions, g2l, epoch, stream);
 }
 
 

@@ -10,14 +10,18 @@ batch of queries in HBM for sessions owned anywhere) use ``Router.match``:
 
 1. ``tm_route_prepare`` buckets the local batch by owner inside this rank's IPC-shared
    region;
-2. a cross-rank barrier (a one-element NCCL all-reduce on the same stream);
-3. ``tm_match_routed``: every owner's K1 kernel reads its queries directly from the
-   requesters' regions over NVLink (P2P loads) and writes matched / parent / dup back
-   into them (P2P stores) — the exchange is fused into the match kernel;
+2. a cross-rank barrier;
+3. every owner's K1 kernel reads its queries directly from the requesters' regions over
+   NVLink (P2P loads) and writes matched / parent / dup back into them (P2P stores) —
+   the exchange is fused into the match kernel;
 4. a second barrier publishes the results to the requesters.
 
-PyTorch provides the process group (plumbing); the routing and matching run in the
-CUDA kernels behind include/tmstore.h.
+By default (``sync="device"``, ``tm_match_routed_sync``) both barriers are epoch flags
+in the region headers written and polled by the kernels themselves over NVLink — no
+collective library call per batch.  ``sync="nccl"`` (``tm_match_routed``) brackets the
+kernel with one-element NCCL all-reduces instead.  PyTorch provides the process group
+(setup plumbing: the IPC handle exchange); routing and matching run in the CUDA kernels
+behind include/tmstore.h.
 """
 
 from __future__ import annotations
@@ -114,6 +118,7 @@ class Router:
         self.out_dup = view(7, n_max, "<i8", None)
         self.g2l = torch.as_tensor(np.asarray(g2l, np.int32), device=dev)
         self._bar = torch.zeros(1, device=dev)
+        self._epoch = 0  # device-side barrier epochs (same sequence on every rank)
         dist.barrier(group=group)
 
     def _barrier(self):
@@ -121,10 +126,11 @@ class Router:
 
         dist.all_reduce(self._bar, group=self.group)  # stream-ordered cross-rank barrier
 
-    def match(self, n: int):
+    def match(self, n: int, sync: str = "device"):
         """Match the n queries staged in this rank's region (gsid / qoff / qlen / tokens)
         against their owners' shards; results land in out_matched / out_parent / out_dup.
-        Enqueued on torch's current stream (the barriers' stream)."""
+        Enqueued on torch's current stream.  Collective: every rank calls it once per
+        batch, in the same order and with the same ``sync``."""
         import torch
 
         if n > self.n_max:
@@ -132,10 +138,17 @@ class Router:
         st = torch.cuda.current_stream(self.store.device).cuda_stream
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
+        g2l = C.c_void_p(self.g2l.data_ptr())
         check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, st))
+        if sync == "device" and self.nranks > 1:
+            self._epoch += 1
+            check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self._epoch, st))
+            return
+        if sync not in ("nccl", "device"):
+            raise ValueError(f"unknown sync mode {sync!r}")
         if self.nranks > 1:
             self._barrier()
-        check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, C.c_void_p(self.g2l.data_ptr()), st))
+        check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, g2l, st))
         if self.nranks > 1:
             self._barrier()
 

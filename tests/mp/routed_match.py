@@ -27,12 +27,18 @@ dist.all_reduce(need, op=dist.ReduceOp.MAX)
 router = Router(store, dist.group.WORLD, n_max=wl.n_queries, tokens_max=int(need.item()), g2l=wl.g2l)
 wl.fill_queries(router)
 for _ in range(3):
-    router.match(wl.n_queries)
+    router.match(wl.n_queries)  # device-side barriers (default)
 torch.cuda.synchronize()
+store.synchronize()  # raises if a peer timed out
 m = router.out_matched[: wl.n_queries].cpu().numpy()
 par = router.out_parent[: wl.n_queries].cpu().numpy()
 ok = np.array_equal(m, wl.q_depth) and bool(np.all((par >= 0) | (m == 0)))
-# the NCCL-only baseline exchange must agree exactly with the fused path
+# the fused path with NCCL barriers, and the NCCL-only baseline exchange, must agree exactly
+for sync in ("nccl", "device"):
+    router.out_matched.fill_(-7)
+    router.match(wl.n_queries, sync=sync)
+    torch.cuda.synchronize()
+    ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
 router.out_matched.fill_(-7)
 router.match_nccl(wl.n_queries)
 torch.cuda.synchronize()
