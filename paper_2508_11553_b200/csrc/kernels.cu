@@ -725,57 +725,61 @@ __device__ __forceinline__ int first_run_of(const DevView &v, int64_t run0, int 
   return lo;
 }
 
-// Export planner: one thread per tile resolves the dependent lookups (tile -> row,
-// parent chain, first run of each piece) for every tile in parallel, so the copy
-// kernel's CTAs start streaming immediately instead of chasing pointers per tile.
+// Export planner: resolves the dependent lookups of every tile (parent chain, first run
+// of each piece) in parallel, so the copy kernel's CTAs start streaming immediately
+// instead of chasing pointers per tile.  One warp per output row, one lane per tile of
+// the row: the tile -> row mapping needs no search.
+__device__ __forceinline__ void plan_tile(const DevView &v, const ExportArgs &e, int64_t t, int64_t i, int64_t row,
+                                          int64_t len, int64_t o, int64_t a) {
+  const int64_t b = min((int64_t)(a + kExportTile), len);
+  int64_t cur = row, upper = len;
+  // climb to the owner of position b-1 with jump pointers (O(log depth)); its range
+  // ends at or after b, so the tile's first piece ends at b
+  while (v.row_m[cur] > b - 1) {
+    const int64_t jp = v.row_jump[cur];
+    cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
+    upper = b;
+  }
+  int np = 0;
+  ExportPiece *out = e.plan[t].p;
+  while (cur >= 0 && upper > a) {
+    const int64_t mx = v.row_m[cur];
+    const int64_t pa = max(mx, a), pb = min(upper, b);
+    if (pa < pb) {
+      TM_DCHECK(v, cur < v.row_cap && v.row_vb[cur] + pb <= v.arena_cap, kErrArena);
+      if (np == kMaxPieces) { np = -1; break; }
+      ExportPiece p;
+      p.vb = v.row_vb[cur];
+      p.run0 = v.row_run0[cur];
+      p.pa = (int32_t)pa;
+      p.pb = (int32_t)pb;
+      p.nrun = v.row_nrun[cur];
+      p.len = v.row_len[cur];
+      p.first_run = first_run_of(v, p.run0, p.nrun, pa);
+      p.pad = 0;
+      out[np++] = p;
+    }
+    upper = mx;
+    cur = v.row_parent[cur];
+  }
+  TileHdr h;
+  h.o = o;
+  h.a = (int32_t)a;
+  h.b = (int32_t)b;
+  h.row = (int32_t)i;
+  h.np = np;
+  h.pad = 0;
+  e.plan[t].h = h;
+}
+
 __global__ void k_export_plan(DevView v, ExportArgs e) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = e.n;  // largest i with tile_off[i] <= t
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) >> 1;
-      if (e.tile_off[mid] <= t) lo = mid; else hi = mid;
-    }
-    const int64_t row = e.rows[lo];
-    const int64_t a = (t - e.tile_off[lo]) * kExportTile;
-    const int64_t b = min((int64_t)(a + kExportTile), (int64_t)v.row_len[row]);
-    int64_t cur = row, upper = v.row_len[row];
-    // climb to the owner of position b-1 with jump pointers (O(log depth)); its range
-    // ends at or after b, so the tile's first piece ends at b
-    while (v.row_m[cur] > b - 1) {
-      const int64_t jp = v.row_jump[cur];
-      cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
-      upper = b;
-    }
-    int np = 0;
-    ExportPiece *out = e.plan[t].p;
-    while (cur >= 0 && upper > a) {
-      const int64_t mx = v.row_m[cur];
-      const int64_t pa = max(mx, a), pb = min(upper, b);
-      if (pa < pb) {
-        TM_DCHECK(v, cur < v.row_cap && v.row_vb[cur] + pb <= v.arena_cap, kErrArena);
-        if (np == kMaxPieces) { np = -1; break; }
-        ExportPiece p;
-        p.vb = v.row_vb[cur];
-        p.run0 = v.row_run0[cur];
-        p.pa = (int32_t)pa;
-        p.pb = (int32_t)pb;
-        p.nrun = v.row_nrun[cur];
-        p.len = v.row_len[cur];
-        p.first_run = first_run_of(v, p.run0, p.nrun, pa);
-        p.pad = 0;
-        out[np++] = p;
-      }
-      upper = mx;
-      cur = v.row_parent[cur];
-    }
-    TileHdr h;
-    h.o = e.out_off[lo];
-    h.a = (int32_t)a;
-    h.b = (int32_t)b;
-    h.row = (int32_t)lo;
-    h.np = np;
-    h.pad = 0;
-    e.plan[t].h = h;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < e.n; i += nwarps) {
+    const int64_t t0 = e.tile_off[i], t1 = e.tile_off[i + 1];
+    const int64_t row = e.rows[i];
+    const int64_t len = v.row_len[row], o = e.out_off[i];
+    for (int64_t t = t0 + lane; t < t1; t += 32) plan_tile(v, e, t, i, row, len, o, (t - t0) * kExportTile);
   }
 }
 
@@ -1227,7 +1231,7 @@ cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms
   if (h.ntiles < 1) return cudaSuccess;
   ExportArgs e{h.n, h.rows, h.out_off, h.tile_off, h.ntiles, h.tokens, h.mask, h.versions,
                (unsigned long long *)h.resp, reinterpret_cast<TilePlan *>(h.plan)};
-  const int pgrid = (int)std::min<int64_t>((h.ntiles + 255) / 256, (int64_t)num_sms * 8);
+  const int pgrid = (int)std::min<int64_t>((h.n * 32 + 255) / 256, (int64_t)num_sms * 8);  // a warp per row
   k_export_plan<<<pgrid, 256, 0, s>>>(v, e);
   const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * kExportCtas);
   k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
