@@ -67,6 +67,8 @@ struct WalkShared {
   long long nvb;  // next row's virtual base / length (from the hint or one probe)
   int nlen;
   int lo;
+  long long pc_vb;  // session path copy (kPathCopyDepth): virtual base / length, or pc_len 0
+  int pc_len;
 };
 
 constexpr int kTmaStages = 4;
@@ -80,10 +82,48 @@ struct NoRing {};
 template <int NT, int U, class R = NoRing>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
                                            WalkOut o, WalkShared &sh, R *rg = nullptr) {
+  // A session with a path copy (a long turn-by-turn chain): compare the query against the
+  // copy in one streaming segment, then resume the walk at the row that owns the last
+  // matched position - exactly the state the hop-by-hop walk would reach there (every
+  // position of the copy's sequence is owned by the deepest ancestor starting at or
+  // before it).
   if (threadIdx.x == 0) {
+    sh.pc_len = 0;
     int64_t r = -1;
-    if (root_hint) r = *root_hint;
-    else if (L > 0) r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+    if (root_hint) {
+      r = *root_hint;
+    } else if (L > 0) {
+      const int64_t pc = v.s_pc_row[sid];  // in flight with the root probe
+      r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+      if (pc >= 0 && r >= 0) {
+        sh.pc_vb = v.s_pc_vb[sid];
+        sh.pc_len = min(L, v.row_len[pc]);
+        sh.nvb = pc;
+      }
+    }
+    sh.row = r;
+  }
+  __syncthreads();
+  int jpc = 0;
+  if (sh.pc_len > 0) {
+    const int32_t *pcq = v.arena + sh.pc_vb;
+    if constexpr (std::is_same<R, NoRing>::value) {
+      jpc = block_first_mismatch<NT, U>(q, pcq, 0, sh.pc_len, sh.red);
+    } else {
+      jpc = block_first_mismatch_tma(q, pcq, 0, sh.pc_len, sh.red, *rg);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int64_t r = sh.row;  // the root row (or -1)
+    int lo = 1;
+    if (jpc > 0) {  // owner of position jpc-1 on the copy's path: O(log depth) ancestor search
+      r = sh.nvb;
+      while (v.row_m[r] > jpc - 1) {
+        const int64_t jp = v.row_jump[r];
+        r = (jp >= 0 && v.row_m[jp] > jpc - 1) ? jp : v.row_parent[r];
+      }
+      lo = jpc;
+    }
     if (r < 0) {  // nothing shares the first token: matched 0
       *o.m = 0;
       *o.parent = -1;
@@ -91,7 +131,7 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
       if (o.tnext) { *o.tnext = L > 0 ? q[0] : -1; *o.spar = -1; }
     }
     sh.row = r;
-    sh.lo = 1;
+    sh.lo = lo;
   }
   __syncthreads();
   int64_t r = sh.row;
@@ -590,6 +630,44 @@ __device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, i
   }
 }
 
+// Session path copy upkeep after entry e committed a new row at depth >= kPathCopyDepth:
+// the row becomes its session's path copy.  A turn that extends the current copy's row
+// exactly at its end appends only its new tokens (amortised O(1) per token: copies are
+// allocated with 2x headroom); anything else copies its whole sequence into a fresh
+// buffer.  The source is the entry's own query (its full sequence, already in HBM).
+template <int NT>
+__device__ __forceinline__ void update_path_copy(const DevView &v, const Batch &b, int64_t e, WalkShared &sh) {
+  const int64_t row = b.c_row[e];
+  if (threadIdx.x == 0) {
+    sh.pc_len = 0;
+    const int64_t L = b.len[e], m = b.o_m[e];
+    if (b.o_dup[e] < 0 && v.row_depth[row] >= kPathCopyDepth) {
+      const int32_t sid = b.sids[e];
+      const int64_t pc = v.s_pc_row[sid], par = b.o_parent[e];
+      int64_t vb = v.s_pc_vb[sid], cap = v.s_pc_cap[sid], from = m;
+      if (!(pc >= 0 && par == pc && m == v.row_len[pc] && L <= cap)) {
+        cap = (2 * L + kAlignWords - 1) / kAlignWords * kAlignWords;
+        vb = (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)cap);
+        from = 0;
+      }
+      TM_DCHECK(v, vb >= 0 && vb + cap <= v.arena_cap, kErrArena);
+      v.s_pc_row[sid] = row;
+      v.s_pc_vb[sid] = vb;
+      v.s_pc_cap[sid] = cap;
+      sh.pc_vb = vb;
+      sh.pc_len = (int)L;
+      sh.lo = (int)from;
+    }
+  }
+  __syncthreads();
+  if (sh.pc_len == 0) return;
+  // int4 copy of positions [from, L) (the copy is congruent with the query mod 4 words;
+  // edge words land in the copy's own padding)
+  const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[e]);
+  int4 *dst = reinterpret_cast<int4 *>(v.arena + sh.pc_vb);
+  for (int64_t i = (sh.lo >> 2) + threadIdx.x; i < ((sh.pc_len + 3) >> 2); i += NT) dst[i] = ldg_stream(src + i);
+}
+
 template <int NT, int U, bool TMA = false, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) k_record(DevView v, RecordArgs a) {
   const Batch &b = a.b;
@@ -629,6 +707,8 @@ __global__ void __launch_bounds__(NT, MINB) k_record(DevView v, RecordArgs a) {
       }
       __syncthreads();
       commit_entry<NT>(v, b, e);
+      __syncthreads();
+      update_path_copy<NT>(v, b, e, sh);
       __syncthreads();  // the next entry of the chain sees this one (same CTA)
     }
   }

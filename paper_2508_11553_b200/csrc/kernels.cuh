@@ -8,6 +8,7 @@
 namespace tms {
 
 constexpr int kAlignWords = 32;  // 128-byte lines: sequence positions are stored congruent mod 32
+constexpr int kPathCopyDepth = 4;  // rows at this chain depth or deeper get a session path copy
 constexpr uint64_t kEmpty = ~0ull;
 constexpr uint64_t kRootTag = 1ull << 62;
 
@@ -43,6 +44,13 @@ struct DevView {
   int32_t *s_nrows;
   int64_t *s_stored;
   int64_t *s_naive;
+  // session path copy (long turn-by-turn chains): the newest row at depth >= kPathCopyDepth
+  // keeps its FULL sequence contiguous in the arena, so a walk compares the shared history
+  // in one streaming segment and resumes in the row tree with an O(log depth) ancestor
+  // search instead of one hop per turn
+  int64_t *s_pc_row;  // -1: none
+  int64_t *s_pc_vb;   // position p of the copy at arena[s_pc_vb + p] (multiple of 32)
+  int64_t *s_pc_cap;  // positions the copy can hold before it is reallocated
   // allocation counters (device-resident, advanced by the commit planner)
   int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=first device error code
   // capacities (device-side bounds checks)

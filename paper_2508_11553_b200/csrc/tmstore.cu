@@ -140,6 +140,7 @@ struct tm_store {
   std::vector<RowHost> rows;
   std::vector<std::vector<int64_t>> sess_rows;
   std::vector<int64_t> sess_stored, sess_naive;
+  std::vector<int32_t> sess_maxdepth;  // deepest row per session (-1: none); sizes path-copy reservations
   int64_t max_depth = 0;
   DevBytes scratch, dtok;
   PinBytes pin, ptok, d2h_slot[2];
@@ -243,6 +244,12 @@ void ensure_sessions(tm_store *s, int64_t need) {
   ck(cudaMemsetAsync(s->v.s_nrows + n, 0, sizeof(int32_t) * (nc - n), s->stream), "memset");
   ck(cudaMemsetAsync(s->v.s_stored + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
   ck(cudaMemsetAsync(s->v.s_naive + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
+  dev_grow(s->v.s_pc_row, n, nc, s->stream);
+  dev_grow(s->v.s_pc_vb, n, nc, s->stream);
+  dev_grow(s->v.s_pc_cap, n, nc, s->stream);
+  ck(tms::launch_fill_u64((uint64_t *)(s->v.s_pc_row + n), nc - n, ~0ull, s->stream), "fill");  // -1: no copy
+  ck(cudaMemsetAsync(s->v.s_pc_vb + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
+  ck(cudaMemsetAsync(s->v.s_pc_cap + n, 0, sizeof(int64_t) * (nc - n), s->stream), "memset");
   s->sess_cap = nc;
 }
 
@@ -606,7 +613,7 @@ void lex_emit(const tm_store *s, const std::vector<std::vector<int64_t>> &kids, 
 
 // ---- snapshot / restore -----------------------------------------------------------------
 namespace {
-constexpr char kMagic[8] = {'T', 'M', 'S', 'T', 'O', 'R', 'E', '2'};
+constexpr char kMagic[8] = {'T', 'M', 'S', 'T', 'O', 'R', 'E', '3'};
 
 struct FileW {
   FILE *f;
@@ -718,7 +725,7 @@ int tm_store_destroy(tm_store *s) {
                   s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.row_ext,
                   s->v.row_ext_tok, s->v.row_ext_len, s->v.row_ext_vb, s->v.row_jump, s->v.run_start,
                   s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
-                  s->v.s_stored, s->v.s_naive, s->v.ctr, s->sched};
+                  s->v.s_stored, s->v.s_naive, s->v.s_pc_row, s->v.s_pc_vb, s->v.s_pc_cap, s->v.ctr, s->sched};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (auto &sl : s->slots) {
@@ -746,6 +753,7 @@ int tm_session_create(tm_store *s, int32_t *out_sid) {
     s->sess_rows.emplace_back();
     s->sess_stored.push_back(0);
     s->sess_naive.push_back(0);
+    s->sess_maxdepth.push_back(-1);
     *out_sid = (int32_t)s->n_sess++;
   });
 }
@@ -804,6 +812,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       chain_len[c]++;
       total_runs += r1 - r0;
       words_upper += round_up(L, tms::kAlignWords) + tms::kAlignWords;
+      // the entry's row may reach path-copy depth: room for a fresh copy with 2x headroom
+      if (s->sess_maxdepth[sid] + chain_len[c] >= tms::kPathCopyDepth) words_upper += round_up(2 * L, tms::kAlignWords);
     }
     const int64_t nchains = (int64_t)chain_tokens.size();
     std::vector<int64_t> chain_beg(nchains + 1, 0);
@@ -927,6 +937,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
         rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
         s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
+        s->sess_maxdepth[sid] = std::max(s->sess_maxdepth[sid], rh.depth);
         s->rows[row] = rh;
         if (r_loc[k] != (int32_t)s->sess_rows[sid].size()) fail(TM_ECUDA, "session ordinal out of sync");
         s->sess_rows[sid].push_back(row);
@@ -1485,6 +1496,9 @@ int tm_store_save(tm_store *s, const char *path) {
       save_dev(s, w, s->v.run_origin, s->n_runs);
       save_dev(s, w, s->v.s_nrows, s->n_sess); save_dev(s, w, s->v.s_stored, s->n_sess);
       save_dev(s, w, s->v.s_naive, s->n_sess);
+      save_dev(s, w, s->v.s_pc_row, s->n_sess);
+      save_dev(s, w, s->v.s_pc_vb, s->n_sess);
+      save_dev(s, w, s->v.s_pc_cap, s->n_sess);
       w.put(kMagic, 8);
     } catch (...) {
       fclose(f);
@@ -1517,6 +1531,9 @@ int tm_store_load(tm_store *s, const char *path) {
       s->sess_rows.assign(nsess, {});
       s->sess_stored.assign(nsess, 0);
       s->sess_naive.assign(nsess, 0);
+      s->sess_maxdepth.assign(nsess, -1);
+      for (const RowHost &rh : s->rows)
+        if (rh.sid >= 0) s->sess_maxdepth[rh.sid] = std::max(s->sess_maxdepth[rh.sid], rh.depth);
       for (int64_t i = 0; i < nsess; i++) {
         s->sess_stored[i] = r.val<int64_t>();
         s->sess_naive[i] = r.val<int64_t>();
@@ -1536,6 +1553,9 @@ int tm_store_load(tm_store *s, const char *path) {
       load_dev(s, r, s->v.run_origin, nruns);
       load_dev(s, r, s->v.s_nrows, nsess); load_dev(s, r, s->v.s_stored, nsess);
       load_dev(s, r, s->v.s_naive, nsess);
+      load_dev(s, r, s->v.s_pc_row, nsess);
+      load_dev(s, r, s->v.s_pc_vb, nsess);
+      load_dev(s, r, s->v.s_pc_cap, nsess);
       r.get(m, 8);
       if (memcmp(m, kMagic, 8)) fail(TM_EINVAL, "snapshot trailer missing");
       s->n_sess = nsess;

@@ -209,6 +209,77 @@ def test_export_deep_chains_and_straddled_tiles(store):
             assert p.resp_start[j] == (zeros[-1] + 1 if len(zeros) else 0)
 
 
+def test_long_turn_chains_with_session_path_copies(store):
+    """Turn-by-turn sessions deep enough for session path copies (kPathCopyDepth): pure
+    extensions (the copy grows in place and is reallocated), branches off every depth
+    (the copy moves), re-recorded turns, prefix and diverging queries - all against the
+    C oracle, in one batch and across calls, with read-only matches and exports."""
+    rng = np.random.default_rng(77)
+    n_sess, turns = 6, 90
+    sids, seqs = [], []
+    cur = {s: [] for s in range(n_sess)}
+    hist = {s: [] for s in range(n_sess)}
+    for t in range(turns):
+        for s in range(n_sess):
+            r = rng.random()
+            if r < 0.12 and len(hist[s]) > 3:      # branch off an older turn
+                base = hist[s][int(rng.integers(len(hist[s])))]
+                cut = int(rng.integers(1, len(base)))
+                seq = base[:cut] + rng.integers(0, 50, int(rng.integers(1, 40))).tolist()
+            elif r < 0.18 and hist[s]:             # re-record an earlier turn
+                seq = list(hist[s][int(rng.integers(len(hist[s])))])
+            else:                                   # extend the newest turn
+                seq = cur[s] + rng.integers(0, 50, int(rng.integers(1, 70))).tolist()
+            cur[s] = seq
+            hist[s].append(seq)
+            sids.append(s)
+            seqs.append(seq)
+    origins = [(rng.random(len(q)) < 0.5).astype(int).tolist() for q in seqs]
+    versions = [np.sort(rng.integers(0, 3, len(q))).tolist() for q in seqs]
+    ora = CRadixStore()
+    om, orow, opar, oadd = ora.insert_batch(*pack_records(sids, seqs, origins, versions))
+    gsid = [store.new_session() for _ in range(n_sess)]
+    g_sids = np.array([gsid[s] for s in sids], np.int32)
+    cuts = [0, 1, 37, 200, len(seqs)]  # a 1-entry call, then batches of many chained turns
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sub = pack_records(g_sids[a:b], seqs[a:b], origins[a:b], versions[a:b])
+        r = store.record_packed(sub[0], sub[1], sub[2][:-1], np.diff(sub[2]), *sub[3:])
+        assert np.array_equal(r.matched, om[a:b]) and np.array_equal(r.local, orow[a:b])
+        assert np.array_equal(r.parent_local, opar[a:b]) and np.array_equal(r.added, oadd[a:b])
+    for s in range(n_sess):
+        assert store.session_stats(gsid[s]) == ora.stats(s)
+        rows = store.session_rows(gsid[s], "insert")
+        p = store.export(rows)
+        for k in range(len(rows)):
+            t, m, v = ora.export_row(s, k)
+            a, b = p.offsets[k], p.offsets[k + 1]
+            assert np.array_equal(p.tokens[a:b], t) and np.array_equal(p.loss_mask[a:b], m)
+            assert np.array_equal(p.versions[a:b], v)
+    # read-only queries: prefixes of deep turns, extensions, divergence at every depth
+    qs, qsid = [], []
+    for _ in range(400):
+        s = int(rng.integers(n_sess))
+        base = hist[s][int(rng.integers(len(hist[s])))]
+        kind = rng.random()
+        if kind < 0.3:
+            q = base[: int(rng.integers(1, len(base) + 1))]
+        elif kind < 0.6:
+            q = base + rng.integers(0, 50, int(rng.integers(1, 30))).tolist()
+        else:
+            cut = int(rng.integers(0, len(base)))
+            q = base[:cut] + [int(base[cut]) + 1] + rng.integers(0, 50, 5).tolist()
+        qs.append(q)
+        qsid.append(s)
+    zeros = [[0] * len(q) for q in qs]
+    qp = pack_records(qsid, qs, zeros, zeros)
+    m_o, p_o, d_o = ora.match_batch(qp[0], qp[1], qp[2])
+    qg = pack_records([gsid[s] for s in qsid], qs, zeros, zeros)
+    m_g, p_g, d_g = store.match(qg[0], qg[1], qg[2][:-1], np.diff(qg[2]))
+    assert np.array_equal(m_g, m_o)
+    assert [store.row_info(int(x))["local"] if x >= 0 else -1 for x in p_g] == p_o.tolist()
+    assert [store.row_info(int(x))["local"] if x >= 0 else -1 for x in d_g] == d_o.tolist()
+
+
 def test_device_match_path_and_alignment(store):
     """TM_MEM_DEVICE match on torch tensors equals the host-path result."""
     import torch
