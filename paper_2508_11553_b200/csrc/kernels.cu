@@ -946,6 +946,11 @@ __global__ void __launch_bounds__(kExportNT, kExportCtas) k_export(DevView v, Ex
       const int64_t row = e.rows[h.row];
       const int64_t a = h.a, b = h.b;
       int64_t cur = row, upper = v.row_len[row];
+      while (v.row_m[cur] > b - 1) {  // skip the rows above the tile (jump pointers, as the planner)
+        const int64_t jp = v.row_jump[cur];
+        cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
+        upper = b;
+      }
       while (cur >= 0 && upper > a) {
         const int64_t mx = v.row_m[cur];
         const int64_t pa = max(mx, a), pb = min(upper, b);

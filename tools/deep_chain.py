@@ -30,8 +30,11 @@ def main(turns=2000, per=32):
             p = trie.path_trajectory(r.node_id)
             de = time.perf_counter() - t0
             assert p.tokens == seq
+            t0 = time.perf_counter()
+            trie.store.export([trie.row_of(r.node_id)], total=len(seq))  # the C-ABI part alone
+            dx = time.perf_counter() - t0
             print(f"turn {t:5d} ({len(seq):6d} tokens, chain depth {t - 1:5d}): lpm_insert {dt * 1e3:7.2f} ms  "
-                  f"path_trajectory {de * 1e3:7.2f} ms", flush=True)
+                  f"path_trajectory {de * 1e3:7.2f} ms (export call {dx * 1e3:6.2f} ms)", flush=True)
 
 
 if __name__ == "__main__":
