@@ -759,41 +759,43 @@ struct ExportArgs {
 // Copy / fill helpers for one piece [pa, pb) of an output row starting at word o.  When
 // o is a multiple of 4 every output position is 16-byte congruent with its arena
 // position (arena rows are 128-byte aligned), so the body moves int4 / uchar4 vectors.
+template <int NT = kExportNT>
 __device__ __forceinline__ void copy_tokens(int32_t *__restrict__ out, const int32_t *__restrict__ src, int64_t o,
                                             int64_t pa, int64_t pb) {
   if ((o & 3) == 0) {
     const int64_t va = (pa + 3) >> 2, vb = pb >> 2;  // int4 body [4va, 4vb)
     if (va < vb) {
-      for (int64_t p = pa + threadIdx.x; p < 4 * va; p += kExportNT) out[o + p] = src[p];
-      for (int64_t p = 4 * vb + threadIdx.x; p < pb; p += kExportNT) out[o + p] = src[p];
+      for (int64_t p = pa + threadIdx.x; p < 4 * va; p += NT) out[o + p] = src[p];
+      for (int64_t p = 4 * vb + threadIdx.x; p < pb; p += NT) out[o + p] = src[p];
       const int4 *s4 = reinterpret_cast<const int4 *>(src);
       int4 *d4 = reinterpret_cast<int4 *>(out + o);
-      for (int64_t q = va + threadIdx.x; q < vb; q += kExportNT) d4[q] = ldg_stream(s4 + q);
+      for (int64_t q = va + threadIdx.x; q < vb; q += NT) d4[q] = ldg_stream(s4 + q);
       return;
     }
   }
-  for (int64_t p = pa + threadIdx.x; p < pb; p += kExportNT) out[o + p] = src[p];
+  for (int64_t p = pa + threadIdx.x; p < pb; p += NT) out[o + p] = src[p];
 }
 
+template <int NT = kExportNT>
 __device__ __forceinline__ void fill_meta(uint8_t *__restrict__ mask, int32_t *__restrict__ vers, int64_t o,
                                           int64_t xa, int64_t xb, uint8_t org, int32_t ver) {
   if ((o & 3) == 0) {
     const int64_t va = (xa + 3) >> 2, vb = xb >> 2;
     if (va < vb) {
-      for (int64_t p = xa + threadIdx.x; p < 4 * va; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
-      for (int64_t p = 4 * vb + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
+      for (int64_t p = xa + threadIdx.x; p < 4 * va; p += NT) { mask[o + p] = org; vers[o + p] = ver; }
+      for (int64_t p = 4 * vb + threadIdx.x; p < xb; p += NT) { mask[o + p] = org; vers[o + p] = ver; }
       const uint32_t m4 = 0x01010101u * org;
       const int4 v4 = make_int4(ver, ver, ver, ver);
       uint32_t *dm = reinterpret_cast<uint32_t *>(mask + o);
       int4 *dv = reinterpret_cast<int4 *>(vers + o);
-      for (int64_t q = va + threadIdx.x; q < vb; q += kExportNT) {
+      for (int64_t q = va + threadIdx.x; q < vb; q += NT) {
         dm[q] = m4;
         dv[q] = v4;
       }
       return;
     }
   }
-  for (int64_t p = xa + threadIdx.x; p < xb; p += kExportNT) { mask[o + p] = org; vers[o + p] = ver; }
+  for (int64_t p = xa + threadIdx.x; p < xb; p += NT) { mask[o + p] = org; vers[o + p] = ver; }
 }
 
 __device__ __forceinline__ int first_run_of(const DevView &v, int64_t run0, int nrun, int64_t pa) {
@@ -863,6 +865,7 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
   }
 }
 
+template <int NT = kExportNT>
 __device__ __forceinline__ void export_runs(const DevView &v, const ExportArgs &e, const ExportPiece &p, int64_t o,
                                             long long &respmax) {
   for (int k = p.first_run; k < p.nrun; k++) {
@@ -871,7 +874,7 @@ __device__ __forceinline__ void export_runs(const DevView &v, const ExportArgs &
     const int64_t re = (k + 1 < p.nrun) ? v.run_start[p.run0 + k + 1] : p.len;
     const int64_t xa = max(rs, (int64_t)p.pa), xb = min(re, (int64_t)p.pb);
     const uint8_t org = v.run_origin[p.run0 + k];
-    fill_meta(e.mask, e.versions, o, xa, xb, org, v.run_version[p.run0 + k]);
+    fill_meta<NT>(e.mask, e.versions, o, xa, xb, org, v.run_version[p.run0 + k]);
     if (org == 0 && xb > respmax) respmax = xb;
   }
 }
@@ -881,6 +884,47 @@ __device__ __forceinline__ int piece_at(const ExportPiece *sp, int np, int32_t p
   int k = 0;
   while (k + 1 < np && sp[k].pa > p) k++;
   return k;
+}
+
+// Tiles the vector paths do not take: an output row that starts off a 16-byte boundary
+// (scalar copies), or a chain deeper than kMaxPieces inside the tile (walked here).
+template <int NT>
+__device__ __forceinline__ void export_tile_generic(const DevView &v, const ExportArgs &e, const TileHdr &h, const ExportPiece *P,
+                                    long long &respmax) {
+  const int64_t o = h.o;
+  if (h.np > 0) {  // unaligned row start
+    for (int k = 0; k < h.np; k++) {
+      copy_tokens<NT>(e.tokens, v.arena + P[k].vb, o, P[k].pa, P[k].pb);
+      export_runs<NT>(v, e, P[k], o, respmax);
+    }
+  } else if (h.np < 0) {  // chain deeper than kMaxPieces inside this tile: walk it here
+    const int64_t row = e.rows[h.row];
+    const int64_t a = h.a, b = h.b;
+    int64_t cur = row, upper = v.row_len[row];
+    while (v.row_m[cur] > b - 1) {  // skip the rows above the tile (jump pointers, as the planner)
+      const int64_t jp = v.row_jump[cur];
+      cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
+      upper = b;
+    }
+    while (cur >= 0 && upper > a) {
+      const int64_t mx = v.row_m[cur];
+      const int64_t pa = max(mx, a), pb = min(upper, b);
+      if (pa < pb) {
+        ExportPiece p;
+        p.vb = v.row_vb[cur];
+        p.run0 = v.row_run0[cur];
+        p.pa = (int32_t)pa;
+        p.pb = (int32_t)pb;
+        p.nrun = v.row_nrun[cur];
+        p.len = v.row_len[cur];
+        p.first_run = first_run_of(v, p.run0, p.nrun, pa);
+        copy_tokens<NT>(e.tokens, v.arena + p.vb, o, p.pa, p.pb);
+        export_runs<NT>(v, e, p, o, respmax);
+      }
+      upper = mx;
+      cur = v.row_parent[cur];
+    }
+  }
 }
 
 constexpr int kExportSlots = kExportTile / 4 / kExportNT;  // int4 output slots per thread per tile
@@ -937,43 +981,96 @@ __global__ void __launch_bounds__(kExportNT, kExportCtas) k_export(DevView v, Ex
           for (int u = 0; u < 4 && p + u < h.b; u++)
             e.tokens[o + p + u] = v.arena[P[piece_at(P, h.np, p + u)].vb + p + u];
       }
-    } else if (h.np > 0) {  // unaligned row start
-      for (int k = 0; k < h.np; k++) {
-        copy_tokens(e.tokens, v.arena + P[k].vb, o, P[k].pa, P[k].pb);
-        export_runs(v, e, P[k], o, respmax);
-      }
-    } else if (h.np < 0) {  // chain deeper than kMaxPieces inside this tile: walk it here
-      const int64_t row = e.rows[h.row];
-      const int64_t a = h.a, b = h.b;
-      int64_t cur = row, upper = v.row_len[row];
-      while (v.row_m[cur] > b - 1) {  // skip the rows above the tile (jump pointers, as the planner)
-        const int64_t jp = v.row_jump[cur];
-        cur = (jp >= 0 && v.row_m[jp] > b - 1) ? jp : v.row_parent[cur];
-        upper = b;
-      }
-      while (cur >= 0 && upper > a) {
-        const int64_t mx = v.row_m[cur];
-        const int64_t pa = max(mx, a), pb = min(upper, b);
-        if (pa < pb) {
-          ExportPiece p;
-          p.vb = v.row_vb[cur];
-          p.run0 = v.row_run0[cur];
-          p.pa = (int32_t)pa;
-          p.pb = (int32_t)pb;
-          p.nrun = v.row_nrun[cur];
-          p.len = v.row_len[cur];
-          p.first_run = first_run_of(v, p.run0, p.nrun, pa);
-          copy_tokens(e.tokens, v.arena + p.vb, o, p.pa, p.pb);
-          export_runs(v, e, p, o, respmax);
-        }
-        upper = mx;
-        cur = v.row_parent[cur];
-      }
+    } else {
+      export_tile_generic<kExportNT>(v, e, h, P, respmax);
     }
     if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[h.row], (unsigned long long)respmax);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();  // next plan visible; this tile's plan no longer read
   }
+}
+
+// K3, TMA variant: token bodies never pass through registers.  Per tile one elected thread
+// issues cp.async.bulk loads of every piece's 16-byte-aligned body from the arena into a
+// 16 KB shared-memory tile (an mbarrier counts the bytes), the other threads put the <= 6
+// edge words per piece into the tile and write the mask / version runs, then the tile
+// leaves with ONE cp.async.bulk store (global <- shared).  Two tile buffers: a tile's
+// store drains while the next tile loads.  Aligned rows only; the rest take
+// export_tile_generic.
+constexpr int kExportTmaNT = 128;
+struct ExportTmaSmem {
+  int4 buf[2][kExportTile / 4];
+  TilePlan plan[2];
+  uint64_t bar[2];
+};
+
+__global__ void __launch_bounds__(kExportTmaNT) k_export_tma(DevView v, ExportArgs e) {
+  extern __shared__ __align__(128) char dyn[];
+  ExportTmaSmem &sm = *reinterpret_cast<ExportTmaSmem *>(dyn);
+  int64_t t = blockIdx.x;
+  if (t >= e.ntiles) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fetch_plan(&sm.plan[0], &e.plan[t]);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  uint32_t phase = 0;  // bit s: parity of stage s's barrier
+  for (int it = 0; t < e.ntiles; t += gridDim.x, it ^= 1) {
+    const TileHdr h = sm.plan[it].h;
+    const ExportPiece *P = sm.plan[it].p;
+    if (t + gridDim.x < e.ntiles) fetch_plan(&sm.plan[it ^ 1], &e.plan[t + gridDim.x]);
+    const int64_t o = h.o;
+    long long respmax = 0;
+    if (h.np > 0 && (o & 3) == 0) {
+      int32_t *B = reinterpret_cast<int32_t *>(sm.buf[it]);
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // store of tile t-2 read B
+      __syncthreads();
+      uint32_t bytes = 0;
+      for (int k = 0; k < h.np; k++) {
+        const int32_t ca = (P[k].pa + 3) & ~3, cb = P[k].pb & ~3;
+        if (ca < cb) bytes += 4u * (uint32_t)(cb - ca);
+      }
+      if (threadIdx.x == 0 && bytes) {
+        mbar_expect_tx(&sm.bar[it], bytes);
+        for (int k = 0; k < h.np; k++) {
+          const int32_t ca = (P[k].pa + 3) & ~3, cb = P[k].pb & ~3;
+          if (ca < cb) bulk_g2s(B + (ca - h.a), v.arena + P[k].vb + ca, 4u * (uint32_t)(cb - ca), &sm.bar[it]);
+        }
+      }
+      // edge words: thread 8k+w takes word w of piece k's head [pa, ca) / tail [cb, pb)
+      if ((int)threadIdx.x < 8 * h.np) {
+        const ExportPiece &q = P[threadIdx.x >> 3];
+        const int w = threadIdx.x & 7;
+        const int32_t ca = (q.pa + 3) & ~3, cb = q.pb & ~3;
+        int32_t pos = -1;
+        if (ca < cb) pos = w < 3 ? (q.pa + w < ca ? q.pa + w : -1) : (w < 6 && cb + (w - 3) < q.pb ? cb + (w - 3) : -1);
+        else if (w < 7 && q.pa + w < q.pb) pos = q.pa + w;
+        if (pos >= 0) B[pos - h.a] = v.arena[q.vb + pos];
+      }
+      for (int k = 0; k < h.np; k++) export_runs<kExportTmaNT>(v, e, P[k], o, respmax);  // stores only
+      if (bytes) mbar_wait(&sm.bar[it], (phase >> it) & 1);
+      if (bytes) phase ^= 1u << it;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // edge words -> visible to the bulk store
+      __syncthreads();
+      const int32_t body = (h.b & ~3) - h.a;  // whole int4s of the tile
+      if (threadIdx.x == 0 && body > 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(e.tokens + o + h.a),
+                     "r"(smem_u32(B)), "r"(4u * (uint32_t)body)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if ((int)threadIdx.x < h.b - (h.b & ~3)) e.tokens[o + (h.b & ~3) + threadIdx.x] = B[body + threadIdx.x];
+    } else {
+      export_tile_generic<kExportTmaNT>(v, e, h, P, respmax);
+    }
+    if (e.resp && threadIdx.x == 0 && respmax > 0) atomicMax(&e.resp[h.row], (unsigned long long)respmax);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // next plan visible; this tile's plan no longer read
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done before smem goes away
 }
 
 // ----------------------------------------------------------------------------------
@@ -1318,6 +1415,24 @@ cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms
                (unsigned long long *)h.resp, reinterpret_cast<TilePlan *>(h.plan)};
   const int pgrid = (int)std::min<int64_t>((h.n * 32 + 255) / 256, (int64_t)num_sms * 8);  // a warp per row
   k_export_plan<<<pgrid, 256, 0, s>>>(v, e);
+  // TM_EXPORT_VARIANT (tuning): "tma" (default: c2 0.271 ms = 6.3 TB/s, c3 0.073 ms) or
+  // "regs" (register path: 0.295-0.310 / 0.089-0.093 ms)
+  static int variant = -1;
+  static int tma_ctas = 0;
+  if (variant < 0) {
+    const char *ev = getenv("TM_EXPORT_VARIANT");
+    variant = (ev && !strcmp(ev, "regs")) ? 0 : 1;
+    if (variant == 1) {
+      cudaFuncSetAttribute(k_export_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ExportTmaSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tma_ctas, k_export_tma, kExportTmaNT, sizeof(ExportTmaSmem));
+      if (tma_ctas < 1) tma_ctas = 1;
+    }
+  }
+  if (variant == 1) {
+    const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * tma_ctas);
+    k_export_tma<<<(int)grid, kExportTmaNT, sizeof(ExportTmaSmem), s>>>(v, e);
+    return cudaGetLastError();
+  }
   const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * kExportCtas);
   k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
   return cudaGetLastError();
