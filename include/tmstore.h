@@ -197,7 +197,7 @@ int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *
  * (acquire), its last CTA writes `done` into every requester's header, and a wait
  * kernel on this rank's stream holds later work until every owner is done.  `epoch`:
  * the same value on every rank, one larger per routed call (1, 2, ...).  A peer that
- * never signals becomes a device error after 20 s (tm_synchronize reports it). */
+ * never signals becomes a device error after 20 s (TM_PEER_TIMEOUT_MS; tm_synchronize reports it). */
 int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
                          const int32_t *g2l, int64_t epoch, void *stream);
 

@@ -373,15 +373,13 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-constexpr uint64_t kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;  // a dead peer becomes an error, not a hang
-
 // Spin until flags[0..nranks) >= epoch in this rank's own header.  false on timeout
 // (the error word is set; callers stop waiting so the stream drains).
-__device__ bool wait_flags(const DevView &v, const int64_t *flags, int nranks, int64_t epoch) {
+__device__ bool wait_flags(const DevView &v, const int64_t *flags, int nranks, int64_t epoch, uint64_t timeout_ns) {
   const uint64_t t0 = globaltimer_ns();
   for (int p = 0; p < nranks; p++) {
     while (ld_acquire_sys(flags + p) < epoch) {
-      if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
         dev_error(v, kErrPeerTimeout);
         return false;
       }
@@ -406,7 +404,7 @@ __global__ void k_route_arrive(RoutedArgs a) {
 __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
   if (threadIdx.x == 0) {
     const RouteDesc *d = reinterpret_cast<const RouteDesc *>(a.peer[a.rank]);
-    wait_flags(v, d->done, a.nranks, a.epoch);
+    wait_flags(v, d->done, a.nranks, a.epoch, a.timeout_ns);
     __threadfence_system();
   }
 }
@@ -440,7 +438,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   int *s_peer = s_bs + ncell;
   if (a.epoch > 0) {  // device-side barrier: every requester has bucketed its batch
     if (threadIdx.x == 0)
-      wait_flags(v, reinterpret_cast<const RouteDesc *>(a.peer[a.rank])->arrive, np, a.epoch);
+      wait_flags(v, reinterpret_cast<const RouteDesc *>(a.peer[a.rank])->arrive, np, a.epoch, a.timeout_ns);
     __syncthreads();
   }
   // cell c: local cells first (bucket order), then remote cells (bucket, peer) order

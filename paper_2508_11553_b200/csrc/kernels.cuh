@@ -125,6 +125,7 @@ struct RoutedArgs {
   const int32_t *g2l;           // global session id -> local session id (-1: not owned)
   Sched *sched;
   int64_t epoch;                // > 0: device-side barriers (wait for arrive, signal done)
+  uint64_t timeout_ns;          // a peer silent this long is a device error, not a hang
 };
 
 // one batch of sequences resident on the device

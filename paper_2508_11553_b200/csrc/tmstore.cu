@@ -1437,6 +1437,11 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
     a.g2l = g2l;
     a.sched = slot->sched;
     a.epoch = epoch;
+    static const uint64_t timeout_ms = [] {  // TM_PEER_TIMEOUT_MS (default 20 s)
+      const char *e = getenv("TM_PEER_TIMEOUT_MS");
+      return e ? (uint64_t)std::max(1ll, atoll(e)) : 20000ull;
+    }();
+    a.timeout_ns = timeout_ms * 1000000ull;
     if (epoch > 0) ck(tms::launch_route_arrive(a, st), "route arrive");
     {
       ProfScope ps(s, 0, st);

@@ -30,3 +30,12 @@ def test_routed_match_world2():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
     _run(2)
+
+
+def test_device_barrier_peer_timeout_is_a_loud_error():
+    """A peer that never arrives at the device-side barrier becomes a device error after
+    TM_PEER_TIMEOUT_MS (here 300 ms) instead of hanging the stream."""
+    env = dict(os.environ, TM_PEER_TIMEOUT_MS="300")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "mp", "peer_timeout.py")], env=env,
+                         capture_output=True, text=True, timeout=120)
+    assert "DEVICE_ERROR" in out.stdout and "peer rank timed out" in out.stdout, out.stdout + out.stderr
