@@ -379,6 +379,7 @@ __device__ bool wait_flags(const DevView &v, const int64_t *flags, int nranks, i
   const uint64_t t0 = globaltimer_ns();
   for (int p = 0; p < nranks; p++) {
     while (ld_acquire_sys(flags + p) < epoch) {
+      if (*(volatile long long *)&v.ctr[3] != 0) return false;  // already failed (e.g. an earlier wait timed out)
       if (globaltimer_ns() - t0 > timeout_ns) {
         dev_error(v, kErrPeerTimeout);
         return false;
