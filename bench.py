@@ -156,6 +156,8 @@ def run_reference(args):
                          "sample": f"full c4 batch ({wl.n_queries} queries) per step, C radix-tree restatement (oracle/radix_oracle.c), {cores} threads"},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.sessions == 10_000 and args.hist == 32_768:
+        line["reference_python_sample"] = python_reference_sample(wl)
     print(json.dumps(line))
 
 
@@ -182,6 +184,39 @@ def cpu_port_bench_reuse(wl, nthreads):
     t0 = time.perf_counter()
     res = st.match_batch(wl.q_sess, _cpu_store["qt"], _cpu_store["qo"], nthreads=nthreads)
     return wl.n_queries, time.perf_counter() - t0, res
+
+
+def python_reference_sample(wl, nq=64):
+    """The reference trie's own algorithm in its own language (oracle/radix.py restates
+    rolloutlab/trie.py in pure Python) on a sample of the batch: one lpm_insert per query
+    into a trie holding that query's session history, one process.  Informational: the
+    reference arm and cpu_baseline use the C restatement, which is far faster."""
+    from oracle.radix import RadixOracle
+
+    def per_token(s):
+        a, b = wl.run_off[s], wl.run_off[s + 1]
+        st = np.r_[wl.run_start[a:b], wl.hist_len[s]]
+        org = np.repeat(wl.run_origin[a:b].astype(np.int64), np.diff(st)).tolist()
+        ver = np.repeat(wl.run_version[a:b].astype(np.int64), np.diff(st)).tolist()
+        return org, ver
+
+    tries, qs = {}, []
+    for i in range(min(nq, wl.n_queries)):
+        s = int(wl.q_sess[i])
+        if s not in tries:
+            org, ver = per_token(s)
+            tries[s] = RadixOracle()
+            tries[s].insert(wl.hist_tokens[wl.hist_off[s]: wl.hist_off[s] + wl.hist_len[s]].tolist(), org, ver)
+        q = wl.q_tokens[wl.q_off[i]: wl.q_off[i] + wl.q_len[i]].tolist()
+        qs.append((s, q, [0] * len(q)))
+    t0 = time.perf_counter()
+    for s, q, z in qs:
+        tries[s].insert(q, z, z)
+    dt = time.perf_counter() - t0
+    return {"value": len(qs) / dt, "unit": "queries/s", "cores": 1, "kind": "port",
+            "sample": f"{len(qs)} c4 queries, one lpm_insert each into its session's trie, pure-Python restatement "
+                      "of the reference trie (oracle/radix.py), one process; sessions are independent, so all "
+                      "cores would give at most cores x this"}
 
 
 def run_c5(args):
@@ -474,6 +509,8 @@ def main():
         line["cpu_baseline"] = {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
                                 "sample": f"full c4 batch ({n} queries), best of 2, C radix-tree restatement "
                                           f"(oracle/radix_oracle.c), {cores} threads"}
+        if args.sessions == 10_000 and not args.mixed:
+            line["reference_python_sample"] = python_reference_sample(wl)
     if rank == 0:
         print(json.dumps(line))
     store.close()
