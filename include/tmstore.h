@@ -167,13 +167,16 @@ int tm_store_stream(tm_store *store, void **out_stream);
 /* ---- Cross-GPU routing on one node (session-hash sharding, config 5) ----------------
  * Every rank publishes its query batch in a shared device region laid out as
  *   [RouteDesc header | int64 gsid[n] | int64 tok_off[n] | int64 len[n] | int32 tokens |
- *    int32 idx[n] | int64 out_matched[n] | int64 out_parent[n] | int64 out_dup[n]]
- * (offsets[8] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup).
- * tm_route_prepare writes the header and buckets the batch by owner rank
- * (owner = splitmix64(gsid) mod nranks).  After a cross-rank barrier (e.g. a tiny NCCL
- * all-reduce on the same stream) every owner calls tm_match_routed, whose kernel reads
- * its queries directly from the requesters' regions over NVLink and writes results
- * back into them (P2P), then a second barrier publishes the results.
+ *    int32 idx[n] | int64 out_matched[n] | int64 out_parent[n] | int64 out_dup[n] |
+ *    uint16 low plane[tokens + 128] | uint8 high plane[(tokens + 128) / 4]]
+ * (offsets[10] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup, lo,
+ * hi; lo = hi = 0: no planes).  tm_route_prepare writes the header, buckets the batch by
+ * owner rank (owner = splitmix64(gsid) mod nranks) and, with peers, packs the tokens into
+ * the 18-bit planes (hostpack.h layout; TM_ROUTE_PACK=0 disables) so remote owners move
+ * 2.25 B per compared position over NVLink instead of 4.  Then either tm_match_routed_sync
+ * (device-side barriers) or a cross-rank barrier + tm_match_routed + a second barrier:
+ * every owner's kernel reads its queries directly from the requesters' regions over
+ * NVLink and writes the results back into them (P2P).
  * Regions come from tm_shared_alloc (whole cudaMalloc allocations, IPC-exportable);
  * peers map them with tm_ipc_handle (64-byte cudaIpcMemHandle) / tm_ipc_open. */
 int tm_route_desc_bytes(int64_t *out_bytes); /* size of the RouteDesc header */

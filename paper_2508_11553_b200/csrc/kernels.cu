@@ -77,11 +77,25 @@ using Ring = TmaRing<64, kTmaStages, kTmaChunk>;
 
 struct NoRing {};
 
+// a remote query's 18-bit planes (routed match): whole-buffer plane bases + the query's start
+struct PackedQuery {
+  const uint16_t *lo;
+  const uint8_t *hi;
+  int64_t off;
+};
+template <class R>
+struct IsPackedRing : std::false_type {};
+template <int S, int CHP>
+struct IsPackedRing<PackedRing<S, CHP>> : std::true_type {};
+constexpr int kPackedChunk = 1024;  // positions per stage of the packed compare
+using RoutedPackedRing = PackedRing<kTmaStages, kPackedChunk>;
+
 // Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).  With a TmaRing
 // the compare goes through the TMA-staged path, otherwise through registers.
 template <int NT, int U, class R = NoRing>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
-                                           WalkOut o, WalkShared &sh, R *rg = nullptr) {
+                                           WalkOut o, WalkShared &sh, R *rg = nullptr,
+                                           const PackedQuery *pk = nullptr) {
   // A session with a path copy (a long turn-by-turn chain): compare the query against the
   // copy in one streaming segment, then resume the walk at the row that owns the last
   // matched position - exactly the state the hop-by-hop walk would reach there (every
@@ -110,7 +124,11 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
     if constexpr (std::is_same<R, NoRing>::value) {
       jpc = block_first_mismatch<NT, U>(q, pcq, 0, sh.pc_len, sh.red);
     } else {
-      jpc = block_first_mismatch_tma(q, pcq, 0, sh.pc_len, sh.red, *rg);
+      if constexpr (IsPackedRing<R>::value) {
+        jpc = block_first_mismatch_packed<NT>(pk->lo, pk->hi, pk->off, pcq, 0, sh.pc_len, sh.red, *rg);
+      } else {
+        jpc = block_first_mismatch_tma(q, pcq, 0, sh.pc_len, sh.red, *rg);
+      }
     }
   }
   if (threadIdx.x == 0) {
@@ -160,7 +178,11 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
     if constexpr (std::is_same<R, NoRing>::value) {
       j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
     } else {
-      j = block_first_mismatch_tma(q, a, lo, hi, sh.red, *rg);
+      if constexpr (IsPackedRing<R>::value) {
+        j = block_first_mismatch_packed<NT>(pk->lo, pk->hi, pk->off, a, lo, hi, sh.red, *rg);
+      } else {
+        j = block_first_mismatch_tma(q, a, lo, hi, sh.red, *rg);
+      }
     }
     if (threadIdx.x == 0) {
       int64_t next = -1;
@@ -410,16 +432,44 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
   }
 }
 
+// Requester side (nranks > 1): pack this rank's query tokens into the region's 18-bit
+// planes (hostpack.h layout) for the owners to pull over NVLink.  One CTA per query, one
+// warp per 32-position group; positions past a query's end pack as 0 (never compared).
+// Any id outside [0, 2^18) sets pk_bad and the owners read the int32 tokens instead.
+constexpr int kPackNT = 256;
+__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
+  RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
+  const int64_t *qoff = reinterpret_cast<const int64_t *>(region + d->qoff_off);
+  const int64_t *qlen = reinterpret_cast<const int64_t *>(region + d->len_off);
+  const int32_t *tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
+  uint16_t *plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
+  uint8_t *phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned bad = 0;
+  for (int64_t i = blockIdx.x; i < d->n; i += gridDim.x) {
+    const int64_t off = qoff[i], len = qlen[i];
+    for (int64_t g = warp; 32 * g < len; g += kPackNT / 32) {
+      const int64_t r = 32 * g + lane, p = off + r;
+      const uint32_t t = r < len ? (uint32_t)tok[p] : 0u;
+      bad |= t >> 18;
+      plo[p] = (uint16_t)t;
+      uint32_t hb = ((t >> 16) & 3u) << (2 * (lane >> 3));
+      hb |= __shfl_xor_sync(0xffffffffu, hb, 8);
+      hb |= __shfl_xor_sync(0xffffffffu, hb, 16);
+      if (lane < 8) phi[(p - lane) / 4 + lane] = (uint8_t)hb;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(&d->pk_bad, 1);
+}
+
 // Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
 // and the other ranks' (query bytes over NVLink).  1/np of the CTAs start on the local
 // queue and the rest on the remote one, each falling back to the other when its queue
 // runs dry, so HBM and the links are busy at the same time instead of in phases.
 // Dynamic shared memory: [TmaRing (only when nranks > 1)][3 x kPlanNB x nranks + 2 ints
 // of routing tables], sized by routed_smem_bytes so a single rank keeps full occupancy.
-using RoutedRing = TmaRing<64, kTmaStages, kTmaChunk>;
-
 __host__ __device__ constexpr size_t routed_smem_bytes(int nranks) {
-  return (nranks > 1 ? (sizeof(RoutedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
+  return (nranks > 1 ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
 }
 
 template <int NT, int U>
@@ -431,10 +481,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   __shared__ int s_nloc;  // cells in the local queue
   const int np = a.nranks;
   const int ncell = kPlanNB * np;
-  // TMA-staged compare for remote queries: bulk copies pull query chunks over NVLink
-  RoutedRing *rg = np > 1 ? reinterpret_cast<RoutedRing *>(dyn) : nullptr;
-  if (np > 1) tma_ring_init(*rg);
-  int *s_pre = reinterpret_cast<int *>(dyn + (np > 1 ? (sizeof(RoutedRing) + 15) / 16 * 16 : 0));  // ncell + 2
+  // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
+  // over NVLink (2.25 B per position instead of 4)
+  RoutedPackedRing *rg = np > 1 ? reinterpret_cast<RoutedPackedRing *>(dyn) : nullptr;
+  if (np > 1) packed_ring_init(*rg);
+  int *s_pre = reinterpret_cast<int *>(dyn + (np > 1 ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0));  // ncell + 2
   int *s_bs = s_pre + ncell + 2;
   int *s_peer = s_bs + ncell;
   if (a.epoch > 0) {  // device-side barrier: every requester has bucketed its batch
@@ -515,8 +566,13 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
       continue;
     }
     const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
-    if (p != a.rank) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg);  // remote query: TMA over NVLink
-    else walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);                  // local: register double buffer
+    if (d->lo_off && !d->pk_bad) {  // packed planes: TMA bulk copies (over NVLink for remote queries)
+      const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
+                           reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
+      walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
+    } else {  // no peers (N=1), or ids that do not fit 18 bits: int32 tokens, register double buffer
+      walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);
+    }
   }
 }
 
@@ -1487,6 +1543,12 @@ cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s
 
 int export_tile_tokens() { return kExportTile; }
 
+cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
+  if (n < 1) return cudaSuccess;
+  k_route_pack<<<(int)std::min<int64_t>(n, 148 * 8), kPackNT, 0, s>>>(region);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_route(char *region, int nranks, cudaStream_t s) {
   k_route<<<1, kRouteNT, 0, s>>>(region, nranks);
   return cudaGetLastError();
@@ -1502,16 +1564,18 @@ cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaSt
   return cudaGetLastError();
 }
 
+// U = 4 for the register path (no peers / ids beyond 18 bits): with the packed TMA compare
+// inlined as well, U = 8 spills
+constexpr int kRoutedU = 4;
 cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   static int occ[kMaxRanks + 1] = {0};
   const size_t smem = routed_smem_bytes(a.nranks);
   if (!occ[a.nranks]) {
-    cudaFuncSetAttribute(k_walk_routed<kWalkNT, kWalkU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, kWalkU>, kWalkNT, smem);
+    cudaFuncSetAttribute(k_walk_routed<kWalkNT, kRoutedU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, kRoutedU>, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
   }
-  k_walk_routed<kWalkNT, kWalkU><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
+  k_walk_routed<kWalkNT, kRoutedU><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
 }
-
 }  // namespace tms

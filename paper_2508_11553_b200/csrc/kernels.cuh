@@ -105,6 +105,9 @@ struct RouteDesc {
   int64_t tok_off;  // int32 tokens
   int64_t idx_off;  // int32 query indices grouped by owner (written by k_route)
   int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
+  int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
+  int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
+  int32_t pad_;
   int32_t count[kMaxRanks];  // queries owned by each rank (written by k_route)
   int32_t start[kMaxRanks];
   // per (owner, length bucket; longest first) counts and starts in idx[], so owners can
@@ -410,6 +413,115 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
   // drain chunks issued but not consumed (keeps stage phases aligned; no copy may land
   // in a stage after it is reused)
   const int issued = min(nch, c - 1 + S);  // prologue issued S, each consumed chunk one more
+  for (int d = c; d < issued; d++) mbar_wait(&rg.bar[(base + d) % S], ((base + d) / S) & 1);
+  __syncthreads();
+  if (threadIdx.x == 0) rg.chunks = base + (uint32_t)issued;
+  __syncthreads();
+  return result;
+}
+
+// ---- TMA compare against a PACKED query (routed match: remote queries cross NVLink as
+// 18-bit split planes, hostpack.h layout: a uint16 low plane + one byte per 4 positions of
+// 2-bit high parts, byte (p & 7) of a 32-position group holding p, p+8, p+16, p+24) ------
+// Chunks are CHP positions; each plane is copied from its own aligned base (low plane: 8
+// positions = 16 B, high plane: 64 positions = 16 B, history: 4 positions), so a chunk
+// moves 2.25 B of query per position instead of 4.
+template <int S, int CHP>
+struct PackedRing {
+  uint16_t lo[S][CHP + 16];
+  uint8_t hi[S][CHP / 4 + 64];
+  int4 a[S][CHP / 4 + 4];
+  uint64_t bar[S];
+  uint32_t chunks;
+};
+
+template <int S, int CHP>
+__device__ __forceinline__ void packed_ring_init(PackedRing<S, CHP> &rg) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) mbar_init(&rg.bar[s], 1);
+    rg.chunks = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// plo / phi: the requester's planes (whole buffer); the query starts at plane position
+// qoff (a multiple of 32).  Same contract as block_first_mismatch_tma for positions [lo, hi)
+// of the query.
+template <int NT, int S, int CHP>
+__device__ __forceinline__ int block_first_mismatch_packed(const uint16_t *__restrict__ plo,
+                                                           const uint8_t *__restrict__ phi, int64_t qoff,
+                                                           const int32_t *__restrict__ a, int lo, int hi,
+                                                           int *s_red, PackedRing<S, CHP> &rg) {
+  static_assert(NT == 64, "written for 64-thread CTAs");
+  static_assert(CHP % (4 * NT) == 0 && CHP % 64 == 0, "chunk must split evenly over the CTA");
+  if (lo >= hi) return hi;
+  const int p0 = lo & ~3;  // chunk c covers positions [p0 + c*CHP, min(p0 + (c+1)*CHP, hi4))
+  const int hi4 = (hi + 3) & ~3;
+  const int nch = (hi4 - p0 + CHP - 1) / CHP;
+  const uint32_t base = rg.chunks;
+  auto issue = [&](int c) {
+    const int st = (int)((base + c) % S);
+    const int s0 = p0 + c * CHP, e0 = min(s0 + CHP, hi4);
+    const int64_t S0 = qoff + s0, E0 = qoff + e0;        // plane positions
+    const int64_t l0 = S0 & ~7ll, l1 = (E0 + 7) & ~7ll;  // low plane: 16-byte granules
+    const int64_t h0 = S0 & ~63ll, h1 = (E0 + 63) & ~63ll;  // high plane: 16-byte granules
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bl = 2u * (uint32_t)(l1 - l0), bh = (uint32_t)(h1 - h0) / 4u, ba = 4u * (uint32_t)(e0 - s0);
+    mbar_expect_tx(&rg.bar[st], bl + bh + ba);
+    bulk_g2s(rg.lo[st], plo + l0, bl, &rg.bar[st]);
+    bulk_g2s(rg.hi[st], phi + h0 / 4, bh, &rg.bar[st]);
+    bulk_g2s(rg.a[st], a + s0, ba, &rg.bar[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < S && c < nch; c++) issue(c);
+  int result = hi;
+  int c = 0;
+  for (; c < nch; c++) {
+    const int st = (int)((base + c) % S);
+    mbar_wait(&rg.bar[st], ((base + c) / S) & 1);
+    const int s0 = p0 + c * CHP;
+    const int64_t S0 = qoff + s0;
+    const int l0 = (int)(S0 & 7), h0 = (int)(S0 & 63);  // plane offsets of position s0 in the stage
+    int first = 0x7fffffff;
+#pragma unroll
+    for (int k = CHP / (4 * NT) - 1; k >= 0; k--) {
+      const int li = k * NT + threadIdx.x;  // int4 slot of the chunk
+      const int p = s0 + 4 * li;
+      if (p >= hi4) continue;
+      const int d = 4 * li;  // p - s0
+      const uint2 l = *reinterpret_cast<const uint2 *>(&rg.lo[st][l0 + d]);
+      const uint32_t hw = *reinterpret_cast<const uint32_t *>(&rg.hi[st][((h0 + d) >> 5) * 8 + ((h0 + d) & 7)]) >>
+                          (2 * (((h0 + d) >> 3) & 3));
+      int4 x;
+      x.x = (int)((l.x & 0xFFFFu) | ((hw & 3u) << 16));
+      x.y = (int)((l.x >> 16) | (((hw >> 8) & 3u) << 16));
+      x.z = (int)((l.y & 0xFFFFu) | (((hw >> 16) & 3u) << 16));
+      x.w = (int)((l.y >> 16) | (((hw >> 24) & 3u) << 16));
+      const int4 y = rg.a[st][li];
+      unsigned ne = (x.x != y.x ? 1u : 0u) | (x.y != y.y ? 2u : 0u) | (x.z != y.z ? 4u : 0u) | (x.w != y.w ? 8u : 0u);
+      unsigned valid = 0xfu;
+      if (p < lo) valid &= (0xfu << (lo - p)) & 0xfu;
+      if (p + 4 > hi) valid &= (hi - p) <= 0 ? 0u : (0xfu >> (4 - (hi - p)));
+      ne &= valid;
+      if (ne) first = min(first, p + __ffs(ne) - 1);
+    }
+    if (__syncthreads_or(first != 0x7fffffff)) {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      unsigned wmin = __reduce_min_sync(0xffffffffu, (unsigned)first);
+      if (lane == 0) s_red[warp] = (int)wmin;
+      __syncthreads();
+      int r = 0x7fffffff;
+#pragma unroll
+      for (int w = 0; w < NT / 32; w++) r = min(r, s_red[w]);
+      result = r;
+      c++;
+      break;
+    }
+    if (threadIdx.x == 0 && c + S < nch) issue(c + S);
+  }
+  const int issued = min(nch, c - 1 + S);
   for (int d = c; d < issued; d++) mbar_wait(&rg.bar[(base + d) % S], ((base + d) / S) & 1);
   __syncthreads();
   if (threadIdx.x == 0) rg.chunks = base + (uint32_t)issued;

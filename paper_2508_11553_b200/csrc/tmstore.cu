@@ -1406,9 +1406,19 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
     d.m_off = offsets[5];
     d.par_off = offsets[6];
     d.dup_off = offsets[7];
+    // 18-bit planes for the owners to pull over NVLink (only with peers; TM_ROUTE_PACK=0 off)
+    static const bool pack = [] {
+      const char *e = getenv("TM_ROUTE_PACK");
+      return !(e && !strcmp(e, "0"));
+    }();
+    const bool packed = pack && nranks > 1 && offsets[8] > 0 && offsets[9] > 0;
+    d.lo_off = packed ? offsets[8] : 0;
+    d.hi_off = packed ? offsets[9] : 0;
+    d.pk_bad = 0;
     // pageable source: the copy is staged before this call returns
     ck(cudaMemcpyAsync(region, &d, offsetof(tms::RouteDesc, count), cudaMemcpyHostToDevice, st), "H2D route desc");
     ck(tms::launch_route((char *)region, nranks, st), "route");
+    if (packed) ck(tms::launch_route_pack((char *)region, n, st), "route pack");
   });
 }
 

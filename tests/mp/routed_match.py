@@ -39,6 +39,18 @@ for sync in ("nccl", "device"):
     router.match(wl.n_queries, sync=sync)
     torch.cuda.synchronize()
     ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
+# an id beyond 18 bits (past every query's compared prefix: results unchanged) makes this
+# rank's owners read the int32 tokens instead of the packed planes
+i0 = int(np.argmax(wl.q_len - wl.q_depth > 8))
+pos = int(wl.q_off[i0] + wl.q_depth[i0] + 5)
+saved = int(router.tokens[pos].item())
+router.tokens[pos] = 1 << 20
+router.out_matched.fill_(-7)
+router.match(wl.n_queries)
+torch.cuda.synchronize()
+ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
+ok = ok and np.array_equal(router.out_parent[: wl.n_queries].cpu().numpy(), par)
+router.tokens[pos] = saved
 router.out_matched.fill_(-7)
 router.match_nccl(wl.n_queries)
 torch.cuda.synchronize()
