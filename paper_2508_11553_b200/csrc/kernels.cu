@@ -433,9 +433,12 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 }
 
 // Requester side (nranks > 1): pack this rank's query tokens into the region's 18-bit
-// planes (hostpack.h layout) for the owners to pull over NVLink.  One CTA per query, one
-// warp per 32-position group; positions past a query's end pack as 0 (never compared).
-// Any id outside [0, 2^18) sets pk_bad and the owners read the int32 tokens instead.
+// planes (hostpack.h layout) for the owners to pull over NVLink.  Each thread packs 8
+// consecutive positions (two 16-byte loads, one 16-byte store of the low plane); the 4
+// threads of a 32-position group OR their 2-bit parts into the group's 8 high-plane bytes
+// (one 8-byte store).  CTAs stride over queries; positions past a query's end pack as 0
+// (never compared).  Any id outside [0, 2^18) sets pk_bad and the owners read the int32
+// tokens instead.
 constexpr int kPackNT = 256;
 __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
@@ -444,22 +447,40 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   const int32_t *tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
   uint16_t *plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
   uint8_t *phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
   unsigned bad = 0;
   for (int64_t i = blockIdx.x; i < d->n; i += gridDim.x) {
     const int64_t off = qoff[i], len = qlen[i];
-    for (int64_t g = warp; 32 * g < len; g += kPackNT / 32) {
-      const int64_t r = 32 * g + lane, p = off + r;
-      const uint32_t t = r < len ? (uint32_t)tok[p] : 0u;
-      bad |= t >> 18;
-      plo[p] = (uint16_t)t;
-      uint32_t hb = ((t >> 16) & 3u) << (2 * (lane >> 3));
-      hb |= __shfl_xor_sync(0xffffffffu, hb, 8);
-      hb |= __shfl_xor_sync(0xffffffffu, hb, 16);
-      if (lane < 8) phi[(p - lane) / 4 + lane] = (uint8_t)hb;
+    const int64_t nch = (len + 31) / 32 * 4;  // 8-position chunks covering whole groups
+    for (int64_t c = threadIdx.x; c < nch; c += kPackNT) {
+      const int64_t r = 8 * c, p = off + r;
+      int t[8];
+      if (r + 8 <= len) {
+        const int4 a = ldg_stream(reinterpret_cast<const int4 *>(tok + p));
+        const int4 b = ldg_stream(reinterpret_cast<const int4 *>(tok + p + 4));
+        t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w; t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; u++) t[u] = r + u < len ? tok[p + u] : 0;
+      }
+      uint4 lo;
+      lo.x = ((uint32_t)t[0] & 0xFFFFu) | ((uint32_t)t[1] << 16);
+      lo.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
+      lo.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
+      lo.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
+      *reinterpret_cast<uint4 *>(plo + p) = lo;
+      unsigned long long h = 0;
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        bad |= (uint32_t)t[u] >> 18;
+        h |= (unsigned long long)(((uint32_t)t[u] >> 16) & 3u) << (8 * u + 2 * k);
+      }
+      h |= __shfl_xor_sync(0xffffffffu, h, 1);
+      h |= __shfl_xor_sync(0xffffffffu, h, 2);
+      if (k == 0) *reinterpret_cast<unsigned long long *>(phi + (p >> 5) * 8) = h;
     }
   }
-  if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(&d->pk_bad, 1);
+  if (bad) atomicOr(&d->pk_bad, 1);
 }
 
 // Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
@@ -468,11 +489,11 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
 // runs dry, so HBM and the links are busy at the same time instead of in phases.
 // Dynamic shared memory: [TmaRing (only when nranks > 1)][3 x kPlanNB x nranks + 2 ints
 // of routing tables], sized by routed_smem_bytes so a single rank keeps full occupancy.
-__host__ __device__ constexpr size_t routed_smem_bytes(int nranks) {
-  return (nranks > 1 ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
+__host__ __device__ constexpr size_t routed_smem_bytes(int nranks, bool packed) {
+  return (packed ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
 }
 
-template <int NT, int U>
+template <int NT, int U, bool PACKED>
 __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v, RoutedArgs a) {
   extern __shared__ __align__(16) char dyn[];
   __shared__ WalkShared sh;
@@ -483,9 +504,9 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   const int ncell = kPlanNB * np;
   // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
   // over NVLink (2.25 B per position instead of 4)
-  RoutedPackedRing *rg = np > 1 ? reinterpret_cast<RoutedPackedRing *>(dyn) : nullptr;
-  if (np > 1) packed_ring_init(*rg);
-  int *s_pre = reinterpret_cast<int *>(dyn + (np > 1 ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0));  // ncell + 2
+  RoutedPackedRing *rg = PACKED ? reinterpret_cast<RoutedPackedRing *>(dyn) : nullptr;
+  if constexpr (PACKED) packed_ring_init(*rg);
+  int *s_pre = reinterpret_cast<int *>(dyn + (PACKED ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0));  // ncell + 2
   int *s_bs = s_pre + ncell + 2;
   int *s_peer = s_bs + ncell;
   if (a.epoch > 0) {  // device-side barrier: every requester has bucketed its batch
@@ -566,13 +587,16 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
       continue;
     }
     const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
-    if (d->lo_off && !d->pk_bad) {  // packed planes: TMA bulk copies (over NVLink for remote queries)
-      const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
-                           reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
-      walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
-    } else {  // no peers (N=1), or ids that do not fit 18 bits: int32 tokens, register double buffer
-      walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);
+    bool packed_q = false;
+    if constexpr (PACKED) {
+      if (d->lo_off && !d->pk_bad) {  // packed planes: TMA bulk copies (over NVLink for remote queries)
+        const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
+                             reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
+        walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
+        packed_q = true;
+      }
     }
+    if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // int32 tokens, register double buffer
   }
 }
 
@@ -1564,18 +1588,24 @@ cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaSt
   return cudaGetLastError();
 }
 
-// U = 4 for the register path (no peers / ids beyond 18 bits): with the packed TMA compare
-// inlined as well, U = 8 spills
-constexpr int kRoutedU = 4;
-cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
+// One rank (no peers): the register-path kernel (U = 8).  Peers: the packed TMA compare for
+// every query whose requester packed its planes, the register path (U = 4: with the TMA
+// compare inlined as well, U = 8 spills) for a requester with ids beyond 18 bits.
+template <int U, bool PACKED>
+static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   static int occ[kMaxRanks + 1] = {0};
-  const size_t smem = routed_smem_bytes(a.nranks);
+  const size_t smem = routed_smem_bytes(a.nranks, PACKED);
   if (!occ[a.nranks]) {
-    cudaFuncSetAttribute(k_walk_routed<kWalkNT, kRoutedU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, kRoutedU>, kWalkNT, smem);
+    cudaFuncSetAttribute(k_walk_routed<kWalkNT, U, PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, U, PACKED>, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
   }
-  k_walk_routed<kWalkNT, kRoutedU><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
+  k_walk_routed<kWalkNT, U, PACKED><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
+  if (a.nranks > 1) return walk_routed_variant<4, true>(v, a, num_sms, s);
+  return walk_routed_variant<kWalkU, false>(v, a, num_sms, s);
 }
 }  // namespace tms
