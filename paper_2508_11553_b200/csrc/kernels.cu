@@ -440,6 +440,7 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 // (never compared).  Any id outside [0, 2^18) sets pk_bad and the owners read the int32
 // tokens instead.
 constexpr int kPackNT = 256;
+constexpr int kPackSplit = 16;  // CTAs per query
 __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
   const int64_t *qoff = reinterpret_cast<const int64_t *>(region + d->qoff_off);
@@ -449,10 +450,12 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   uint8_t *phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
   const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
   unsigned bad = 0;
+  // grid (queries, kPackSplit): the CTAs of one query interleave over its chunks, so a
+  // 128k-token query does not hold up the batch behind 1k-token ones
   for (int64_t i = blockIdx.x; i < d->n; i += gridDim.x) {
     const int64_t off = qoff[i], len = qlen[i];
     const int64_t nch = (len + 31) / 32 * 4;  // 8-position chunks covering whole groups
-    for (int64_t c = threadIdx.x; c < nch; c += kPackNT) {
+    for (int64_t c = (int64_t)blockIdx.y * kPackNT + threadIdx.x; c < nch; c += (int64_t)kPackNT * gridDim.y) {
       const int64_t r = 8 * c, p = off + r;
       int t[8];
       if (r + 8 <= len) {
@@ -1569,7 +1572,7 @@ int export_tile_tokens() { return kExportTile; }
 
 cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
   if (n < 1) return cudaSuccess;
-  k_route_pack<<<(int)std::min<int64_t>(n, 148 * 8), kPackNT, 0, s>>>(region);
+  k_route_pack<<<dim3((unsigned)std::min<int64_t>(n, 1 << 20), kPackSplit), kPackNT, 0, s>>>(region);
   return cudaGetLastError();
 }
 
