@@ -171,9 +171,10 @@ int tm_store_stream(tm_store *store, void **out_stream);
  *    uint16 low plane[tokens + 128] | uint8 high plane[(tokens + 128) / 4]]
  * (offsets[10] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup, lo,
  * hi; lo = hi = 0: no planes).  tm_route_prepare writes the header, buckets the batch by
- * owner rank (owner = splitmix64(gsid) mod nranks) and, with peers, packs the tokens into
- * the 18-bit planes (hostpack.h layout; TM_ROUTE_PACK=0 disables) so remote owners move
- * 2.25 B per compared position over NVLink instead of 4.  Then either tm_match_routed_sync
+ * owner rank (owner = splitmix64(gsid) mod nranks) and, with peers, packs the tokens of the
+ * queries owned by OTHER ranks (this is `rank`) into the 18-bit planes (hostpack.h layout;
+ * TM_ROUTE_PACK=0 disables) so remote owners move 2.25 B per compared position over NVLink
+ * instead of 4.  Then either tm_match_routed_sync
  * (device-side barriers) or a cross-rank barrier + tm_match_routed + a second barrier:
  * every owner's kernel reads its queries directly from the requesters' regions over
  * NVLink and writes the results back into them (P2P).
@@ -186,7 +187,7 @@ int tm_ipc_handle(tm_store *store, void *ptr, void *out_handle64);
 int tm_ipc_open(tm_store *store, const void *handle64, void **out_ptr);
 int tm_ipc_close(tm_store *store, void *ptr);
 int tm_route_prepare(tm_store *store, void *region, int64_t n, const int64_t *offsets, int32_t nranks,
-                     void *stream);
+                     int32_t rank, void *stream);
 /* Per-owner query counts of a prepared region (kMaxRanks = 16 int32; synchronous). */
 int tm_route_counts(tm_store *store, const void *region, int32_t *out_counts16, void *stream);
 /* g2l: device int32[global sessions] -> this store's session id (-1 if not owned).

@@ -437,8 +437,8 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 // consecutive positions (two 16-byte loads, one 16-byte store of the low plane); the 4
 // threads of a 32-position group OR their 2-bit parts into the group's 8 high-plane bytes
 // (one 8-byte store).  CTAs stride over queries; positions past a query's end pack as 0
-// (never compared).  Any id outside [0, 2^18) sets pk_bad and the owners read the int32
-// tokens instead.
+// (never compared).  Queries this rank owns itself are skipped (read from HBM as int32).
+// Any id outside [0, 2^18) sets pk_bad and the owners read the int32 tokens instead.
 constexpr int kPackNT = 256;
 constexpr int kPackSplit = 16;  // CTAs per query
 __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
@@ -452,7 +452,9 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   unsigned bad = 0;
   // grid (queries, kPackSplit): the CTAs of one query interleave over its chunks, so a
   // 128k-token query does not hold up the batch behind 1k-token ones
+  const int64_t *gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
   for (int64_t i = blockIdx.x; i < d->n; i += gridDim.x) {
+    if (owner_of(gsid[i], d->nranks) == d->rank) continue;  // this rank matches its own queries from HBM
     const int64_t off = qoff[i], len = qlen[i];
     const int64_t nch = (len + 31) / 32 * 4;  // 8-position chunks covering whole groups
     for (int64_t c = (int64_t)blockIdx.y * kPackNT + threadIdx.x; c < nch; c += (int64_t)kPackNT * gridDim.y) {
@@ -592,14 +594,14 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
     const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
     bool packed_q = false;
     if constexpr (PACKED) {
-      if (d->lo_off && !d->pk_bad) {  // packed planes: TMA bulk copies (over NVLink for remote queries)
+      if (p != a.rank && d->lo_off && !d->pk_bad) {  // remote query: packed planes, TMA bulk copies over NVLink
         const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
                              reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
         walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
         packed_q = true;
       }
     }
-    if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // int32 tokens, register double buffer
+    if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // local (or ids beyond 18 bits): int32, registers
   }
 }
 

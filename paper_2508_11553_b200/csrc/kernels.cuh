@@ -107,6 +107,8 @@ struct RouteDesc {
   int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
   int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
   int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
+  int32_t rank;                     // the rank whose batch this is (its own queries stay unpacked)
+  int32_t nranks;
   int32_t pad_;
   int32_t count[kMaxRanks];  // queries owned by each rank (written by k_route)
   int32_t start[kMaxRanks];

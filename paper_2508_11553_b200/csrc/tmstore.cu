@@ -1390,12 +1390,15 @@ int tm_route_desc_bytes(int64_t *out_bytes) {
   return TM_OK;
 }
 
-int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, void *stream) {
+int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, int32_t rank,
+                     void *stream) {
   NvtxRange nvtx_("tm_route_prepare");
   return guarded(s, [&] {
-    if (nranks < 1 || nranks > tms::kMaxRanks) fail(TM_EINVAL, "nranks out of range");
+    if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
     tms::RouteDesc d{};  // counts are (re)written by k_route
+    d.rank = rank;
+    d.nranks = nranks;
     if (offsets[0] < (int64_t)sizeof(d)) fail(TM_EINVAL, "routing arrays overlap the RouteDesc header");
     d.n = n;
     d.sid_off = offsets[0];

@@ -143,7 +143,7 @@ class Router:
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
         g2l = C.c_void_p(self.g2l.data_ptr())
-        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, st))
+        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, self.rank, st))
         if sync == "device" and self.nranks > 1:
             self._epoch += 1
             check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self._epoch, st))
@@ -168,7 +168,7 @@ class Router:
         st = torch.cuda.current_stream(self.store.device).cuda_stream
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
-        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, st))
+        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, self.rank, st))
         cnt = np.zeros(16, np.int32)
         check(lib.tm_route_counts(h, C.c_void_p(self.base), cnt.ctypes.data_as(C.c_void_p), st))
         counts = cnt[: self.nranks].astype(np.int64)
