@@ -327,6 +327,7 @@ __device__ __forceinline__ int owner_of(int64_t gsid, int nranks) {
 }
 
 constexpr int kRouteNT = 1024;
+constexpr int kPackBlock = 4096;  // positions per k_route_pack work item
 
 // One CTA buckets the batch by (owner, length bucket) — owner-major, longest first.
 __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
@@ -379,6 +380,39 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n; i += kRouteNT)
     idx[atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1)] = (int32_t)i;
+  if (!d->lo_off) return;
+  // pack work for k_route_pack: the queries owned by OTHER ranks (idx minus this rank's
+  // range), cut into 4096-position blocks; pkf[j] = blocks before remote query j
+  __syncthreads();
+  int32_t *pkf = reinterpret_cast<int32_t *>(region + d->pkf_off);
+  const int own0 = d->start[d->rank], own1 = own0 + d->count[d->rank];
+  const int64_t nrem = n - (own1 - own0);
+  int running = 0;
+  for (int64_t b0 = 0; b0 < nrem; b0 += kRouteNT) {
+    const int64_t j = b0 + threadIdx.x;
+    int blocks = 0;
+    if (j < nrem) {
+      const int64_t q = idx[j < own0 ? j : j + (own1 - own0)];
+      blocks = (int)((len[q] + kPackBlock - 1) / kPackBlock);
+    }
+    int y = blocks;  // inclusive warp scan, then across warps
+#pragma unroll
+    for (int s2 = 1; s2 < 32; s2 <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, y, s2);
+      if (lane >= s2) y += t;
+    }
+    if (lane == 31) wsum[warp] = y;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int w = 0; w < kRouteNT / 32; w++) {
+      if (w < warp) wpre += wsum[w];
+      tot += wsum[w];
+    }
+    if (j < nrem) pkf[j] = running + wpre + y - blocks;
+    running += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pkf[nrem] = running;
 }
 
 // ---- device-side cross-rank barriers (epoch flags in the RouteDesc headers) ----------
@@ -440,25 +474,34 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 // (never compared).  Queries this rank owns itself are skipped (read from HBM as int32).
 // Any id outside [0, 2^18) sets pk_bad and the owners read the int32 tokens instead.
 constexpr int kPackNT = 256;
-constexpr int kPackSplit = 16;  // CTAs per query
 __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
   const int64_t *qoff = reinterpret_cast<const int64_t *>(region + d->qoff_off);
   const int64_t *qlen = reinterpret_cast<const int64_t *>(region + d->len_off);
   const int32_t *tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
+  const int32_t *idx = reinterpret_cast<const int32_t *>(region + d->idx_off);
+  const int32_t *pkf = reinterpret_cast<const int32_t *>(region + d->pkf_off);
   uint16_t *plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
   uint8_t *phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
+  const int own0 = d->start[d->rank], nown = d->count[d->rank];
+  const int64_t nrem = d->n - nown;
+  const int64_t nblk = pkf[nrem];
   const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
   unsigned bad = 0;
-  // grid (queries, kPackSplit): the CTAs of one query interleave over its chunks, so a
-  // 128k-token query does not hold up the batch behind 1k-token ones
-  const int64_t *gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
-  for (int64_t i = blockIdx.x; i < d->n; i += gridDim.x) {
-    if (owner_of(gsid[i], d->nranks) == d->rank) continue;  // this rank matches its own queries from HBM
-    const int64_t off = qoff[i], len = qlen[i];
-    const int64_t nch = (len + 31) / 32 * 4;  // 8-position chunks covering whole groups
-    for (int64_t c = (int64_t)blockIdx.y * kPackNT + threadIdx.x; c < nch; c += (int64_t)kPackNT * gridDim.y) {
-      const int64_t r = 8 * c, p = off + r;
+  // persistent CTAs over 4096-position blocks of the remote queries (k_route's prefix)
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    int64_t lo = 0, hi = nrem;  // last remote query j with pkf[j] <= blk
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (pkf[mid] <= blk) lo = mid; else hi = mid;
+    }
+    const int64_t q = idx[lo < own0 ? lo : lo + nown];
+    const int64_t off = qoff[q], len = qlen[q];
+    const int64_t r0 = (blk - pkf[lo]) * kPackBlock;
+#pragma unroll
+    for (int u2 = 0; u2 < kPackBlock / (8 * kPackNT); u2++) {
+      const int64_t r = r0 + 8 * (u2 * kPackNT + (int64_t)threadIdx.x), p = off + r;
+      if (r >= (len + 31) / 32 * 32) continue;  // (uniform per 32-position group)
       int t[8];
       if (r + 8 <= len) {
         const int4 a = ldg_stream(reinterpret_cast<const int4 *>(tok + p));
@@ -468,20 +511,21 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
 #pragma unroll
         for (int u = 0; u < 8; u++) t[u] = r + u < len ? tok[p + u] : 0;
       }
-      uint4 lo;
-      lo.x = ((uint32_t)t[0] & 0xFFFFu) | ((uint32_t)t[1] << 16);
-      lo.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
-      lo.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
-      lo.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
-      *reinterpret_cast<uint4 *>(plo + p) = lo;
+      uint4 lo4;
+      lo4.x = ((uint32_t)t[0] & 0xFFFFu) | ((uint32_t)t[1] << 16);
+      lo4.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
+      lo4.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
+      lo4.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
+      *reinterpret_cast<uint4 *>(plo + p) = lo4;
       unsigned long long h = 0;
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         bad |= (uint32_t)t[u] >> 18;
         h |= (unsigned long long)(((uint32_t)t[u] >> 16) & 3u) << (8 * u + 2 * k);
       }
-      h |= __shfl_xor_sync(0xffffffffu, h, 1);
-      h |= __shfl_xor_sync(0xffffffffu, h, 2);
+      const unsigned quad = __activemask();  // whole 32-position groups are active together
+      h |= __shfl_xor_sync(quad, h, 1);
+      h |= __shfl_xor_sync(quad, h, 2);
       if (k == 0) *reinterpret_cast<unsigned long long *>(phi + (p >> 5) * 8) = h;
     }
   }
@@ -1574,7 +1618,7 @@ int export_tile_tokens() { return kExportTile; }
 
 cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
   if (n < 1) return cudaSuccess;
-  k_route_pack<<<dim3((unsigned)std::min<int64_t>(n, 1 << 20), kPackSplit), kPackNT, 0, s>>>(region);
+  k_route_pack<<<148 * 8, kPackNT, 0, s>>>(region);
   return cudaGetLastError();
 }
 

@@ -106,6 +106,7 @@ struct RouteDesc {
   int64_t idx_off;  // int32 query indices grouped by owner (written by k_route)
   int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
   int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
+  int64_t pkf_off;                  // int32[n+1]: 4096-position pack blocks before each remote query (k_route)
   int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
   int32_t rank;                     // the rank whose batch this is (its own queries stay unpacked)
   int32_t nranks;

@@ -1414,9 +1414,10 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
       const char *e = getenv("TM_ROUTE_PACK");
       return !(e && !strcmp(e, "0"));
     }();
-    const bool packed = pack && nranks > 1 && offsets[8] > 0 && offsets[9] > 0;
+    const bool packed = pack && nranks > 1 && offsets[8] > 0 && offsets[9] > 0 && offsets[10] > 0;
     d.lo_off = packed ? offsets[8] : 0;
     d.hi_off = packed ? offsets[9] : 0;
+    d.pkf_off = packed ? offsets[10] : 0;
     d.pk_bad = 0;
     // pageable source: the copy is staged before this call returns
     ck(cudaMemcpyAsync(region, &d, offsetof(tms::RouteDesc, count), cudaMemcpyHostToDevice, st), "H2D route desc");
