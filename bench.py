@@ -276,6 +276,7 @@ def run_c5(args):
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
+        phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
         # keep the clocks sampler running for >= 1 s under load; every rank must make the
         # same number of (collective) routed calls, so the count is agreed on first
         left = torch.tensor([max(0.0, 1.0 - (time.perf_counter() - t_wall))], device=dev, dtype=torch.float64)
@@ -315,6 +316,7 @@ def run_c5(args):
         "tokens_compared_per_s": toks * args.steps / elapsed,
         "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * args.steps / elapsed / 1e9,
         "routed_walk_ms_avg_rank0": walk_ms / max(walk_n, 1),
+        "phase_ms_avg_rank0": {k: (ms / n if n else 0.0) for k, (ms, n) in phase_ms.items()},
         "nvlink_query_GBps_during_walk_rank0": 4.0 * remote_toks / world / (walk_ms / max(walk_n, 1)) / 1e6,
         "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
                      "achieved": (4.0 * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
@@ -325,8 +327,10 @@ def run_c5(args):
                      "traffic": None,
                      "note": "N>1: remote query bytes cross NVLink (tools/p2p_probe: SM peer reads 780 GB/s one "
                              "direction, 670 GB/s both directions at once); history bytes come from local HBM"},
-        # ours per batch: k_route + k_walk_routed (+ k_route_arrive + k_route_wait_done with device barriers)
-        "gpu_launches": args.steps * (4 if args.routing == "fused" else 2),
+        # ours per batch: k_route + k_walk_routed (+ k_route_pack with peers, + k_route_arrive +
+        # k_route_wait_done with device barriers)
+        "gpu_launches": args.steps * ((4 if args.routing == "fused" else 2) + (1 if world > 1 and
+                                                                             args.routing != "nccl" else 0)),
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -432,6 +436,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
+        phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
         plan_ms, plan_n = store.profile_end("plan")
         # short regions: keep the identical load running so the sampler sees >= 1 s of it
         while time.perf_counter() - t_wall < 1.0:

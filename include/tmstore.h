@@ -214,7 +214,10 @@ int tm_store_load(tm_store *store, const char *path);
 /* Per-kernel CUDA-event timing for benchmarks.  tm_profile_begin starts recording an
  * event pair around every launch; tm_profile_end(kind) waits for them and returns the
  * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */
-enum { TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3 };
+enum {
+  TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3,
+  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6
+};
 int tm_profile_begin(tm_store *store);
 int tm_profile_end(tm_store *store, int32_t kind, double *total_ms, int64_t *launches);
 

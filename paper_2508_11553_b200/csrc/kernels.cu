@@ -329,20 +329,44 @@ __device__ __forceinline__ int owner_of(int64_t gsid, int nranks) {
 constexpr int kRouteNT = 1024;
 constexpr int kPackBlock = 4096;  // positions per k_route_pack work item
 
-// One CTA buckets the batch by (owner, length bucket) — owner-major, longest first.
-__global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
+// One CTA buckets the batch by (owner, length bucket) — owner-major, longest first — and,
+// when the planes are packed, builds the pack work list.  Latency-bound (one CTA), so
+// every pass issues all of a thread's loads of a chunk before using any of them: the
+// whole kernel is a handful of dependent global round trips for a 4096-query batch.
+constexpr int kRouteU = 4;  // queries per thread per chunk
+__global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
-  const int64_t n = d->n;
-  const int64_t *gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
-  const int64_t *len = reinterpret_cast<const int64_t *>(region + d->len_off);
-  int32_t *idx = reinterpret_cast<int32_t *>(region + d->idx_off);
+  if (threadIdx.x == 0) *reinterpret_cast<RouteHead *>(region) = head;
+  const int nranks = head.nranks;
+  const int64_t n = head.n;
+  const int64_t *gsid = reinterpret_cast<const int64_t *>(region + head.sid_off);
+  const int64_t *len = reinterpret_cast<const int64_t *>(region + head.len_off);
+  int32_t *idx = reinterpret_cast<int32_t *>(region + head.idx_off);
   constexpr int NC = kMaxRanks * kPlanNB;
+  constexpr int CH = kRouteNT * kRouteU;
   __shared__ int cnt[NC];
   __shared__ int wsum[kRouteNT / 32];
   for (int i = threadIdx.x; i < NC; i += kRouteNT) cnt[i] = 0;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < n; i += kRouteNT)
-    atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1);
+  auto load_keys = [&](int64_t c0, int key[kRouteU], int64_t L[kRouteU]) {
+    int64_t g[kRouteU];
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++) {
+      const int64_t i = c0 + u * kRouteNT + threadIdx.x;
+      g[u] = i < n ? gsid[i] : 0;
+      L[u] = i < n ? len[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++) key[u] = owner_of(g[u], nranks) * kPlanNB + len_bucket(L[u]);
+  };
+  for (int64_t c0 = 0; c0 < n; c0 += CH) {
+    int key[kRouteU];
+    int64_t L[kRouteU];
+    load_keys(c0, key, L);
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++)
+      if (c0 + u * kRouteNT + threadIdx.x < n) atomicAdd(&cnt[key[u]], 1);
+  }
   __syncthreads();
   // exclusive scan of the 2048 counters (2 per thread)
   constexpr int PER = NC / kRouteNT;
@@ -362,40 +386,57 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
   for (int w = 0; w < warp; w++) pre += wsum[w];
   const int excl = pre + x - acc;
   __syncthreads();
+  __shared__ int s_own0, s_nown;
 #pragma unroll
   for (int j = 0; j < PER; j++) {
     const int c = threadIdx.x * PER + j;
     d->bcount[c] = cnt[c];
     d->bstart[c] = excl + loc[j];
+    cnt[c] = excl + loc[j];  // cursors
   }
   __syncthreads();
   if (threadIdx.x < kMaxRanks) {
-    int tot = 0;
-    for (int b2 = 0; b2 < kPlanNB; b2++) tot += d->bcount[threadIdx.x * kPlanNB + b2];
-    d->count[threadIdx.x] = tot;
-    d->start[threadIdx.x] = d->bstart[threadIdx.x * kPlanNB];
+    const int r = threadIdx.x;
+    const int st = cnt[r * kPlanNB];
+    const int tot = (r + 1 < kMaxRanks ? cnt[(r + 1) * kPlanNB] : (int)n) - st;
+    d->count[r] = tot;
+    d->start[r] = st;
+    if (r == head.rank) { s_own0 = st; s_nown = tot; }
   }
+  __syncthreads();
+  // scatter; with planes, also the pack blocks of every remote query at its place in the
+  // remote order (idx minus this rank's own range)
+  const bool pk = head.lo_off != 0;
+  int32_t *pkf = reinterpret_cast<int32_t *>(region + head.pkf_off);
+  const int own0 = s_own0, nown = s_nown;
+  for (int64_t c0 = 0; c0 < n; c0 += CH) {
+    int key[kRouteU];
+    int64_t L[kRouteU];
+    load_keys(c0, key, L);
 #pragma unroll
-  for (int j = 0; j < PER; j++) cnt[threadIdx.x * PER + j] = excl + loc[j];  // cursors
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < n; i += kRouteNT)
-    idx[atomicAdd(&cnt[owner_of(gsid[i], nranks) * kPlanNB + len_bucket(len[i])], 1)] = (int32_t)i;
-  if (!d->lo_off) return;
-  // pack work for k_route_pack: the queries owned by OTHER ranks (idx minus this rank's
-  // range), cut into 4096-position blocks; pkf[j] = blocks before remote query j
-  __syncthreads();
-  int32_t *pkf = reinterpret_cast<int32_t *>(region + d->pkf_off);
-  const int own0 = d->start[d->rank], own1 = own0 + d->count[d->rank];
-  const int64_t nrem = n - (own1 - own0);
-  int running = 0;
-  for (int64_t b0 = 0; b0 < nrem; b0 += kRouteNT) {
-    const int64_t j = b0 + threadIdx.x;
-    int blocks = 0;
-    if (j < nrem) {
-      const int64_t q = idx[j < own0 ? j : j + (own1 - own0)];
-      blocks = (int)((len[q] + kPackBlock - 1) / kPackBlock);
+    for (int u = 0; u < kRouteU; u++) {
+      const int64_t i = c0 + u * kRouteNT + threadIdx.x;
+      if (i >= n) continue;
+      const int pos = atomicAdd(&cnt[key[u]], 1);
+      idx[pos] = (int32_t)i;
+      if (pk && key[u] / kPlanNB != head.rank)
+        pkf[pos < own0 ? pos : pos - nown] = (int)((L[u] + kPackBlock - 1) / kPackBlock);
     }
-    int y = blocks;  // inclusive warp scan, then across warps
+  }
+  if (!pk) return;
+  // pkf[j] = blocks before remote query j (exclusive scan in place), pkf[nrem] = total
+  __syncthreads();
+  const int64_t nrem = n - nown;
+  int running = 0;
+  for (int64_t c0 = 0; c0 < nrem; c0 += CH) {
+    int v[kRouteU], sum = 0;
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++) {
+      const int64_t j = c0 + (int64_t)threadIdx.x * kRouteU + u;
+      v[u] = j < nrem ? pkf[j] : 0;
+      sum += v[u];
+    }
+    int y = sum;  // inclusive warp scan, then across warps
 #pragma unroll
     for (int s2 = 1; s2 < 32; s2 <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, y, s2);
@@ -408,7 +449,13 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, int nranks) {
       if (w < warp) wpre += wsum[w];
       tot += wsum[w];
     }
-    if (j < nrem) pkf[j] = running + wpre + y - blocks;
+    int e = running + wpre + y - sum;
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++) {
+      const int64_t j = c0 + (int64_t)threadIdx.x * kRouteU + u;
+      if (j < nrem) pkf[j] = e;
+      e += v[u];
+    }
     running += tot;
     __syncthreads();
   }
@@ -467,69 +514,108 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 }
 
 // Requester side (nranks > 1): pack this rank's query tokens into the region's 18-bit
-// planes (hostpack.h layout) for the owners to pull over NVLink.  Each thread packs 8
-// consecutive positions (two 16-byte loads, one 16-byte store of the low plane); the 4
-// threads of a 32-position group OR their 2-bit parts into the group's 8 high-plane bytes
-// (one 8-byte store).  CTAs stride over queries; positions past a query's end pack as 0
-// (never compared).  Queries this rank owns itself are skipped (read from HBM as int32).
-// Any id outside [0, 2^18) sets pk_bad and the owners read the int32 tokens instead.
+// planes (hostpack.h layout) for the owners to pull over NVLink.  Work item = a
+// 4096-position block of a query owned by ANOTHER rank (queries this rank owns itself are
+// read from HBM as int32), located through k_route's block prefix pkf.  Each thread packs
+// 8 consecutive positions per slot (two 16-byte loads, one 16-byte store of the low
+// plane); the 4 threads of a 32-position group OR their 2-bit parts into the group's 8
+// high-plane bytes (one 8-byte store).  All of a thread's loads are issued before any
+// packing so a 64-thread CTA keeps 8 x 32 B in flight per thread.  Positions past a
+// query's end pack as 0 (never compared).  Returns nonzero if any id is outside [0, 2^18)
+// (the owners then read the int32 tokens instead).
 constexpr int kPackNT = 256;
-__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
+struct PackView {
+  const int64_t *qoff, *qlen;
+  const int32_t *tok, *idx, *pkf;
+  uint16_t *plo;
+  uint8_t *phi;
+  int own0, nown;
+  int64_t nrem, nblk;
+};
+__device__ __forceinline__ PackView pack_view(char *region) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
-  const int64_t *qoff = reinterpret_cast<const int64_t *>(region + d->qoff_off);
-  const int64_t *qlen = reinterpret_cast<const int64_t *>(region + d->len_off);
-  const int32_t *tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
-  const int32_t *idx = reinterpret_cast<const int32_t *>(region + d->idx_off);
-  const int32_t *pkf = reinterpret_cast<const int32_t *>(region + d->pkf_off);
-  uint16_t *plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
-  uint8_t *phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
-  const int own0 = d->start[d->rank], nown = d->count[d->rank];
-  const int64_t nrem = d->n - nown;
-  const int64_t nblk = pkf[nrem];
+  PackView w;
+  w.qoff = reinterpret_cast<const int64_t *>(region + d->qoff_off);
+  w.qlen = reinterpret_cast<const int64_t *>(region + d->len_off);
+  w.tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
+  w.idx = reinterpret_cast<const int32_t *>(region + d->idx_off);
+  w.pkf = reinterpret_cast<const int32_t *>(region + d->pkf_off);
+  w.plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
+  w.phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
+  w.own0 = d->start[d->rank];
+  w.nown = d->count[d->rank];
+  w.nrem = d->n - w.nown;
+  w.nblk = w.pkf[w.nrem];
+  return w;
+}
+// block blk of remote query j (pkf[j] <= blk < pkf[j + 1]); bj = pkf[j]
+template <int NT>
+__device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int64_t bj, int64_t blk) {
+  constexpr int SL = kPackBlock / (8 * NT);  // 8-position slots per thread
+  const int64_t q = w.idx[j < w.own0 ? j : j + w.nown];
+  const int64_t off = w.qoff[q], len = w.qlen[q];
+  const int64_t r0 = (blk - bj) * kPackBlock;
   const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
-  unsigned bad = 0;
-  // persistent CTAs over 4096-position blocks of the remote queries (k_route's prefix)
-  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    int64_t lo = 0, hi = nrem;  // last remote query j with pkf[j] <= blk
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (pkf[mid] <= blk) lo = mid; else hi = mid;
-    }
-    const int64_t q = idx[lo < own0 ? lo : lo + nown];
-    const int64_t off = qoff[q], len = qlen[q];
-    const int64_t r0 = (blk - pkf[lo]) * kPackBlock;
+  int4 a[SL], b[SL];
 #pragma unroll
-    for (int u2 = 0; u2 < kPackBlock / (8 * kPackNT); u2++) {
-      const int64_t r = r0 + 8 * (u2 * kPackNT + (int64_t)threadIdx.x), p = off + r;
-      if (r >= (len + 31) / 32 * 32) continue;  // (uniform per 32-position group)
+  for (int u = 0; u < SL; u++) {
+    const int64_t r = r0 + 8 * (u * NT + (int64_t)threadIdx.x), p = off + r;
+    if (r + 8 <= len) {
+      a[u] = ldg_stream(reinterpret_cast<const int4 *>(w.tok + p));
+      b[u] = ldg_stream(reinterpret_cast<const int4 *>(w.tok + p + 4));
+    } else {
       int t[8];
-      if (r + 8 <= len) {
-        const int4 a = ldg_stream(reinterpret_cast<const int4 *>(tok + p));
-        const int4 b = ldg_stream(reinterpret_cast<const int4 *>(tok + p + 4));
-        t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w; t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
-      } else {
 #pragma unroll
-        for (int u = 0; u < 8; u++) t[u] = r + u < len ? tok[p + u] : 0;
-      }
-      uint4 lo4;
-      lo4.x = ((uint32_t)t[0] & 0xFFFFu) | ((uint32_t)t[1] << 16);
-      lo4.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
-      lo4.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
-      lo4.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
-      *reinterpret_cast<uint4 *>(plo + p) = lo4;
-      unsigned long long h = 0;
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        bad |= (uint32_t)t[u] >> 18;
-        h |= (unsigned long long)(((uint32_t)t[u] >> 16) & 3u) << (8 * u + 2 * k);
-      }
-      const unsigned quad = __activemask();  // whole 32-position groups are active together
-      h |= __shfl_xor_sync(quad, h, 1);
-      h |= __shfl_xor_sync(quad, h, 2);
-      if (k == 0) *reinterpret_cast<unsigned long long *>(phi + (p >> 5) * 8) = h;
+      for (int e = 0; e < 8; e++) t[e] = r + e < len ? w.tok[p + e] : 0;
+      a[u] = make_int4(t[0], t[1], t[2], t[3]);
+      b[u] = make_int4(t[4], t[5], t[6], t[7]);
     }
   }
-  if (bad) atomicOr(&d->pk_bad, 1);
+  unsigned bad = 0;
+#pragma unroll
+  for (int u = 0; u < SL; u++) {
+    const int64_t r = r0 + 8 * (u * NT + (int64_t)threadIdx.x), p = off + r;
+    if (r >= (len + 31) / 32 * 32) continue;  // (uniform per 32-position group)
+    const int t[8] = {a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, b[u].y, b[u].z, b[u].w};
+    uint4 lo4;
+    lo4.x = ((uint32_t)t[0] & 0xFFFFu) | ((uint32_t)t[1] << 16);
+    lo4.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
+    lo4.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
+    lo4.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
+    *reinterpret_cast<uint4 *>(w.plo + p) = lo4;
+    unsigned long long h = 0;
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      bad |= (uint32_t)t[e] >> 18;
+      h |= (unsigned long long)(((uint32_t)t[e] >> 16) & 3u) << (8 * e + 2 * k);
+    }
+    const unsigned quad = __activemask();  // whole 32-position groups are active together
+    h |= __shfl_xor_sync(quad, h, 1);
+    h |= __shfl_xor_sync(quad, h, 2);
+    if (k == 0) *reinterpret_cast<unsigned long long *>(w.phi + (p >> 5) * 8) = h;
+  }
+  return bad;
+}
+
+// tm_route_prepare with peers: every CTA packs one contiguous range of blocks (one
+// binary search for its first query, then it steps through the queries in order)
+__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
+  const PackView w = pack_view(region);
+  const int64_t per = (w.nblk + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = min(w.nblk, b0 + per);
+  if (b0 >= b1) return;
+  int64_t lo = 0, hi = w.nrem;  // last remote query j with pkf[j] <= b0
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (w.pkf[mid] <= b0) lo = mid; else hi = mid;
+  }
+  int64_t j = lo, bj = w.pkf[j], bn = w.pkf[j + 1];
+  unsigned bad = 0;
+  for (int64_t blk = b0; blk < b1; blk++) {
+    while (blk >= bn) { j++; bj = bn; bn = w.pkf[j + 1]; }
+    bad |= pack_block<kPackNT>(w, j, bj, blk);
+  }
+  if (bad) atomicOr(&reinterpret_cast<RouteDesc *>(region)->pk_bad, 1);
 }
 
 // Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
@@ -538,11 +624,12 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
 // runs dry, so HBM and the links are busy at the same time instead of in phases.
 // Dynamic shared memory: [TmaRing (only when nranks > 1)][3 x kPlanNB x nranks + 2 ints
 // of routing tables], sized by routed_smem_bytes so a single rank keeps full occupancy.
+template <class RG>
 __host__ __device__ constexpr size_t routed_smem_bytes(int nranks, bool packed) {
-  return (packed ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
+  return (packed ? (sizeof(RG) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
 }
 
-template <int NT, int U, bool PACKED>
+template <int NT, int U, bool PACKED, class RG = RoutedPackedRing>
 __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v, RoutedArgs a) {
   extern __shared__ __align__(16) char dyn[];
   __shared__ WalkShared sh;
@@ -553,14 +640,14 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   const int ncell = kPlanNB * np;
   // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
   // over NVLink (2.25 B per position instead of 4)
-  RoutedPackedRing *rg = PACKED ? reinterpret_cast<RoutedPackedRing *>(dyn) : nullptr;
+  RG *rg = PACKED ? reinterpret_cast<RG *>(dyn) : nullptr;
   if constexpr (PACKED) packed_ring_init(*rg);
-  int *s_pre = reinterpret_cast<int *>(dyn + (PACKED ? (sizeof(RoutedPackedRing) + 15) / 16 * 16 : 0));  // ncell + 2
+  int *s_pre = reinterpret_cast<int *>(dyn + (PACKED ? (sizeof(RG) + 15) / 16 * 16 : 0));  // ncell + 2
   int *s_bs = s_pre + ncell + 2;
   int *s_peer = s_bs + ncell;
+  RouteDesc *own = reinterpret_cast<RouteDesc *>(const_cast<char *>(a.peer[a.rank]));
   if (a.epoch > 0) {  // device-side barrier: every requester has bucketed its batch
-    if (threadIdx.x == 0)
-      wait_flags(v, reinterpret_cast<const RouteDesc *>(a.peer[a.rank])->arrive, np, a.epoch, a.timeout_ns);
+    if (threadIdx.x == 0) wait_flags(v, own->arrive, np, a.epoch, a.timeout_ns);
     __syncthreads();
   }
   // cell c: local cells first (bucket order), then remote cells (bucket, peer) order
@@ -591,9 +678,8 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
     if (threadIdx.x == 0) {
       long long it = -1;
       int cell = -1;
-      for (int tries = 0; tries < 2 && it < 0; tries++) {
-        const int qq = tries ? 1 - q : q;
-        if (dry[qq]) continue;
+      while (it < 0 && !(dry[0] && dry[1])) {
+        const int qq = dry[q] ? 1 - q : q;
         const long long x = (long long)atomicAdd(qq ? &a.sched->work2 : &a.sched->work, 1ull);
         if (x >= tot[qq]) { dry[qq] = true; continue; }
         int lo = qq ? kPlanNB : 0, hi = qq ? ncell : kPlanNB;  // last cell with prefix <= x
@@ -638,7 +724,8 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
     const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
     bool packed_q = false;
     if constexpr (PACKED) {
-      if (p != a.rank && d->lo_off && !d->pk_bad) {  // remote query: packed planes, TMA bulk copies over NVLink
+      if (p != a.rank && d->lo_off && !*reinterpret_cast<const volatile int32_t *>(&d->pk_bad)) {
+        // remote query: packed planes, TMA bulk copies over NVLink
         const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
                              reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
         walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
@@ -1622,8 +1709,8 @@ cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_route(char *region, int nranks, cudaStream_t s) {
-  k_route<<<1, kRouteNT, 0, s>>>(region, nranks);
+cudaError_t launch_route(char *region, const RouteHead &head, cudaStream_t s) {
+  k_route<<<1, kRouteNT, 0, s>>>(region, head);
   return cudaGetLastError();
 }
 
@@ -1640,21 +1727,34 @@ cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaSt
 // One rank (no peers): the register-path kernel (U = 8).  Peers: the packed TMA compare for
 // every query whose requester packed its planes, the register path (U = 4: with the TMA
 // compare inlined as well, U = 8 spills) for a requester with ids beyond 18 bits.
-template <int U, bool PACKED>
+template <int U, bool PACKED, class RG = RoutedPackedRing>
 static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   static int occ[kMaxRanks + 1] = {0};
-  const size_t smem = routed_smem_bytes(a.nranks, PACKED);
+  const size_t smem = routed_smem_bytes<RG>(a.nranks, PACKED);
+  auto kern = k_walk_routed<kWalkNT, U, PACKED, RG>;
   if (!occ[a.nranks]) {
-    cudaFuncSetAttribute(k_walk_routed<kWalkNT, U, PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], k_walk_routed<kWalkNT, U, PACKED>, kWalkNT, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], kern, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
   }
-  k_walk_routed<kWalkNT, U, PACKED><<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
+  kern<<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
-  if (a.nranks > 1) return walk_routed_variant<4, true>(v, a, num_sms, s);
+  if (a.nranks > 1) {
+    // remote-query ring (TM_ROUTED_RING = stages x positions per stage; tuning knob)
+    static const int ring = [] {
+      const char *e = getenv("TM_ROUTED_RING");
+      return e ? atoi(e) : 0;
+    }();
+    switch (ring) {
+      case 1: return walk_routed_variant<4, true, PackedRing<8, 1024>>(v, a, num_sms, s);
+      case 2: return walk_routed_variant<4, true, PackedRing<4, 2048>>(v, a, num_sms, s);
+      case 3: return walk_routed_variant<4, true, PackedRing<6, 1024>>(v, a, num_sms, s);
+      default: return walk_routed_variant<4, true>(v, a, num_sms, s);
+    }
+  }
   return walk_routed_variant<kWalkU, false>(v, a, num_sms, s);
 }
 }  // namespace tms

@@ -2,6 +2,7 @@
 // hot kernels (K1 prefix-match walk, K2 record/commit, K3 trajectory assembly).
 // sm_100a; integer and HBM-bound — no tensor cores.  See DESIGN.md.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -97,6 +98,24 @@ struct Sched {
 // Routing descriptor at the start of every rank's IPC-shared region (byte offsets are
 // relative to the region base; arrays hold the rank's query batch and its results).
 constexpr int kMaxRanks = 16;
+// The header fields tm_route_prepare sets (k_route writes them into the
+// region: no host-to-device copy per batch); RouteDesc starts with the same members.
+struct RouteHead {
+  int64_t n;        // queries in this rank's batch
+  int64_t sid_off;  // int64 global session id per query
+  int64_t qoff_off; // int64 token offset per query (multiple of 32)
+  int64_t len_off;  // int64 length per query
+  int64_t tok_off;  // int32 tokens
+  int64_t idx_off;  // int32 query indices grouped by owner (written by k_route)
+  int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
+  int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
+  int64_t pkf_off;                  // int32[n+1]: 4096-position pack blocks before each remote query (k_route)
+  int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
+  int32_t rank;                     // the rank whose batch this is (its own queries stay unpacked)
+  int32_t nranks;
+  int32_t pad_;
+};
+
 struct RouteDesc {
   int64_t n;        // queries in this rank's batch
   int64_t sid_off;  // int64 global session id per query
@@ -124,6 +143,8 @@ struct RouteDesc {
   int64_t arrive[kMaxRanks];
   int64_t done[kMaxRanks];
 };
+static_assert(offsetof(RouteDesc, count) == sizeof(RouteHead) && offsetof(RouteDesc, nranks) == offsetof(RouteHead, nranks),
+              "RouteHead must be RouteDesc's prefix");
 
 struct RoutedArgs {
   int nranks, rank;

@@ -54,7 +54,7 @@ cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t 
 cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
 int export_tile_tokens();
-cudaError_t launch_route(char *region, int nranks, cudaStream_t s);
+cudaError_t launch_route(char *region, const RouteHead &head, cudaStream_t s);
 // pack the region's query tokens into its 18-bit planes (RouteDesc::lo_off / hi_off)
 cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s);
 // device-side barriers of the routed match (RoutedArgs::epoch > 0)

@@ -152,6 +152,7 @@ struct tm_store {
   bool pack_pending = false;
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
   bool pack_auto = true;                // TM_H2D_PACK_MIN unset: pack only as the node's sole GPU client
+  double pack_frac = 1.0;               // share of a packed call's tokens that is packed (TM_H2D_PACK_FRAC)
   int local_world = 1;                  // LOCAL_WORLD_SIZE (torchrun) at creation
   int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0,
           c_h2d_bytes = 0;  // token bytes actually copied host->device
@@ -175,8 +176,9 @@ struct tm_store {
   int plan_roots = 0;           // planner also resolves root rows (TM_PLAN_ROOTS=1)
   tms::Sched *sched = nullptr;  // walk scheduler block (self-cleaning)
   bool profile = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[4];
-  size_t ev_used[4] = {0, 0, 0, 0};
+  static constexpr int kProfKinds = 7;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kProfKinds];
+  size_t ev_used[kProfKinds] = {};
 };
 
 namespace {
@@ -278,7 +280,8 @@ void ensure_table(tm_store *s, int64_t entries) {
   cudaFree(ov);
 }
 
-// Bracket a launch with events when profiling (kind: 0 walk, 1 commit, 2 export, 3 plan).
+// Bracket a launch with events when profiling (kind: 0 walk, 1 commit, 2 export, 3 plan,
+// 4 route, 5 route pack, 6 routed wait).
 struct ProfScope {
   tm_store *s;
   int kind;
@@ -513,9 +516,27 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
         for (i++; i < iv.size() && iv[i].first < b; i++) b = std::max(b, iv[i].second);  // overlapping only
         add_pieces(pieces, tokens + a, a, b - a);
       }
-      if (stage_packed(s, pieces, end, d, st)) {
+      // Hybrid split: the tail of the range goes raw, straight from the caller's buffer,
+      // and its DMA starts at once, while the host threads pack the head (TM_H2D_PACK_FRAC
+      // of the tokens).  Packing alone leaves PCIe idle while the host packs; raw alone is
+      // PCIe-bound - the split keeps both busy.
+      size_t k = pieces.size();
+      if (s->pack_frac < 1.0 && !pieces.empty()) {
+        int64_t tot = 0, acc = 0;
+        for (const auto &pc : pieces) tot += pc.len;
+        for (k = 0; k < pieces.size() && acc < (int64_t)(s->pack_frac * (double)tot); k++) acc += pieces[k].len;
+      }
+      int64_t raw_bytes = 0;
+      if (k < pieces.size()) {
+        const int64_t r0 = pieces[k].dst;  // a multiple of 32: no unpacked chunk writes past it
+        raw_bytes = 4 * (end - r0);
+        ck(cudaMemcpyAsync(d + r0, tokens + r0, (size_t)raw_bytes, cudaMemcpyHostToDevice, st), "H2D tokens (raw tail)");
+        pieces.resize(k);
+      }
+      if (pieces.empty() || stage_packed(s, pieces, pieces.empty() ? 0 : pieces.back().dst + pieces.back().len, d, st)) {
         s->c_pack_calls++;
         s->c_pack_tokens += ntok;
+        s->c_h2d_bytes += raw_bytes;
         return;
       }
       s->c_pack_fallbacks++;
@@ -679,6 +700,7 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
     s->pack_min = atoll(e);
     s->pack_auto = false;
   }
+  if (const char *e = getenv("TM_H2D_PACK_FRAC")) s->pack_frac = std::min(1.0, std::max(0.0, atof(e)));
   if (const char *e = getenv("LOCAL_WORLD_SIZE")) s->local_world = std::max(1, atoi(e));
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
@@ -732,7 +754,7 @@ int tm_store_destroy(tm_store *s) {
     cudaEventDestroy(sl.done);
     if (sl.sched) cudaFree(sl.sched);
   }
-  for (int k = 0; k < 4; k++)
+  for (int k = 0; k < tm_store::kProfKinds; k++)
     for (auto &e : s->ev[k]) {
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);
@@ -1396,10 +1418,10 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
-    tms::RouteDesc d{};  // counts are (re)written by k_route
+    tms::RouteHead d{};  // counts are (re)written by k_route
     d.rank = rank;
     d.nranks = nranks;
-    if (offsets[0] < (int64_t)sizeof(d)) fail(TM_EINVAL, "routing arrays overlap the RouteDesc header");
+    if (offsets[0] < (int64_t)sizeof(tms::RouteDesc)) fail(TM_EINVAL, "routing arrays overlap the RouteDesc header");
     d.n = n;
     d.sid_off = offsets[0];
     d.qoff_off = offsets[1];
@@ -1419,10 +1441,14 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
     d.hi_off = packed ? offsets[9] : 0;
     d.pkf_off = packed ? offsets[10] : 0;
     d.pk_bad = 0;
-    // pageable source: the copy is staged before this call returns
-    ck(cudaMemcpyAsync(region, &d, offsetof(tms::RouteDesc, count), cudaMemcpyHostToDevice, st), "H2D route desc");
-    ck(tms::launch_route((char *)region, nranks, st), "route");
-    if (packed) ck(tms::launch_route_pack((char *)region, n, st), "route pack");
+    {
+      ProfScope ps(s, 4, st);
+      ck(tms::launch_route((char *)region, d, st), "route");
+    }
+    if (packed) {
+      ProfScope ps(s, 5, st);
+      ck(tms::launch_route_pack((char *)region, n, st), "route pack");
+    }
   });
 }
 
@@ -1461,7 +1487,10 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
       ProfScope ps(s, 0, st);
       ck(tms::launch_walk_routed(s->v, a, s->num_sms, st), "walk_routed");
     }
-    if (epoch > 0) ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
+    if (epoch > 0) {
+      ProfScope ps(s, 6, st);
+      ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
+    }
     ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
     slot->used = true;
   });
@@ -1598,13 +1627,13 @@ int tm_store_load(tm_store *s, const char *path) {
 int tm_profile_begin(tm_store *s) {
   return guarded(s, [&] {
     s->profile = true;
-    for (int k = 0; k < 4; k++) s->ev_used[k] = 0;
+    for (int k = 0; k < tm_store::kProfKinds; k++) s->ev_used[k] = 0;
   });
 }
 
 int tm_profile_end(tm_store *s, int32_t kind, double *total_ms, int64_t *launches) {
   return guarded(s, [&] {
-    if (kind < 0 || kind > 3) fail(TM_EINVAL, "bad kernel kind");
+    if (kind < 0 || kind >= tm_store::kProfKinds) fail(TM_EINVAL, "bad kernel kind");
     double t = 0;
     for (size_t i = 0; i < s->ev_used[kind]; i++) {
       ck(cudaEventSynchronize(s->ev[kind][i].second), "event sync");

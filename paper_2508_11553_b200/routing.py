@@ -9,7 +9,7 @@ the owner's store — no collective.  GPU-originated batches (config 5: each ran
 batch of queries in HBM for sessions owned anywhere) use ``Router.match``:
 
 1. ``tm_route_prepare`` buckets the local batch by owner inside this rank's IPC-shared
-   region;
+   region and packs the tokens of the queries other ranks own into 18-bit planes;
 2. a cross-rank barrier;
 3. every owner's K1 kernel reads its queries directly from the requesters' regions over
    NVLink (P2P loads) and writes matched / parent / dup back into them (P2P stores) —
@@ -111,6 +111,7 @@ class Router:
             self.peers.append(out.value)
         self._peer_arr = (C.c_void_p * self.nranks)(*self.peers)
         self._off_arr = (C.c_int64 * 11)(*self.offsets)
+        self._off_arr_raw = (C.c_int64 * 11)(*self.offsets[:8], 0, 0, 0)  # no 18-bit planes
         dev = torch.device("cuda", store.device)
         view = lambda i, n, ts, dt: torch.as_tensor(_CudaArray(self.base + self.offsets[i], (n,), ts), device=dev)  # noqa: E731
         self.gsid = view(0, n_max, "<i8", None)
@@ -168,7 +169,7 @@ class Router:
         st = torch.cuda.current_stream(self.store.device).cuda_stream
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
-        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, self.rank, st))
+        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr_raw, self.nranks, self.rank, st))
         cnt = np.zeros(16, np.int32)
         check(lib.tm_route_counts(h, C.c_void_p(self.base), cnt.ctypes.data_as(C.c_void_p), st))
         counts = cnt[: self.nranks].astype(np.int64)

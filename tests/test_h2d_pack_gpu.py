@@ -17,18 +17,22 @@ from workloads import pack_records
 pytestmark = pytest.mark.gpu
 
 
-def _store(pack_min):
+def _store(pack_min, frac=None):
     from paper_2508_11553_b200 import DeviceStore
 
-    old = os.environ.get("TM_H2D_PACK_MIN")
-    os.environ["TM_H2D_PACK_MIN"] = str(pack_min)
+    env = {"TM_H2D_PACK_MIN": str(pack_min)}
+    if frac is not None:
+        env["TM_H2D_PACK_FRAC"] = str(frac)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         return DeviceStore(0)
     finally:
-        if old is None:
-            os.environ.pop("TM_H2D_PACK_MIN")
-        else:
-            os.environ["TM_H2D_PACK_MIN"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
 
 
 def _sessions(rng, n_sess, n_ins, vocab, max_new):
@@ -174,3 +178,29 @@ def test_auto_policy_stays_raw_with_several_gpu_clients():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.37, 0.8])
+def test_hybrid_split_packed_head_raw_tail(frac):
+    """TM_H2D_PACK_FRAC < 1: the head of an aligned call's token range is packed, the tail
+    goes raw from the caller's buffer in the same call; results equal the raw copy's."""
+    rng = np.random.default_rng(23)
+    sids, seqs = _sessions(rng, 16, 300, _small_ids, 1500)
+    hyb, raw = _store(0, frac), _store(-1)
+    try:
+        rh, mh, eh = _record_and_match(hyb, sids, seqs, 32)
+        rr, mr, er = _record_and_match(raw, sids, seqs, 32)
+        for f in ("matched", "local", "parent_local", "added"):
+            assert np.array_equal(getattr(rh, f), getattr(rr, f)), f
+        for a, b in zip(mh, mr):
+            assert np.array_equal(a, b)
+        for f in ("offsets", "tokens", "loss_mask", "versions", "resp_start"):
+            assert np.array_equal(getattr(eh, f), getattr(er, f)), f
+        h = hyb.h2d_stats()
+        assert h["pack_fallbacks"] == 0 and h["packed_calls"] == 2
+        total = 2 * sum(len(q) for q in seqs)
+        # fewer PCIe bytes than raw unless nothing is packed
+        assert (h["token_bytes"] < 4 * total) == (frac > 0)
+    finally:
+        hyb.close()
+        raw.close()
