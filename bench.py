@@ -219,6 +219,9 @@ def python_reference_sample(wl, nq=64):
                       "cores would give at most cores x this"}
 
 
+LINK_PEAK = 670.0  # GB/s per GPU, SM peer reads with both directions busy (tools/p2p_probe)
+
+
 def run_c5(args):
     """Config 5: 1M sessions (log-uniform 1k-128k tokens) sharded by session hash; every
     rank originates 4096 queries for sessions owned anywhere; Router.match routes them
@@ -297,6 +300,7 @@ def run_c5(args):
     dist.all_reduce(stats)
     toks, remote_toks = float(stats[0]), float(stats[1])
     value = world * wl.n_queries * args.steps / elapsed
+    wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
     peak, peak_kind = peaks()
     per_gpu_alg = 8.0 * toks / world  # HBM+link bytes per rank per batch (average)
     line = {
@@ -315,18 +319,24 @@ def run_c5(args):
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,
         "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * args.steps / elapsed / 1e9,
+        # bytes that actually cross the links: remote queries move as 18-bit planes (2.25 B per
+        # compared position) unless the exchange is the NCCL baseline (int32)
+        "nvlink_wire_bytes_per_position": wire_b,
+        "nvlink_wire_GBps_per_rank": wire_b * remote_toks / world * args.steps / elapsed / 1e9,
         "routed_walk_ms_avg_rank0": walk_ms / max(walk_n, 1),
         "phase_ms_avg_rank0": {k: (ms / n if n else 0.0) for k, (ms, n) in phase_ms.items()},
         "nvlink_query_GBps_during_walk_rank0": 4.0 * remote_toks / world / (walk_ms / max(walk_n, 1)) / 1e6,
         "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
-                     "achieved": (4.0 * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
-                     "peak": 770.0 if world > 1 else peak, "unit": "GB/s",
-                     "frac": ((4.0 * remote_toks / world) / 770.0 if world > 1 else per_gpu_alg / peak)
+                     "achieved": (wire_b * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
+                     "peak": LINK_PEAK if world > 1 else peak, "unit": "GB/s",
+                     "frac": ((wire_b * remote_toks / world) / LINK_PEAK if world > 1 else per_gpu_alg / peak)
                      * args.steps / elapsed / 1e9,
-                     "peak_kind": "measured peer copy per direction (B200_PROFILING.md)" if world > 1 else peak_kind,
+                     "peak_kind": "measured SM peer reads per GPU with both directions busy (tools/p2p_probe)"
+                     if world > 1 else peak_kind,
                      "traffic": None,
-                     "note": "N>1: remote query bytes cross NVLink (tools/p2p_probe: SM peer reads 780 GB/s one "
-                             "direction, 670 GB/s both directions at once); history bytes come from local HBM"},
+                     "note": "N>1: achieved = bytes on the wire (remote compared positions x nvlink_wire_bytes_per_"
+                             "position) over the whole step; history bytes come from local HBM (tools/p2p_probe: SM "
+                             "peer reads 780 GB/s one direction, 670 GB/s per GPU both directions at once)"},
         # ours per batch: k_route + k_walk_routed (+ k_route_pack with peers, + k_route_arrive +
         # k_route_wait_done with device barriers)
         "gpu_launches": args.steps * ((4 if args.routing == "fused" else 2) + (1 if world > 1 and
@@ -449,6 +459,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(t.item())
     value = world * wl.n_queries * args.steps / elapsed
+    wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
     toks_per_s = world * float(cq.sum()) * args.steps / elapsed
 
     # e2e: the public host-buffer API, pinned inputs, copies inside the timed region
