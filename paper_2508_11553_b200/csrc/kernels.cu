@@ -638,15 +638,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
   __shared__ int s_nloc;  // cells in the local queue
   const int np = a.nranks;
   const int ncell = kPlanNB * np;
-  // PACKED: TMA-staged compare for remote queries, bulk copies pull the query's 18-bit
-  // planes over NVLink (2.25 B per position instead of 4).  One rank (RG = Ring): the
-  // TMA-staged int32 compare of k_walk_tma for the local queries.
-  constexpr bool LTMA = !PACKED && !std::is_same<RG, NoRing>::value;
-  constexpr bool RING = PACKED || LTMA;
-  RG *rg = RING ? reinterpret_cast<RG *>(dyn) : nullptr;
+  // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
+  // over NVLink (2.25 B per position instead of 4)
+  RG *rg = PACKED ? reinterpret_cast<RG *>(dyn) : nullptr;
   if constexpr (PACKED) packed_ring_init(*rg);
-  if constexpr (LTMA) tma_ring_init(*rg);
-  int *s_pre = reinterpret_cast<int *>(dyn + (RING ? (sizeof(RG) + 15) / 16 * 16 : 0));  // ncell + 2
+  int *s_pre = reinterpret_cast<int *>(dyn + (PACKED ? (sizeof(RG) + 15) / 16 * 16 : 0));  // ncell + 2
   int *s_bs = s_pre + ncell + 2;
   int *s_peer = s_bs + ncell;
   RouteDesc *own = reinterpret_cast<RouteDesc *>(const_cast<char *>(a.peer[a.rank]));
@@ -736,11 +732,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v,
         packed_q = true;
       }
     }
-    if constexpr (LTMA) {
-      walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg);
-    } else {
-      if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // local (or ids beyond 18 bits): int32, registers
-    }
+    if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // local (or ids beyond 18 bits): int32, registers
   }
 }
 
@@ -1738,7 +1730,7 @@ cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaSt
 template <int U, bool PACKED, class RG = RoutedPackedRing>
 static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   static int occ[kMaxRanks + 1] = {0};
-  const size_t smem = routed_smem_bytes<RG>(a.nranks, PACKED || !std::is_same<RG, NoRing>::value);
+  const size_t smem = routed_smem_bytes<RG>(a.nranks, PACKED);
   auto kern = k_walk_routed<kWalkNT, U, PACKED, RG>;
   if (!occ[a.nranks]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1763,12 +1755,8 @@ cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sm
       default: return walk_routed_variant<4, true>(v, a, num_sms, s);
     }
   }
-  // one rank: TMA-staged int32 compare (TM_ROUTED_LOCAL=regs: the register path)
-  static const bool regs = [] {
-    const char *e = getenv("TM_ROUTED_LOCAL");
-    return e && !strcmp(e, "regs");
-  }();
-  if (regs) return walk_routed_variant<kWalkU, false, NoRing>(v, a, num_sms, s);
-  return walk_routed_variant<8, false, Ring>(v, a, num_sms, s);
+  // one rank: the register path (the TMA-staged int32 compare measured 6 % slower here:
+  // 25.0-25.2 vs 26.7 M q/s on c5 at N=1)
+  return walk_routed_variant<kWalkU, false>(v, a, num_sms, s);
 }
 }  // namespace tms
