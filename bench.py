@@ -55,6 +55,9 @@ def parse():
                     help="c4 (default): per-rank 10k x 32k shard, host-routed; c5: 1M-session store sharded "
                          "by session hash with GPU-originated batches routed over NVLink (fused P2P K1)")
     ap.add_argument("--c5-sessions", type=int, default=1_000_000)
+    ap.add_argument("--pipeline", action=argparse.BooleanOptionalAction, default=True,
+                    help="c5, N>1, fused routing: two routing regions, batch k+1 bucketed + packed while batch k "
+                         "is matched (--no-pipeline: one region, batches back to back)")
     ap.add_argument("--routing", default="fused", choices=["fused", "fused-nccl-barrier", "nccl"],
                     help="c5 exchange: fused P2P K1 (product) or NCCL all-to-all + local match (baseline)")
     ap.add_argument("--mixed", default=None,
@@ -252,14 +255,29 @@ def run_c5(args):
     dist.all_reduce(tok_need, op=dist.ReduceOp.MAX)
     router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
     wl.fill_queries(router)
+    routers = [router]
+    if args.pipeline and world > 1 and args.routing == "fused":
+        # a second region: the next batch is bucketed + packed while this one is matched
+        routers.append(Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()),
+                              g2l=wl.g2l))
+        wl.fill_queries(routers[1])
     torch.cuda.synchronize()
-    route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
-             "nccl": router.match_nccl}[args.routing]
-    for _ in range(max(3, args.warmup)):
-        route(wl.n_queries)
+    if len(routers) > 1:
+        from paper_2508_11553_b200.routing import match_pipelined
+
+        side = torch.cuda.Stream(dev)
+        run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side)  # noqa: E731
+    else:
+        route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
+                 "nccl": router.match_nccl}[args.routing]
+
+        def run_batches(k):
+            for _ in range(k):
+                route(wl.n_queries)
+    run_batches(max(3, args.warmup))
     torch.cuda.synchronize()
-    m = router.out_matched[: wl.n_queries].cpu().numpy()
-    bad = np.flatnonzero(m != wl.q_depth)
+    m = np.concatenate([r.out_matched[: wl.n_queries].cpu().numpy() for r in routers])
+    bad = np.flatnonzero(m != np.tile(wl.q_depth, len(routers))) % wl.n_queries
     if len(bad):
         print(f"rank {rank}: {len(bad)} mismatches, e.g.", [(int(i), int(m[i]), int(wl.q_depth[i]), int(wl.lens[wl.q_g[i]]),
               int(wl.q_g[i]), int(wl.owner[wl.q_g[i]])) for i in bad[:8]], file=sys.stderr)
@@ -274,8 +292,7 @@ def run_c5(args):
         t_wall = time.perf_counter()
         store.profile_begin()
         e0.record(stream)
-        for _ in range(args.steps):
-            route(wl.n_queries)
+        run_batches(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
@@ -286,8 +303,7 @@ def run_c5(args):
         per = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev, dtype=torch.float64)
         dist.all_reduce(left, op=dist.ReduceOp.MAX)
         dist.all_reduce(per, op=dist.ReduceOp.MAX)
-        for _ in range(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1):
-            route(wl.n_queries)
+        run_batches(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1)
         torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
@@ -315,6 +331,7 @@ def run_c5(args):
                                "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
                                "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
                                    args.routing],
+                   "pipelined": len(routers) > 1,
                    "cross_shard_frac": float(remote.mean()), "shard_build_s": build_s,
                    "arena_GB_per_rank": owned_tokens * 4 / 1e9},
         "tokens_compared_per_s": toks * args.steps / elapsed,
@@ -345,7 +362,8 @@ def run_c5(args):
     }
     if rank == 0:
         print(json.dumps(line))
-    router.close()
+    for r in routers:
+        r.close()
     store.close()
     dist.destroy_process_group()
 

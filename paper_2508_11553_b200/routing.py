@@ -136,21 +136,35 @@ class Router:
         against their owners' shards; results land in out_matched / out_parent / out_dup.
         Enqueued on torch's current stream.  Collective: every rank calls it once per
         batch, in the same order and with the same ``sync``."""
+        if sync not in ("nccl", "device"):
+            raise ValueError(f"unknown sync mode {sync!r}")
+        self.prepare(n)
+        self.match_prepared(sync)
+
+    def prepare(self, n: int, stream=None):
+        """Bucket the staged batch by owner and pack its remote queries (tm_route_prepare),
+        on ``stream`` (default: torch's current stream).  Local to this rank."""
         import torch
 
         if n > self.n_max:
             raise ValueError("batch larger than the routing region")
+        st = (stream or torch.cuda.current_stream(self.store.device)).cuda_stream
+        st = C.c_void_p(1 if st == 0 else st)
+        check(self.store.lib.tm_route_prepare(self.store.h, C.c_void_p(self.base), n, self._off_arr, self.nranks,
+                                              self.rank, st))
+
+    def match_prepared(self, sync: str = "device"):
+        """The exchange + match of a prepared batch on torch's current stream (collective)."""
+        import torch
+
         st = torch.cuda.current_stream(self.store.device).cuda_stream
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
         g2l = C.c_void_p(self.g2l.data_ptr())
-        check(lib.tm_route_prepare(h, C.c_void_p(self.base), n, self._off_arr, self.nranks, self.rank, st))
         if sync == "device" and self.nranks > 1:
             self._epoch += 1
             check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self._epoch, st))
             return
-        if sync not in ("nccl", "device"):
-            raise ValueError(f"unknown sync mode {sync!r}")
         if self.nranks > 1:
             self._barrier()
         check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, g2l, st))
@@ -217,3 +231,35 @@ class Router:
         if self.base:
             lib.tm_shared_free(h, C.c_void_p(self.base))
             self.base = None
+
+
+def match_pipelined(routers, n: int, batches: int, side_stream=None):
+    """Run ``batches`` routed batches alternating between routers (separate regions, the
+    same staged queries or different ones): batch i+1 is bucketed and packed on a side
+    stream while batch i is exchanged and matched on torch's current stream, so the pack
+    of one batch hides under the NVLink-bound walk of the previous one.  Batch i's results
+    are in routers[i % len(routers)].  Collective like Router.match (device barriers)."""
+    import torch
+
+    main = torch.cuda.current_stream(routers[0].store.device)
+    side = side_stream or torch.cuda.Stream(routers[0].store.device)
+    k = len(routers)
+    prepared = [torch.cuda.Event() for _ in range(k)]
+    done = [None] * k
+
+    def prep(i):
+        b = i % k
+        if done[b] is not None:
+            side.wait_event(done[b])  # the owners are finished with this region's last batch
+        routers[b].prepare(n, stream=side)
+        prepared[b].record(side)
+
+    prep(0)
+    for i in range(batches):
+        b = i % k
+        main.wait_event(prepared[b])
+        routers[b].match_prepared("device")
+        done[b] = torch.cuda.Event()
+        done[b].record(main)
+        if i + 1 < batches:
+            prep(i + 1)

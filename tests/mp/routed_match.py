@@ -56,6 +56,21 @@ router.match_nccl(wl.n_queries)
 torch.cuda.synchronize()
 ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
 ok = ok and np.array_equal(router.out_parent[: wl.n_queries].cpu().numpy(), par)
+# pipelined: two regions, batch i+1 bucketed + packed on a side stream while batch i matches
+from paper_2508_11553_b200.routing import match_pipelined  # noqa: E402
+
+router2 = Router(store, dist.group.WORLD, n_max=wl.n_queries, tokens_max=int(need.item()), g2l=wl.g2l)
+wl.fill_queries(router2)
+for r in (router, router2):
+    r.out_matched.fill_(-7)
+torch.cuda.synchronize()
+match_pipelined([router, router2], wl.n_queries, 5)
+torch.cuda.synchronize()
+store.synchronize()
+for r in (router, router2):
+    ok = ok and np.array_equal(r.out_matched[: wl.n_queries].cpu().numpy(), m)
+    ok = ok and np.array_equal(r.out_parent[: wl.n_queries].cpu().numpy(), par)
+router2.close()
 remote = float(np.mean(wl.owner[wl.q_g] != rank))
 flag = torch.tensor([1 if ok else 0], device=dev)
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
