@@ -599,8 +599,7 @@ __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int
 
 // tm_route_prepare with peers: every CTA packs one contiguous range of blocks (one
 // binary search for its first query, then it steps through the queries in order)
-template <int NT>
-__global__ void __launch_bounds__(NT) k_route_pack(char *region) {
+__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
   const PackView w = pack_view(region);
   const int64_t per = (w.nblk + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = min(w.nblk, b0 + per);
@@ -614,7 +613,7 @@ __global__ void __launch_bounds__(NT) k_route_pack(char *region) {
   unsigned bad = 0;
   for (int64_t blk = b0; blk < b1; blk++) {
     while (blk >= bn) { j++; bj = bn; bn = w.pkf[j + 1]; }
-    bad |= pack_block<NT>(w, j, bj, blk);
+    bad |= pack_block<kPackNT>(w, j, bj, blk);
   }
   if (bad) atomicOr(&reinterpret_cast<RouteDesc *>(region)->pk_bad, 1);
 }
@@ -1706,18 +1705,7 @@ int export_tile_tokens() { return kExportTile; }
 
 cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
   if (n < 1) return cudaSuccess;
-  // TM_ROUTE_PACK_CTAS / TM_ROUTE_PACK_NT (256 or 64): small CTAs fit beside a running
-  // walk's CTAs, so a pipelined pack of the next batch can start before the walk drains
-  static const int nt = [] {
-    const char *e = getenv("TM_ROUTE_PACK_NT");
-    return e && atoi(e) == 64 ? 64 : kPackNT;
-  }();
-  static const int ctas = [] {
-    const char *e = getenv("TM_ROUTE_PACK_CTAS");
-    return e ? std::max(1, atoi(e)) : 148 * 8;
-  }();
-  if (nt == 64) k_route_pack<64><<<ctas, 64, 0, s>>>(region);
-  else k_route_pack<kPackNT><<<ctas, kPackNT, 0, s>>>(region);
+  k_route_pack<<<148 * 8, kPackNT, 0, s>>>(region);
   return cudaGetLastError();
 }
 
@@ -1748,8 +1736,6 @@ static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, in
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], kern, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
-    // TM_ROUTED_OCC caps the CTAs per SM (room for a pipelined pack of the next batch)
-    if (const char *e = getenv("TM_ROUTED_OCC")) occ[a.nranks] = std::max(1, std::min(occ[a.nranks], atoi(e)));
   }
   kern<<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
