@@ -1755,10 +1755,8 @@ cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sm
       default: return walk_routed_variant<4, true>(v, a, num_sms, s);
     }
   }
-  // one rank: the register path (the TMA-staged int32 compare measured 6 % slower here:
-  // 25.0-25.2 vs 26.7 M q/s on c5 at N=1)
-  static const bool u4 = getenv("TM_ROUTED_U4") != nullptr;  // tuning: 4 int4 per thread per stream (no spills)
-  if (u4) return walk_routed_variant<4, false>(v, a, num_sms, s);
+  // one rank: the register path with U = 8 (the TMA-staged int32 compare measured 6 % slower
+  // here, 25.0-25.2 vs 26.7 M q/s on c5 at N=1; U = 4, which does not spill, 24.3 vs 26.6)
   return walk_routed_variant<kWalkU, false>(v, a, num_sms, s);
 }
 }  // namespace tms

@@ -56,6 +56,19 @@ router.match_nccl(wl.n_queries)
 torch.cuda.synchronize()
 ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), m)
 ok = ok and np.array_equal(router.out_parent[: wl.n_queries].cpu().numpy(), par)
+# ragged edge cases: empty, one-token, sub-group and group-straddling queries (the pack skips
+# empty queries and zero-fills partial 32-position groups); truth = min(length, depth)
+short = np.array(wl.q_len, np.int64)
+sel = np.arange(0, wl.n_queries, 7)
+short[sel] = np.resize(np.array([0, 1, 5, 31, 33, 4097], np.int64), len(sel))
+short = np.minimum(short, wl.q_len)
+router.qlen[: wl.n_queries].copy_(torch.as_tensor(short, device=dev))
+for sync in ("device", "nccl"):
+    router.out_matched.fill_(-7)
+    router.match(wl.n_queries, sync=sync)
+    torch.cuda.synchronize()
+    ok = ok and np.array_equal(router.out_matched[: wl.n_queries].cpu().numpy(), np.minimum(short, wl.q_depth))
+router.qlen[: wl.n_queries].copy_(torch.as_tensor(wl.q_len, device=dev))
 # pipelined: two regions, batch i+1 bucketed + packed on a side stream while batch i matches
 from paper_2508_11553_b200.routing import match_pipelined  # noqa: E402
 

@@ -8,5 +8,4 @@ python bench.py --workload c5 --steps 20 > gpurun_out/e_c5_n1.json 2> gpurun_out
 python tools/route_pack_probe.py > gpurun_out/e_pack_probe.txt 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_route" -s 6 -c 2 -o gpurun_out/e_route python tools/route_pack_probe.py > gpurun_out/e_route_ncu.log 2>&1
 python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/e_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/e_c4_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
 
-TM_ROUTED_U4=1 python bench.py --workload c5 --steps 20 > gpurun_out/e_c5_n1_u4.json 2> gpurun_out/e_c5_n1_u4.err
 echo done
