@@ -19,7 +19,9 @@ batch of queries in HBM for sessions owned anywhere) use ``Router.match``:
 By default (``sync="device"``, ``tm_match_routed_sync``) both barriers are epoch flags
 in the region headers written and polled by the kernels themselves over NVLink — no
 collective library call per batch.  ``sync="nccl"`` (``tm_match_routed``) brackets the
-kernel with one-element NCCL all-reduces instead.  PyTorch provides the process group
+kernel with one-element NCCL all-reduces instead.  ``match_pipelined`` runs a stream of
+batches over two regions: batch k+1 is bucketed and packed on a side stream while batch k
+is exchanged and matched.  PyTorch provides the process group
 (setup plumbing: the IPC handle exchange); routing and matching run in the CUDA kernels
 behind include/tmstore.h.
 """
