@@ -629,8 +629,8 @@ __host__ __device__ constexpr size_t routed_smem_bytes(int nranks, bool packed) 
   return (packed ? (sizeof(RG) + 15) / 16 * 16 : 0) + sizeof(int) * (3 * (size_t)kPlanNB * nranks + 2);
 }
 
-template <int NT, int U, bool PACKED, class RG = RoutedPackedRing>
-__global__ void __launch_bounds__(NT, NT == 64 ? 6 : 1) k_walk_routed(DevView v, RoutedArgs a) {
+template <int NT, int U, bool PACKED, class RG = RoutedPackedRing, int MINB = 6>
+__global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView v, RoutedArgs a) {
   extern __shared__ __align__(16) char dyn[];
   __shared__ WalkShared sh;
   __shared__ long long s_item;
@@ -1727,15 +1727,21 @@ cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaSt
 // One rank (no peers): the register-path kernel (U = 8).  Peers: the packed TMA compare for
 // every query whose requester packed its planes, the register path (U = 4: with the TMA
 // compare inlined as well, U = 8 spills) for a requester with ids beyond 18 bits.
-template <int U, bool PACKED, class RG = RoutedPackedRing>
+// With peers the walk is compiled for <= 128 registers (8 CTAs' worth) but launched with 6
+// CTAs per SM: the registers left over hold one 256-thread k_route_pack CTA per SM, so the
+// next batch's pack (match_pipelined) runs beside the walk instead of after it
+// (N=2: 27.1 -> 28.8 M q/s; the walk itself is as fast as with 147 registers).
+constexpr int kRoutedCtasPerSm = 6;
+template <int U, bool PACKED, class RG = RoutedPackedRing, int MINB = 6>
 static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   static int occ[kMaxRanks + 1] = {0};
   const size_t smem = routed_smem_bytes<RG>(a.nranks, PACKED);
-  auto kern = k_walk_routed<kWalkNT, U, PACKED, RG>;
+  auto kern = k_walk_routed<kWalkNT, U, PACKED, RG, MINB>;
   if (!occ[a.nranks]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], kern, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
+    if (PACKED) occ[a.nranks] = std::min(occ[a.nranks], kRoutedCtasPerSm);
   }
   kern<<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();
@@ -1752,7 +1758,7 @@ cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sm
       case 1: return walk_routed_variant<4, true, PackedRing<8, 1024>>(v, a, num_sms, s);
       case 2: return walk_routed_variant<4, true, PackedRing<4, 2048>>(v, a, num_sms, s);
       case 3: return walk_routed_variant<4, true, PackedRing<6, 1024>>(v, a, num_sms, s);
-      default: return walk_routed_variant<4, true>(v, a, num_sms, s);
+      default: return walk_routed_variant<4, true, RoutedPackedRing, 8>(v, a, num_sms, s);
     }
   }
   // one rank: the register path with U = 8 (the TMA-staged int32 compare measured 6 % slower
