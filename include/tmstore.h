@@ -168,9 +168,12 @@ int tm_store_stream(tm_store *store, void **out_stream);
  * Every rank publishes its query batch in a shared device region laid out as
  *   [RouteDesc header | int64 gsid[n] | int64 tok_off[n] | int64 len[n] | int32 tokens |
  *    int32 idx[n] | int64 out_matched[n] | int64 out_parent[n] | int64 out_dup[n] |
- *    uint16 low plane[tokens + 128] | uint8 high plane[(tokens + 128) / 4] | int32 pk[n + 1]]
- * (offsets[11] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup, lo,
- * hi, pk; lo = hi = pk = 0: no planes).  tm_route_prepare writes the header, buckets the batch by
+ *    uint16 low plane[tokens + 128] | uint8 high plane[(tokens + 128) / 4] | int32 pk[n + 1] |
+ *    32-byte query records[n]]
+ * (offsets[12] = byte offsets of those arrays: sid, qoff, len, tok, idx, m, par, dup, lo,
+ * hi, pk, rec; lo = hi = pk = rec = 0: no planes.  The pack writes each remote query's
+ * record - gsid, offset, length, index, first token - at its idx position, so an owner
+ * starts it with one load instead of three dependent ones).  tm_route_prepare writes the header, buckets the batch by
  * owner rank (owner = splitmix64(gsid) mod nranks) and, with peers, packs the tokens of the
  * queries owned by OTHER ranks (this is `rank`) into the 18-bit planes (hostpack.h layout;
  * TM_ROUTE_PACK=0 disables) so remote owners move 2.25 B per compared position over NVLink

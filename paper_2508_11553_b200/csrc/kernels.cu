@@ -95,7 +95,7 @@ using RoutedPackedRing = PackedRing<kTmaStages, kPackedChunk>;
 template <int NT, int U, class R = NoRing>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
                                            WalkOut o, WalkShared &sh, R *rg = nullptr,
-                                           const PackedQuery *pk = nullptr) {
+                                           const PackedQuery *pk = nullptr, const int32_t *q0 = nullptr) {
   // A session with a path copy (a long turn-by-turn chain): compare the query against the
   // copy in one streaming segment, then resume the walk at the row that owns the last
   // matched position - exactly the state the hop-by-hop walk would reach there (every
@@ -108,7 +108,7 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
       r = *root_hint;
     } else if (L > 0) {
       const int64_t pc = v.s_pc_row[sid];  // in flight with the root probe
-      r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q[0], false));
+      r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q0 ? *q0 : q[0], false));  // q0: known first token
       if (pc >= 0 && r >= 0) {
         sh.pc_vb = v.s_pc_vb[sid];
         sh.pc_len = min(L, v.row_len[pc]);
@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head
   __shared__ int wsum[kRouteNT / 32];
   for (int i = threadIdx.x; i < NC; i += kRouteNT) cnt[i] = 0;
   __syncthreads();
-  auto load_keys = [&](int64_t c0, int key[kRouteU], int64_t L[kRouteU]) {
-    int64_t g[kRouteU];
+  auto load_keys = [&](int64_t c0, int key[kRouteU], int64_t L[kRouteU], int64_t g[kRouteU]) {
 #pragma unroll
     for (int u = 0; u < kRouteU; u++) {
       const int64_t i = c0 + u * kRouteNT + threadIdx.x;
@@ -361,8 +360,8 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head
   };
   for (int64_t c0 = 0; c0 < n; c0 += CH) {
     int key[kRouteU];
-    int64_t L[kRouteU];
-    load_keys(c0, key, L);
+    int64_t L[kRouteU], g[kRouteU];
+    load_keys(c0, key, L, g);
 #pragma unroll
     for (int u = 0; u < kRouteU; u++)
       if (c0 + u * kRouteNT + threadIdx.x < n) atomicAdd(&cnt[key[u]], 1);
@@ -411,16 +410,19 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head
   const int own0 = s_own0, nown = s_nown;
   for (int64_t c0 = 0; c0 < n; c0 += CH) {
     int key[kRouteU];
-    int64_t L[kRouteU];
-    load_keys(c0, key, L);
+    int64_t L[kRouteU], g[kRouteU];
+    load_keys(c0, key, L, g);
 #pragma unroll
     for (int u = 0; u < kRouteU; u++) {
       const int64_t i = c0 + u * kRouteNT + threadIdx.x;
       if (i >= n) continue;
       const int pos = atomicAdd(&cnt[key[u]], 1);
       idx[pos] = (int32_t)i;
-      if (pk && key[u] / kPlanNB != head.rank)
+      if (pk && key[u] / kPlanNB != head.rank) {
         pkf[pos < own0 ? pos : pos - nown] = (int)((L[u] + kPackBlock - 1) / kPackBlock);
+        if (L[u] == 0 && head.rec_off)  // no block to pack: its record is written here
+          reinterpret_cast<RouteRec *>(region + head.rec_off)[pos] = RouteRec{g[u], 0, 0, (int32_t)i, 0, 0};
+      }
     }
   }
   if (!pk) return;
@@ -525,7 +527,8 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 // (the owners then read the int32 tokens instead).
 constexpr int kPackNT = 256;
 struct PackView {
-  const int64_t *qoff, *qlen;
+  const int64_t *qoff, *qlen, *gsid;
+  RouteRec *rec;  // or nullptr
   const int32_t *tok, *idx, *pkf;
   uint16_t *plo;
   uint8_t *phi;
@@ -539,6 +542,8 @@ __device__ __forceinline__ PackView pack_view(char *region) {
   w.qlen = reinterpret_cast<const int64_t *>(region + d->len_off);
   w.tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
   w.idx = reinterpret_cast<const int32_t *>(region + d->idx_off);
+  w.gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
+  w.rec = d->rec_off ? reinterpret_cast<RouteRec *>(region + d->rec_off) : nullptr;
   w.pkf = reinterpret_cast<const int32_t *>(region + d->pkf_off);
   w.plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
   w.phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
@@ -552,9 +557,11 @@ __device__ __forceinline__ PackView pack_view(char *region) {
 template <int NT>
 __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int64_t bj, int64_t blk) {
   constexpr int SL = kPackBlock / (8 * NT);  // 8-position slots per thread
-  const int64_t q = w.idx[j < w.own0 ? j : j + w.nown];
+  const int64_t pos = j < w.own0 ? j : j + w.nown;
+  const int64_t q = w.idx[pos];
   const int64_t off = w.qoff[q], len = w.qlen[q];
   const int64_t r0 = (blk - bj) * kPackBlock;
+  const int64_t g = (w.rec && blk == bj && threadIdx.x == 0) ? w.gsid[q] : 0;  // in flight with the tokens
   const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
   int4 a[SL], b[SL];
 #pragma unroll
@@ -571,6 +578,8 @@ __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int
       b[u] = make_int4(t[4], t[5], t[6], t[7]);
     }
   }
+  if (w.rec && blk == bj && threadIdx.x == 0)  // the query's first block: its record
+    w.rec[pos] = RouteRec{g, off, (int32_t)len, (int32_t)q, a[0].x, 0};
   unsigned bad = 0;
 #pragma unroll
   for (int u = 0; u < SL; u++) {
@@ -636,6 +645,8 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
   __shared__ long long s_item;
   __shared__ int s_cell;
   __shared__ int s_nloc;  // cells in the local queue
+  __shared__ RouteRec s_rec;
+  __shared__ bool s_has_rec;
   const int np = a.nranks;
   const int ncell = kPlanNB * np;
   // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
@@ -692,6 +703,21 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
       }
       s_item = it;
       s_cell = cell;
+      s_has_rec = false;
+      if (it >= 0 && s_peer[cell] != a.rank) {  // a remote query's record: one load over NVLink
+        const RouteDesc *dd = reinterpret_cast<const RouteDesc *>(a.peer[s_peer[cell]]);
+        if (dd->rec_off) {
+          const int4 *rp = reinterpret_cast<const int4 *>(reinterpret_cast<const char *>(dd) + dd->rec_off) +
+                           2 * (s_bs[cell] + (it - s_pre[cell]));
+          const int4 r0 = rp[0], r1 = rp[1];
+          s_rec.gsid = (int64_t)(uint32_t)r0.x | ((int64_t)r0.y << 32);
+          s_rec.off = (int64_t)(uint32_t)r0.z | ((int64_t)r0.w << 32);
+          s_rec.len = r1.x;
+          s_rec.qi = r1.y;
+          s_rec.q0 = r1.z;
+          s_has_rec = true;
+        }
+      }
     }
     __syncthreads();
     const long long it = s_item;
@@ -708,10 +734,12 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
     const int p = s_peer[cell];
     const char *reg = a.peer[p];
     const RouteDesc *d = reinterpret_cast<const RouteDesc *>(reg);
-    const int32_t qi = reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[cell] + (it - s_pre[cell])];
-    const int64_t g = reinterpret_cast<const int64_t *>(reg + d->sid_off)[qi];
-    const int64_t off = reinterpret_cast<const int64_t *>(reg + d->qoff_off)[qi];
-    const int L = (int)reinterpret_cast<const int64_t *>(reg + d->len_off)[qi];
+    const bool has_rec = s_has_rec;
+    const int32_t qi = has_rec ? s_rec.qi : reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[cell] + (it - s_pre[cell])];
+    const int64_t g = has_rec ? s_rec.gsid : reinterpret_cast<const int64_t *>(reg + d->sid_off)[qi];
+    const int64_t off = has_rec ? s_rec.off : reinterpret_cast<const int64_t *>(reg + d->qoff_off)[qi];
+    const int L = has_rec ? s_rec.len : (int)reinterpret_cast<const int64_t *>(reg + d->len_off)[qi];
+    const int32_t *q0 = has_rec ? &s_rec.q0 : nullptr;
     char *wreg = const_cast<char *>(reg);
     WalkOut o{reinterpret_cast<int64_t *>(wreg + d->m_off) + qi, reinterpret_cast<int64_t *>(wreg + d->par_off) + qi,
               reinterpret_cast<int64_t *>(wreg + d->dup_off) + qi, nullptr, nullptr};
@@ -728,11 +756,12 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
         // remote query: packed planes, TMA bulk copies over NVLink
         const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
                              reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
-        walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk);
+        walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk, q0);
         packed_q = true;
       }
     }
-    if (!packed_q) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh);  // local (or ids beyond 18 bits): int32, registers
+    if (!packed_q)  // local (or ids beyond 18 bits): int32, registers
+      walk_query<NT, U, NoRing>(v, q, L, sid, nullptr, o, sh, nullptr, nullptr, q0);
   }
 }
 

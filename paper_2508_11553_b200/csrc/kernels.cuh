@@ -110,6 +110,7 @@ struct RouteHead {
   int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
   int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
   int64_t pkf_off;                  // int32[n+1]: 4096-position pack blocks before each remote query (k_route)
+  int64_t rec_off;                  // RouteRec[n] at the idx positions of remote queries (pack): 0 none
   int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
   int32_t rank;                     // the rank whose batch this is (its own queries stay unpacked)
   int32_t nranks;
@@ -126,6 +127,7 @@ struct RouteDesc {
   int64_t m_off, par_off, dup_off;  // int64 results, written by the owners
   int64_t lo_off, hi_off;           // 18-bit planes of tok (remote owners read these), 0: not packed
   int64_t pkf_off;                  // int32[n+1]: 4096-position pack blocks before each remote query (k_route)
+  int64_t rec_off;                  // RouteRec[n] at the idx positions of remote queries (pack): 0 none
   int32_t pk_bad;                   // a token outside [0, 2^18): owners read tok instead
   int32_t rank;                     // the rank whose batch this is (its own queries stay unpacked)
   int32_t nranks;
@@ -145,6 +147,19 @@ struct RouteDesc {
 };
 static_assert(offsetof(RouteDesc, count) == sizeof(RouteHead) && offsetof(RouteDesc, nranks) == offsetof(RouteHead, nranks),
               "RouteHead must be RouteDesc's prefix");
+
+// What an owner needs to start a remote query, at the query's idx position: written by
+// the CTA that packs the query's first block (k_route for an empty query), read with one
+// 32-byte load over NVLink instead of idx -> gsid / offset / length -> first token
+struct RouteRec {
+  int64_t gsid;
+  int64_t off;
+  int32_t len;
+  int32_t qi;
+  int32_t q0;  // first token (0 if len == 0)
+  int32_t pad_;
+};
+static_assert(sizeof(RouteRec) == 32, "two 16-byte loads");
 
 struct RoutedArgs {
   int nranks, rank;

@@ -1441,6 +1441,7 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
     d.hi_off = packed ? offsets[9] : 0;
     d.pkf_off = packed ? offsets[10] : 0;
     d.pk_bad = 0;
+    d.rec_off = packed ? offsets[11] : 0;  // per-query records, written with the pack
     {
       ProfScope ps(s, 4, st);
       ck(tms::launch_route((char *)region, d, st), "route");

@@ -67,8 +67,9 @@ class _CudaArray:
 
 def route_layout(n_max: int, tokens_max: int, header: int | None = None) -> tuple[list[int], int]:
     """Byte offsets (sid, qoff, len, tok, idx, m, par, dup, low plane, high plane, pack
-    blocks) and total bytes of a region.  The 18-bit planes (include/tmstore.h) carry 128
-    positions of slack: owners copy them in 64-position granules."""
+    blocks, query records) and total bytes of a region.  The 18-bit planes
+    (include/tmstore.h) carry 128 positions of slack: owners copy them in 64-position
+    granules."""
     if header is None:
         from . import _lib
 
@@ -78,7 +79,7 @@ def route_layout(n_max: int, tokens_max: int, header: int | None = None) -> tupl
     off, cur = [], (header + 255) // 256 * 256  # RouteDesc header
     planes = (tokens_max + 63) // 64 * 64 + 128
     for nbytes in (8 * n_max, 8 * n_max, 8 * n_max, 4 * tokens_max, 4 * n_max, 8 * n_max, 8 * n_max, 8 * n_max,
-                   2 * planes, planes // 4, 4 * (n_max + 1)):
+                   2 * planes, planes // 4, 4 * (n_max + 1), 32 * n_max):
         off.append(cur)
         cur += (nbytes + 255) // 256 * 256
     return off, cur
@@ -112,8 +113,8 @@ class Router:
             check(store.lib.tm_ipc_open(store.h, (C.c_char * 64).from_buffer_copy(hb), C.byref(out)))
             self.peers.append(out.value)
         self._peer_arr = (C.c_void_p * self.nranks)(*self.peers)
-        self._off_arr = (C.c_int64 * 11)(*self.offsets)
-        self._off_arr_raw = (C.c_int64 * 11)(*self.offsets[:8], 0, 0, 0)  # no 18-bit planes
+        self._off_arr = (C.c_int64 * 12)(*self.offsets)
+        self._off_arr_raw = (C.c_int64 * 12)(*self.offsets[:8], 0, 0, 0, 0)  # no planes, no records
         dev = torch.device("cuda", store.device)
         view = lambda i, n, ts, dt: torch.as_tensor(_CudaArray(self.base + self.offsets[i], (n,), ts), device=dev)  # noqa: E731
         self.gsid = view(0, n_max, "<i8", None)

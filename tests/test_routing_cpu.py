@@ -36,8 +36,8 @@ def test_route_layout_disjoint_and_aligned():
     assert off[0] >= 16_000
     planes = (1_000_000 + 63) // 64 * 64 + 128  # 18-bit planes with 64-position copy granules of slack
     sizes = [8 * 4096, 8 * 4096, 8 * 4096, 4 * 1_000_000, 4 * 4096, 8 * 4096, 8 * 4096, 8 * 4096, 2 * planes,
-             planes // 4, 4 * 4097]
-    assert len(off) == 11
+             planes // 4, 4 * 4097, 32 * 4096]
+    assert len(off) == 12
     for (a, s), b in zip(zip(off, sizes), off[1:] + [total]):
         assert a % 256 == 0 and a + s <= b
 

@@ -32,7 +32,7 @@ def main(n=4096, nranks=2):
     view(1, n, "<i8").copy_(torch.as_tensor(qoff[:-1]))
     view(2, n, "<i8").copy_(torch.as_tensor(lens))
     view(3, int(qoff[-1]), "<i4").copy_(torch.randint(0, 151936, (int(qoff[-1]),), dtype=torch.int32, device=dev))
-    offs = (C.c_int64 * 11)(*off)
+    offs = (C.c_int64 * 12)(*off)
     st = torch.cuda.current_stream().cuda_stream
     st = 1 if st == 0 else st  # cudaStreamLegacy: a null handle would mean the store's own stream
     for _ in range(3):
