@@ -1791,7 +1791,8 @@ cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sm
     }
   }
   // one rank: the register path with U = 8 (the TMA-staged int32 compare measured 6 % slower
-  // here, 25.0-25.2 vs 26.7 M q/s on c5 at N=1; U = 4, which does not spill, 24.3 vs 26.6)
+  // here, 25.0-25.2 vs 26.7 M q/s on c5 at N=1; U = 4, which does not spill, 24.3 vs 26.6;
+  // 4 CTAs per SM at 233 registers without spills 23.6 vs 26.3)
   return walk_routed_variant<kWalkU, false>(v, a, num_sms, s);
 }
 }  // namespace tms
