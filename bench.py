@@ -291,9 +291,14 @@ def run_c5(args):
         time.sleep(0.3)
         t_wall = time.perf_counter()
         store.profile_begin()
+        # no device-side gate here (unlike c4): routed batches are device-bound (host enqueue
+        # ~50 us per batch vs 280-380 us on the GPU) and a per-rank gate only adds the ranks'
+        # gate-end skew to the routed barriers (profiles/r01_bench_c5_gate_check.txt)
         e0.record(stream)
+        t_enq = time.perf_counter()
         run_batches(args.steps)
         e1.record(stream)
+        t_enq = time.perf_counter() - t_enq
         torch.cuda.synchronize()
         walk_ms, walk_n = store.profile_end("walk")
         phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
@@ -306,6 +311,8 @@ def run_c5(args):
         run_batches(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1)
         torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
+    print(f"[bench] rank {rank}: device-timed region {1e3 * elapsed:.3f} ms for {args.steps} routed batches "
+          f"(host enqueue {1e3 * t_enq:.3f} ms)", file=sys.stderr)
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())

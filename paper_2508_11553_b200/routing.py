@@ -247,6 +247,7 @@ def match_pipelined(routers, n: int, batches: int, side_stream=None):
     main = torch.cuda.current_stream(routers[0].store.device)
     side = side_stream or torch.cuda.Stream(routers[0].store.device)
     k = len(routers)
+    side.wait_stream(main)  # the first prepare is ordered after whatever main holds
     prepared = [torch.cuda.Event() for _ in range(k)]
     done = [None] * k
 
