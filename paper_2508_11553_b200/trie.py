@@ -83,16 +83,17 @@ def meta_runs(origins, versions):
     changes from an int64 view (skipped when every token has the same version)."""
     n = len(origins)
     if isinstance(origins, np.ndarray) or not n:
-        o = np.asarray([ORIGIN_CODE.get(x, x) for x in origins] if not isinstance(origins, np.ndarray) else origins,
-                       np.int64)
+        o = np.asarray([ORIGIN_CODE.get(x, 1 if getattr(x, "value", x) in (1, True, "model_output") else 0)
+                        for x in origins] if not isinstance(origins, np.ndarray) else origins, np.int64)
         return runs_from_per_token(o, np.asarray(versions, np.int64))
     first = origins[0]
     o_starts, o_vals = [0], [first]
     cur, i = first, 0
     other = {SpanOrigin.AGENT_INPUT: SpanOrigin.MODEL_OUTPUT, SpanOrigin.MODEL_OUTPUT: SpanOrigin.AGENT_INPUT}
-    if cur not in other:  # not SpanOrigin members: generic path
-        return runs_from_per_token(np.asarray([1 if x in (1, True, "model_output") else 0 for x in origins], np.int64),
-                                   np.asarray(versions, np.int64))
+    if cur not in other:  # not this package's SpanOrigin (0/1, bools, the reference's own enum): by value
+        return runs_from_per_token(
+            np.asarray([1 if getattr(x, "value", x) in (1, True, "model_output") else 0 for x in origins], np.int64),
+            np.asarray(versions, np.int64))
     while True:
         nxt = other[cur]
         try:
