@@ -193,10 +193,11 @@ int tm_route_prepare(tm_store *store, void *region, int64_t n, const int64_t *of
                      int32_t rank, void *stream);
 /* Per-owner query counts of a prepared region (kMaxRanks = 16 int32; synchronous). */
 int tm_route_counts(tm_store *store, const void *region, int32_t *out_counts16, void *stream);
-/* g2l: device int32[global sessions] -> this store's session id (-1 if not owned).
+/* g2l: device int32[g2l_len] global session id -> this store's session id (-1 if not
+ * owned); a query whose global id is outside [0, g2l_len) or maps to -1 gets matched = -1.
  * peer_regions: host array of nranks device pointers (this rank's own region at [rank]). */
 int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                    void *stream);
+                    int64_t g2l_len, void *stream);
 
 /* tm_match_routed with the two cross-rank barriers done on the device instead of by the
  * caller: a 32-thread kernel writes this rank's `arrive` epoch into every peer's region
@@ -206,7 +207,7 @@ int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *
  * the same value on every rank, one larger per routed call (1, 2, ...).  A peer that
  * never signals becomes a device error after 20 s (TM_PEER_TIMEOUT_MS; tm_synchronize reports it). */
 int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
-                         const int32_t *g2l, int64_t epoch, void *stream);
+                         const int32_t *g2l, int64_t g2l_len, int64_t epoch, void *stream);
 
 /* Snapshot / restore (the reference store is in-memory only, trajectory.py:128): write
  * the arena, row table, metadata runs, session counters and the host row mirror to a
@@ -219,7 +220,7 @@ int tm_store_load(tm_store *store, const char *path);
  * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */
 enum {
   TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3,
-  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6
+  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6, TM_KERNEL_RECORD_COPY = 7
 };
 int tm_profile_begin(tm_store *store);
 int tm_profile_end(tm_store *store, int32_t kind, double *total_ms, int64_t *launches);

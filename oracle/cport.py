@@ -38,6 +38,7 @@ def lib():
         l.ro_row_len.restype = C.c_int64
         l.ro_export_row.argtypes = [_P, C.c_int64, C.c_int32, _P, _P, _P]
         l.ro_lex_rows.argtypes = [_P, C.c_int64, _P, _P]
+        l.ro_export_batch.argtypes = [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_int]
         _lib = l
     return _lib
 
@@ -104,6 +105,22 @@ class CRadixStore:
         v = np.empty(L, np.int32)
         lib().ro_export_row(self.h, sid, row, _p(t), _p(m), _p(v))
         return t, m, v
+
+    def export_batch(self, sids, rows, nthreads=1):
+        """Rows (sids[k], rows[k]) packed: (offsets[n+1], tokens, mask, versions)."""
+        sids = np.ascontiguousarray(sids, np.int64)
+        rows = np.ascontiguousarray(rows, np.int32)
+        lens = np.array([lib().ro_row_len(self.h, int(s), int(r)) for s, r in zip(sids, rows)], np.int64)
+        if np.any(lens < 0):
+            raise KeyError("unknown row")
+        off = np.zeros(len(rows) + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        t = np.empty(off[-1], np.int32)
+        m = np.empty(off[-1], np.uint8)
+        v = np.empty(off[-1], np.int32)
+        if lib().ro_export_batch(self.h, len(rows), _p(sids), _p(rows), _p(off), _p(t), _p(m), _p(v), nthreads):
+            raise KeyError("unknown row")
+        return off, t, m, v
 
     def lex_rows(self, sid):
         _, _, nrows = self.stats(sid)

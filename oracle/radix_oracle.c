@@ -418,3 +418,43 @@ int ro_lex_rows(void *h, int64_t sid, int32_t *out_rows, int32_t *n_out) {
   lex(&st->sess[sid]->root, out_rows, n_out);
   return 0;
 }
+
+/* Many path_trajectory calls at once (test speed only): row k of session sids[k] is
+ * written at [out_off[k], out_off[k+1]); rows are split over nthreads threads. */
+typedef struct {
+  Store *st;
+  int64_t n;
+  const int64_t *sids;
+  const int32_t *rows;
+  const int64_t *off;
+  int32_t *tok, *ver;
+  uint8_t *mask;
+  int tid, nthreads, rc;
+} ExportJob;
+
+static void *export_worker(void *arg) {
+  ExportJob *j = arg;
+  for (int64_t k = j->tid; k < j->n; k += j->nthreads)
+    if (ro_export_row(j->st, j->sids[k], j->rows[k], j->tok + j->off[k], j->mask + j->off[k], j->ver + j->off[k]))
+      j->rc = 2;
+  return NULL;
+}
+
+int ro_export_batch(void *h, int64_t n, const int64_t *sids, const int32_t *rows, const int64_t *out_off,
+                    int32_t *tokens, uint8_t *mask, int32_t *versions, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  ExportJob jobs[256];
+  for (int t = 0; t < nthreads; t++) {
+    ExportJob j = {h, n, sids, rows, out_off, tokens, versions, mask, t, nthreads, 0};
+    jobs[t] = j;
+  }
+  for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, export_worker, &jobs[t]);
+  int rc = 0;
+  for (int t = 0; t < nthreads; t++) {
+    pthread_join(th[t], NULL);
+    if (jobs[t].rc) rc = jobs[t].rc;
+  }
+  return rc;
+}

@@ -92,7 +92,7 @@ using RoutedPackedRing = PackedRing<kTmaStages, kPackedChunk>;
 
 // Whole-CTA walk of one query q[0:L) (q may live in a peer GPU's memory).  With a TmaRing
 // the compare goes through the TMA-staged path, otherwise through registers.
-template <int NT, int U, class R = NoRing>
+template <int NT, int U, class R = NoRing, bool COH = false>
 __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, int L, int32_t sid, const int64_t *root_hint,
                                            WalkOut o, WalkShared &sh, R *rg = nullptr,
                                            const PackedQuery *pk = nullptr, const int32_t *q0 = nullptr) {
@@ -106,7 +106,7 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
     int64_t r = -1;
     if (root_hint) {
       r = *root_hint;
-    } else if (L > 0) {
+    } else if (L > 0 && sid >= 0 && sid < v.n_sess) {  // unknown session ids: matched 0
       const int64_t pc = v.s_pc_row[sid];  // in flight with the root probe
       r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sid, dt_key(0, q0 ? *q0 : q[0], false));  // q0: known first token
       if (pc >= 0 && r >= 0) {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
   if (sh.pc_len > 0) {
     const int32_t *pcq = v.arena + sh.pc_vb;
     if constexpr (std::is_same<R, NoRing>::value) {
-      jpc = block_first_mismatch<NT, U>(q, pcq, 0, sh.pc_len, sh.red);
+      jpc = block_first_mismatch<NT, U, COH>(q, pcq, 0, sh.pc_len, sh.red);
     } else {
       if constexpr (IsPackedRing<R>::value) {
         jpc = block_first_mismatch_packed<NT>(pk->lo, pk->hi, pk->off, pcq, 0, sh.pc_len, sh.red, *rg);
@@ -164,19 +164,22 @@ __device__ __forceinline__ void walk_query(const DevView &v, const int32_t *q, i
   while (r >= 0) {
     TM_DCHECK(v, r < v.row_cap, kErrRow);
     const int hi = min(Lr, L);
-    TM_DCHECK(v, vb + v.row_m[r] >= 0 && vb + ((Lr + 3) & ~3) <= v.arena_cap, kErrArena);
+    TM_DCHECK(v, (vb + v.row_m[r] >= 0 && vb + ((Lr + 3) & ~3) <= v.arena_cap) ||
+                     (vb + v.row_m[r] >= v.qv_lo && vb + ((Lr + 3) & ~3) <= v.qv_hi), kErrArena);
     const int32_t *a = v.arena + vb;
     // the extension hint is read before the compare so a turn-by-turn chain hops for free
     int64_t ext = -1;
     int32_t ext_tok = 0, ext_len = 0;
     int64_t ext_vb = 0;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // one round trip: the hint's fields are read speculatively
       ext = v.row_ext[r];
-      if (ext >= 0) { ext_tok = v.row_ext_tok[r]; ext_len = v.row_ext_len[r]; ext_vb = v.row_ext_vb[r]; }
+      ext_tok = v.row_ext_tok[r];
+      ext_len = v.row_ext_len[r];
+      ext_vb = v.row_ext_vb[r];
     }
     int j;
     if constexpr (std::is_same<R, NoRing>::value) {
-      j = block_first_mismatch<NT, U>(q, a, lo, hi, sh.red);
+      j = block_first_mismatch<NT, U, COH>(q, a, lo, hi, sh.red);
     } else {
       if constexpr (IsPackedRing<R>::value) {
         j = block_first_mismatch_packed<NT>(pk->lo, pk->hi, pk->off, a, lo, hi, sh.red, *rg);
@@ -743,8 +746,8 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
     char *wreg = const_cast<char *>(reg);
     WalkOut o{reinterpret_cast<int64_t *>(wreg + d->m_off) + qi, reinterpret_cast<int64_t *>(wreg + d->par_off) + qi,
               reinterpret_cast<int64_t *>(wreg + d->dup_off) + qi, nullptr, nullptr};
-    const int32_t sid = a.g2l[g];
-    if (sid < 0) {  // routed to the wrong owner: flag it, never guess
+    const int32_t sid = (g >= 0 && g < a.g2l_len) ? a.g2l[g] : -1;
+    if (sid < 0) {  // unknown id, or routed to the wrong owner: flag it, never guess
       if (threadIdx.x == 0) { *o.m = -1; *o.parent = -1; *o.dup = -1; }
       __syncthreads();
       continue;
@@ -769,10 +772,20 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
 // K2 record: one persistent launch per batch.  Work item = a session's CHAIN of entries
 // (its inserts in batch order: the sequential semantics of lpm_insert, trie.py:120-179,
 // only bind entries of the same session — sessions never share rows or branch keys).
-// The CTA owning a chain walks (K1) and commits each entry in order; chains run in
-// parallel, longest first.  Row ids are reserved by the host in batch order
-// (deterministic; an entry that re-records an existing sequence leaves its slot
-// unused); arena lines and run slots come from atomic bump counters.
+// The CTA owning a chain walks and commits each entry in order; chains run in parallel,
+// longest first.  Row ids are reserved by the host in batch order (deterministic; an entry
+// that re-records an existing sequence leaves its slot to be reused).
+//
+// A chain is serial, so its cost is the latency of each entry's dependent steps, not its
+// bytes: k_record keeps only the steps the NEXT entry of the chain depends on (the walk,
+// the row table, the branch index, the session counters) and leaves everything else to
+// k_record_copy, which runs after it over all entries at once: arena / run-table
+// allocation, the novel suffix copy, the metadata runs.  Until then a committed row is
+// read where its tokens already are - in its entry's query (read-only for the launch).
+// Inside an entry, the session's counters and path-copy state live in shared memory for
+// the whole chain, the entries' offsets / lengths / first tokens are fetched 64 at a time,
+// a row's fields are read in one round trip, and the compare hands back the two tokens at
+// the mismatch out of the shared-memory stage that held them.
 
 __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m) {
   // index (relative) of the run containing position m (runs start at 0, ascending)
@@ -785,175 +798,378 @@ __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m
   return (int)(lo - r0);
 }
 
-// allocation need of entry e: (arena words, runs, new row)
-__device__ __forceinline__ void entry_need(const Batch &b, int64_t e, long long &words, long long &runs,
-                                           long long &isnew) {
-  words = runs = isnew = 0;
-  const int64_t m = b.o_m[e], L = b.len[e];
-  b.c_firstrun[e] = 0;
-  if (b.o_dup[e] >= 0) return;
-  isnew = 1;
-  if (L > m) {
-    words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
-    const int fr = first_run_at(b, e, m);
-    b.c_firstrun[e] = fr;
-    runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
-  }
+constexpr int kCopyU = 4;      // int4 loads in flight per thread in K2's copies
+constexpr int kRecPre = 64;    // entries whose offset / length / first token are fetched at once
+
+struct RowFields {  // what the walk and the commit need of a row, read in one round trip
+  long long vb, ext, ext_vb, jump;
+  int len, m, ext_tok, ext_len, depth;
+};
+
+__device__ __forceinline__ void load_row(const DevView &v, int64_t r, RowFields &f) {
+  f.vb = v.row_vb[r];
+  f.len = v.row_len[r];
+  f.m = v.row_m[r];
+  f.ext = v.row_ext[r];
+  f.ext_tok = v.row_ext_tok[r];
+  f.ext_len = v.row_ext_len[r];
+  f.ext_vb = v.row_ext_vb[r];
+  f.depth = v.row_depth[r];
+  f.jump = v.row_jump[r];
 }
 
-// commit entry e (whole CTA)
-template <int NT>
-__device__ __forceinline__ void commit_entry(const DevView &v, const Batch &b, int64_t e) {
-  const int64_t m = b.o_m[e];
-  const int64_t L = b.len[e];
-  const int32_t sid = b.sids[e];
-  const int64_t row = b.c_row[e];
-  const bool isnew = b.o_dup[e] < 0;
-  if (threadIdx.x == 0) {
-    TM_DCHECK(v, row >= 0 && row < v.row_cap, kErrRow);
-    if (isnew && L > m) {
-      TM_DCHECK(v, b.c_vb[e] + (m & ~31ll) >= 0 && b.c_vb[e] + ((L + 31) & ~31ll) <= v.arena_cap, kErrArena);
-      TM_DCHECK(v, b.c_run0[e] >= 0 && b.c_run0[e] + (b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) <= v.run_cap,
-                kErrRun);
-    }
-    if (isnew) {
-      const int64_t par = b.o_parent[e];
-      const int32_t local = v.s_nrows[sid];
-      v.s_nrows[sid] = local + 1;
-      v.row_vb[row] = b.c_vb[e];
-      v.row_m[row] = (int32_t)m;
-      v.row_len[row] = (int32_t)L;
-      v.row_parent[row] = par;
-      v.row_sess[row] = sid;
-      v.row_local[row] = local;
-      v.row_depth[row] = par >= 0 ? v.row_depth[par] + 1 : 0;
-      v.row_run0[row] = b.c_run0[e];
-      v.row_nrun[row] = L > m ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
-      v.row_ext[row] = -1;
-      // skew-binary jump pointer (Myers): O(1) here, O(log depth) ancestor searches
-      int64_t jmp = -1;
-      if (par >= 0) {
-        const int64_t j1 = v.row_jump[par];
-        const int64_t j2 = j1 >= 0 ? v.row_jump[j1] : -1;
-        const int32_t d1 = j1 >= 0 ? v.row_depth[j1] : -1, d2 = j2 >= 0 ? v.row_depth[j2] : -1;
-        jmp = (j1 >= 0 && v.row_depth[par] - d1 == d1 - d2) ? j2 : par;
-        // the parent's extension hint; its only readers are this CTA's later entries (same
-        // session chain) and later launches, so program order suffices
-        if (L > m && m == v.row_len[par] && v.row_ext[par] < 0) {
-          v.row_ext_tok[par] = b.tok[b.off[e] + m];
-          v.row_ext_len[par] = (int32_t)L;
-          v.row_ext_vb[par] = b.c_vb[e];
-          v.row_ext[par] = row;
-        }
-      }
-      v.row_jump[row] = jmp;
-      v.s_stored[sid] += L - m;
-      const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sid);
-      if (L > m) ht_insert(v, owner, dt_key(m, b.tok[b.off[e] + m], false), row);
-      else ht_insert(v, owner, dt_key(m, 0, true), row);
-      b.c_local[e] = local;
-    } else {
-      b.c_local[e] = v.row_local[row];
-    }
-    v.s_naive[sid] += L;
-  }
-  if (!isnew || L <= m) return;
-  // novel suffix: int4 copy of [m, L) (congruent mod 4 words; edges land in padding)
-  const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[e]);
-  int4 *dst = reinterpret_cast<int4 *>(v.arena + b.c_vb[e]);
-  for (int64_t i = (m >> 2) + threadIdx.x; i < ((L + 3) >> 2); i += NT) dst[i] = ldg_stream(src + i);
-  // metadata runs overlapping [m, L), first one clamped to m
-  const int64_t r0 = b.run_off[e] + b.c_firstrun[e];
-  const int64_t nr = b.run_off[e + 1] - r0;
-  for (int64_t k = threadIdx.x; k < nr; k += NT) {
-    const int64_t d = b.c_run0[e] + k;
-    const int32_t st = b.run_start[r0 + k];
-    v.run_start[d] = (int32_t)(st > m ? (int64_t)st : m);
-    v.run_origin[d] = b.run_origin[r0 + k];
-    v.run_version[d] = b.run_version[r0 + k];
-  }
-}
+struct RecShared {
+  int red[2];
+  int cap[6];  // compare capture: per-warp (q, a) tokens, then the CTA's
+  // the current entry
+  long long off;
+  int len, q0;
+  // the walk
+  long long row;
+  int lo, pc_len;
+  RowFields f;       // the current row's fields
+  long long m, parent, dup;
+  int tnext, spar;
+  RowFields pf;      // the parent's fields (commit)
+  // the chain's session (cached for the whole chain, written back at its end)
+  int sid, nrows;
+  long long stored, naive;
+  long long pc_row, pc_vb, pc_cap;
+  int pc_rlen, pc_depth;  // the path copy's row: length, depth
+  // path-copy upkeep of the current entry
+  long long pcw_vb;
+  int pcw_from, pcw_len;
+  // entry prefetch
+  long long pre_off[kRecPre];
+  int pre_len[kRecPre], pre_q0[kRecPre];
+};
 
-// Session path copy upkeep after entry e committed a new row at depth >= kPathCopyDepth:
-// the row becomes its session's path copy.  A turn that extends the current copy's row
-// exactly at its end appends only its new tokens (amortised O(1) per token: copies are
-// allocated with 2x headroom); anything else copies its whole sequence into a fresh
-// buffer.  The source is the entry's own query (its full sequence, already in HBM).
-template <int NT>
-__device__ __forceinline__ void update_path_copy(const DevView &v, const Batch &b, int64_t e, WalkShared &sh) {
-  const int64_t row = b.c_row[e];
+// Whole-CTA walk of the chain's current entry (sh.off / sh.len / sh.q0), the LPM walk of
+// trie.py:136-158 over rows (see walk_query): results into sh.m / parent / dup / tnext /
+// spar and the parent's fields into sh.pf.
+template <int S, int CHV>
+__device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, RecShared &sh,
+                                            TmaRing<64, S, CHV> &rg) {
+  const int32_t *q = b.tok + sh.off;
+  const int L = sh.len;
   if (threadIdx.x == 0) {
     sh.pc_len = 0;
-    const int64_t L = b.len[e], m = b.o_m[e];
-    if (b.o_dup[e] < 0 && v.row_depth[row] >= kPathCopyDepth) {
-      const int32_t sid = b.sids[e];
-      const int64_t pc = v.s_pc_row[sid], par = b.o_parent[e];
-      int64_t vb = v.s_pc_vb[sid], cap = v.s_pc_cap[sid], from = m;
-      if (!(pc >= 0 && par == pc && m == v.row_len[pc] && L <= cap)) {
-        cap = (2 * L + kAlignWords - 1) / kAlignWords * kAlignWords;
-        vb = (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)cap);
-        from = 0;
-      }
-      TM_DCHECK(v, vb >= 0 && vb + cap <= v.arena_cap, kErrArena);
-      v.s_pc_row[sid] = row;
-      v.s_pc_vb[sid] = vb;
-      v.s_pc_cap[sid] = cap;
-      sh.pc_vb = vb;
-      sh.pc_len = (int)L;
-      sh.lo = (int)from;
-    }
+    const int64_t r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sh.sid, dt_key(0, sh.q0, false));
+    if (sh.pc_row >= 0 && r >= 0) sh.pc_len = min(L, sh.pc_rlen);
+    sh.row = r;
   }
   __syncthreads();
-  if (sh.pc_len == 0) return;
-  // int4 copy of positions [from, L) (the copy is congruent with the query mod 4 words;
-  // edge words land in the copy's own padding)
-  const int4 *src = reinterpret_cast<const int4 *>(b.tok + b.off[e]);
-  int4 *dst = reinterpret_cast<int4 *>(v.arena + sh.pc_vb);
-  for (int64_t i = (sh.lo >> 2) + threadIdx.x; i < ((sh.pc_len + 3) >> 2); i += NT) dst[i] = ldg_stream(src + i);
+  int jpc = 0;
+  if (sh.pc_len > 0) jpc = block_first_mismatch_tma(q, v.arena + sh.pc_vb, 0, sh.pc_len, sh.red, rg);
+  if (threadIdx.x == 0) {
+    int64_t r = sh.row;
+    int lo = 1;
+    if (jpc > 0) {  // owner of position jpc-1 on the copy's path: O(log depth) ancestor search
+      r = sh.pc_row;
+      while (v.row_m[r] > jpc - 1) {
+        const int64_t jp = v.row_jump[r];
+        r = (jp >= 0 && v.row_m[jp] > jpc - 1) ? jp : v.row_parent[r];
+      }
+      lo = jpc;
+    }
+    if (r < 0) {  // nothing shares the first token: matched 0
+      sh.m = 0;
+      sh.parent = -1;
+      sh.dup = -1;
+      sh.tnext = sh.q0;
+      sh.spar = -1;
+    } else {
+      load_row(v, r, sh.f);
+    }
+    sh.row = r;
+    sh.lo = lo;
+  }
+  __syncthreads();
+  while (sh.row >= 0) {
+    const int64_t r = sh.row;
+    const int lo = sh.lo, Lr = sh.f.len;
+    const int hi = min(Lr, L);
+    TM_DCHECK(v, (sh.f.vb + sh.f.m >= 0 && sh.f.vb + ((Lr + 3) & ~3) <= v.arena_cap) ||
+                     (sh.f.vb + sh.f.m >= v.qv_lo && sh.f.vb + ((Lr + 3) & ~3) <= v.qv_hi), kErrArena);
+    const int32_t *a = v.arena + sh.f.vb;
+    const int j = block_first_mismatch_tma(q, a, lo, hi, sh.red, rg, sh.cap);
+    if (threadIdx.x == 0) {
+      int64_t next = -1;
+      if (j < L) {
+        const int32_t t = j < hi ? sh.cap[4] : q[j];  // j == hi == Lr: the row ended before the query
+        if (j == Lr && sh.f.ext >= 0 && t == sh.f.ext_tok) next = sh.f.ext;
+        else next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
+        if (next < 0) {
+          sh.m = j;
+          sh.parent = r;
+          sh.dup = -1;
+          sh.tnext = t;
+          sh.spar = j < Lr ? sh.cap[5] : -1;
+          sh.pf = sh.f;
+        } else {
+          load_row(v, next, sh.f);
+        }
+      } else {  // the query ended inside (or at the end of) row r
+        sh.m = L;
+        sh.parent = r;
+        sh.dup = (L == Lr) ? r : ht_find(v, (uint64_t)r, dt_key(L, 0, true));
+        sh.tnext = -1;
+        sh.spar = L < Lr ? a[L] : -1;
+        sh.pf = sh.f;
+      }
+      sh.row = next;
+      sh.lo = j + 1;
+    }
+    __syncthreads();
+  }
 }
 
-template <int NT, int U, bool TMA = false, int MINB = 1>
-__global__ void __launch_bounds__(NT, MINB) k_record(DevView v, RecordArgs a) {
+// Commit the walked entry e (thread 0): row table, the parent's extension hint, the
+// branch index, the session counters (shared memory).  Arena / run slots: k_record_copy.
+__device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, int64_t e, RecShared &sh) {
+  const int64_t m = sh.m, L = sh.len, par = sh.parent;
+  sh.pcw_len = 0;  // no path-copy write unless this entry's row takes the copy (below)
+  b.o_m[e] = m;
+  b.o_parent[e] = par;
+  b.o_dup[e] = sh.dup;
+  b.o_tnext[e] = sh.tnext;
+  b.o_spar[e] = sh.spar;
+  sh.naive += L;
+  const int64_t row = b.c_row[e];
+  TM_DCHECK(v, row >= 0 && row < v.row_cap, kErrRow);
+  if (sh.dup >= 0) {  // re-recorded sequence: its reserved slot stays an empty hole
+    v.row_len[row] = 0;
+    v.row_sess[row] = -1;
+    b.c_row[e] = sh.dup;
+    b.c_local[e] = v.row_local[sh.dup];
+    return;
+  }
+  const int64_t vbq = (int64_t)((b.tok + sh.off) - v.arena);  // the row's positions, in its query
+  // skew-binary jump pointer (Myers): O(1) here, O(log depth) ancestor searches
+  int64_t jmp = -1;
+  if (par >= 0) {
+    const int64_t j1 = sh.pf.jump;
+    int64_t j2 = -1;
+    int32_t d1 = -1, d2 = -1;
+    if (j1 >= 0) {
+      j2 = v.row_jump[j1];
+      d1 = v.row_depth[j1];
+      d2 = j2 >= 0 ? v.row_depth[j2] : -1;
+    }
+    jmp = (j1 >= 0 && sh.pf.depth - d1 == d1 - d2) ? j2 : par;
+  }
+  const int32_t local = sh.nrows++;
+  const int32_t depth = par >= 0 ? sh.pf.depth + 1 : 0;
+  sh.stored += L - m;
+  v.row_vb[row] = vbq;
+  v.row_m[row] = (int32_t)m;
+  v.row_len[row] = (int32_t)L;
+  v.row_parent[row] = par;
+  v.row_sess[row] = sh.sid;
+  v.row_local[row] = local;
+  v.row_depth[row] = depth;
+  v.row_ext[row] = -1;
+  v.row_jump[row] = jmp;
+  // the parent's extension hint; its only readers are this CTA's later entries (same
+  // session chain) and later launches, so program order suffices
+  if (par >= 0 && L > m && m == sh.pf.len && sh.pf.ext < 0) {
+    v.row_ext_tok[par] = sh.tnext;
+    v.row_ext_len[par] = (int32_t)L;
+    v.row_ext_vb[par] = vbq;
+    v.row_ext[par] = row;
+  }
+  const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sh.sid);
+  if (L > m) ht_insert(v, owner, dt_key(m, sh.tnext, false), row);  // tnext = q[m]
+  else ht_insert(v, owner, dt_key(m, 0, true), row);
+  b.c_local[e] = local;
+  // session path copy upkeep (rows at chain depth >= kPathCopyDepth): a turn that extends
+  // the copy's row exactly at its end appends only its new tokens (2x headroom); a row
+  // deeper than the copy's re-seats the copy (in place when it fits, else a fresh buffer
+  // of twice its length); siblings and shallower rows leave it alone, so sampling many
+  // completions of one deep turn costs no copies and a session's copy buffers total
+  // <= 4x its longest sequence.
+  if (depth >= kPathCopyDepth) {
+    int64_t vb = sh.pc_vb, cap = sh.pc_cap, from = m;
+    bool write = true;
+    if (sh.pc_row >= 0 && par == sh.pc_row && m == sh.pc_rlen && L <= cap) {
+      // the next turn of the copy's own chain: append
+    } else if (sh.pc_row < 0 || depth > sh.pc_depth) {
+      from = 0;
+      if (sh.pc_row < 0 || L > cap) {
+        cap = (2 * L + kAlignWords - 1) / kAlignWords * kAlignWords;
+        vb = (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)cap);
+      }
+    } else {
+      write = false;
+    }
+    if (write) {
+      TM_DCHECK(v, vb >= 0 && vb + cap <= v.arena_cap, kErrArena);
+      sh.pc_row = row;
+      sh.pc_vb = vb;
+      sh.pc_cap = cap;
+      sh.pc_rlen = (int)L;
+      sh.pc_depth = depth;
+      sh.pcw_vb = vb;
+      sh.pcw_from = (int)from;
+      sh.pcw_len = (int)L;
+    }
+  }
+}
+
+template <int S, int CHV, int MINB>
+__global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a) {
   const Batch &b = a.b;
-  __shared__ WalkShared sh;
+  __shared__ RecShared sh;
   __shared__ long long s_item;
-  __shared__ TmaRing<64, 2, 256> rg;
-  if constexpr (TMA) tma_ring_init(rg);
+  __shared__ TmaRing<64, S, CHV> rg;
+  tma_ring_init(rg);
   for (;;) {
     if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
     __syncthreads();
     const int64_t it = s_item;
-    __syncthreads();
     if (it >= a.nchains) {
       sched_exit(a.sched);
       return;
     }
     const int64_t c = a.chain_order[it];
-    for (int64_t e = a.chain_beg[c]; e < a.chain_beg[c + 1]; e++) {
-      WalkOut o{b.o_m + e, b.o_parent + e, b.o_dup + e, b.o_tnext + e, b.o_spar + e};
-      if constexpr (TMA) walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh, &rg);
-      else walk_query<NT, U>(v, b.tok + b.off[e], (int)b.len[e], b.sids[e], nullptr, o, sh);
-      if (threadIdx.x == 0) {  // allocate (the reserved row id is already in c_row)
-        long long words, runs, isnew;
-        entry_need(b, e, words, runs, isnew);
-        const int64_t m = b.o_m[e];
-        if (isnew) {
-          const long long base = words ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)words) : 0;
-          b.c_vb[e] = base - (m / kAlignWords) * kAlignWords;
-          b.c_run0[e] = runs ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)runs) : 0;
-        } else {  // re-recorded sequence: its reserved slot stays an empty hole
-          v.row_len[b.c_row[e]] = 0;
-          v.row_sess[b.c_row[e]] = -1;
-          b.c_row[e] = b.o_dup[e];
-          b.c_vb[e] = 0;
-          b.c_run0[e] = 0;
+    const int64_t e0 = a.chain_beg[c], e1 = a.chain_beg[c + 1];
+    if (threadIdx.x == 0) {  // the session, cached for the whole chain
+      const int32_t sid = b.sids[e0];
+      sh.sid = sid;
+      sh.nrows = v.s_nrows[sid];
+      sh.stored = v.s_stored[sid];
+      sh.naive = v.s_naive[sid];
+      sh.pc_row = v.s_pc_row[sid];
+      sh.pc_vb = v.s_pc_vb[sid];
+      sh.pc_cap = v.s_pc_cap[sid];
+      if (sh.pc_row >= 0) {
+        sh.pc_rlen = v.row_len[sh.pc_row];
+        sh.pc_depth = v.row_depth[sh.pc_row];
+      }
+    }
+    for (int64_t e = e0; e < e1; e++) {
+      const int k = (int)((e - e0) % kRecPre);
+      if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
+        __syncthreads();
+        const int64_t w = e + threadIdx.x;
+        if (threadIdx.x < kRecPre && w < e1) {
+          const int64_t off = b.off[w];
+          sh.pre_off[threadIdx.x] = off;
+          sh.pre_len[threadIdx.x] = (int)b.len[w];
+          sh.pre_q0[threadIdx.x] = b.tok[off];
         }
       }
       __syncthreads();
-      commit_entry<NT>(v, b, e);
+      if (threadIdx.x == 0) {
+        sh.off = sh.pre_off[k];
+        sh.len = sh.pre_len[k];
+        sh.q0 = sh.pre_q0[k];
+      }
       __syncthreads();
-      update_path_copy<NT>(v, b, e, sh);
-      __syncthreads();  // the next entry of the chain sees this one (same CTA)
+      record_walk(v, b, sh, rg);
+      if (threadIdx.x == 0) record_commit(v, b, e, sh);
+      __syncthreads();
+      if (sh.pcw_len > 0) {  // path copy: [from, L) of the entry's query (congruent layout)
+        block_copy4<64, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
+                                reinterpret_cast<const int4 *>(b.tok + sh.off), sh.pcw_from >> 2, (sh.pcw_len + 3) >> 2);
+        // generic-proxy arena writes -> visible to the next entry's cp.async.bulk reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) {  // write the session back
+      const int32_t sid = sh.sid;
+      v.s_nrows[sid] = sh.nrows;
+      v.s_stored[sid] = sh.stored;
+      v.s_naive[sid] = sh.naive;
+      v.s_pc_row[sid] = sh.pc_row;
+      v.s_pc_vb[sid] = sh.pc_vb;
+      v.s_pc_cap[sid] = sh.pc_cap;
+    }
+    __syncthreads();
+  }
+}
+
+// K2b (after k_record, all entries at once): allocate arena lines and run slots for every
+// new row (a block scan per CTA, one atomic per CTA and counter), move its novel suffix
+// [m, L) from the query into the arena (congruent mod 32 words; edge words land in the
+// row's own padding) and its metadata runs into the run table (first run clamped to m),
+// then switch the row's virtual base - and a parent's extension hint pointing at it - to
+// the arena.  CTA b owns entries [b*chunk, (b+1)*chunk), chunk <= NT.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_record_copy(DevView v, RecordArgs a, int64_t chunk) {
+  const Batch &b = a.b;
+  __shared__ long long s_words[NT / 32], s_runs[NT / 32];
+  __shared__ long long s_base_w, s_base_r;
+  const int64_t e0 = blockIdx.x * chunk;
+  const int64_t e = e0 + threadIdx.x;
+  long long words = 0, runs = 0;
+  int fr = 0;
+  bool isnew = false;
+  int64_t m = 0, L = 0;
+  if (threadIdx.x < chunk && e < b.n) {
+    isnew = b.o_dup[e] < 0;
+    m = b.o_m[e];
+    L = b.len[e];
+    if (isnew && L > m) {
+      words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
+      fr = first_run_at(b, e, m);
+      runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
+    }
+  }
+  // block-wide exclusive scans of words and runs
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long iw = words, ir = runs;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const long long tw = __shfl_up_sync(0xffffffffu, iw, d), tr = __shfl_up_sync(0xffffffffu, ir, d);
+    if (lane >= d) { iw += tw; ir += tr; }
+  }
+  if (lane == 31) { s_words[warp] = iw; s_runs[warp] = ir; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tw = 0, tr = 0;
+    for (int w = 0; w < NT / 32; w++) {
+      const long long x = s_words[w], y = s_runs[w];
+      s_words[w] = tw;
+      s_runs[w] = tr;
+      tw += x;
+      tr += y;
+    }
+    s_base_w = tw ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)tw) : 0;
+    s_base_r = tr ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)tr) : 0;
+  }
+  __syncthreads();
+  if (isnew) {
+    const long long vb = words ? s_base_w + s_words[warp] + iw - words - (m / kAlignWords) * kAlignWords : -m;
+    const long long run0 = runs ? s_base_r + s_runs[warp] + ir - runs : 0;
+    TM_DCHECK(v, !words || (vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap), kErrArena);
+    TM_DCHECK(v, run0 >= 0 && run0 + runs <= v.run_cap, kErrRun);
+    b.c_vb[e] = vb;
+    b.c_run0[e] = run0;
+    b.c_firstrun[e] = fr;
+  }
+  __syncthreads();
+  const int64_t e_end = min(e0 + chunk, b.n);
+  for (int64_t x = e0; x < e_end; x++) {
+    if (b.o_dup[x] >= 0) continue;
+    const int64_t mx = b.o_m[x], Lx = b.len[x], row = b.c_row[x], vb = b.c_vb[x];
+    if (Lx > mx) {
+      block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + vb), reinterpret_cast<const int4 *>(b.tok + b.off[x]),
+                              mx >> 2, (Lx + 3) >> 2);
+      const int64_t r0 = b.run_off[x] + b.c_firstrun[x], nr = b.run_off[x + 1] - r0, d0 = b.c_run0[x];
+      for (int64_t k = threadIdx.x; k < nr; k += NT) {
+        const int32_t st = b.run_start[r0 + k];
+        v.run_start[d0 + k] = (int32_t)(st > mx ? (int64_t)st : mx);
+        v.run_origin[d0 + k] = b.run_origin[r0 + k];
+        v.run_version[d0 + k] = b.run_version[r0 + k];
+      }
+    }
+    if (threadIdx.x == 0) {
+      v.row_vb[row] = vb;
+      v.row_run0[row] = b.c_run0[x];
+      v.row_nrun[row] = Lx > mx ? (int32_t)(b.run_off[x + 1] - b.run_off[x] - b.c_firstrun[x]) : 0;
+      const int64_t par = b.o_parent[x];
+      if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
     }
   }
 }
@@ -1555,30 +1771,19 @@ static cudaError_t walk_variant(const DevView &v, const Batch &b, int num_sms, c
   return cudaGetLastError();
 }
 
-// TM_WALK_VARIANT (tuning only).  Default: the TMA-staged compare, 4 stages x 4 KB per
-// stream (c4: 31.9 M q/s vs 30.7 for the register-double-buffered "64x8").
+// Default K1: the TMA-staged compare, 4 stages x 4 KB per stream (c4: 31.9 M q/s vs 30.7
+// for the register-double-buffered "64x8").  The other shapes measured in round 1 are only
+// compiled into tuning builds (make TUNING=1 -> -DTM_TUNING; TM_WALK_VARIANT selects).
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s) {
+#ifdef TM_TUNING
   static int variant = -1;
   if (variant < 0) {
+    static const char *names[] = {"tma", "256x2", "512x2", "128x4", "512x1", "128x2", "128x8", "64x8", "256x4",
+                                  "64x4", "tma3", "tma8x128", "tma6x128", "tma2x512"};
     const char *e = getenv("TM_WALK_VARIANT");
     variant = 0;
-    if (e) {
-      if (!strcmp(e, "256x2")) variant = 1;
-      else if (!strcmp(e, "512x2")) variant = 2;
-      else if (!strcmp(e, "128x4")) variant = 3;
-      else if (!strcmp(e, "512x1")) variant = 4;
-      else if (!strcmp(e, "128x2")) variant = 5;
-      else if (!strcmp(e, "128x8")) variant = 6;
-      else if (!strcmp(e, "64x8")) variant = 7;
-      else if (!strcmp(e, "256x4")) variant = 8;
-      else if (!strcmp(e, "64x4")) variant = 9;
-      else if (!strcmp(e, "tma")) variant = 10;
-      else if (!strcmp(e, "tma3")) variant = 11;
-      else if (!strcmp(e, "tma8x128")) variant = 12;
-      else if (!strcmp(e, "tma6x128")) variant = 13;
-      else if (!strcmp(e, "tma2x512")) variant = 14;
-      else if (!strcmp(e, "64x8")) variant = 15;
-    }
+    for (int i = 0; e && i < (int)(sizeof(names) / sizeof(names[0])); i++)
+      if (!strcmp(e, names[i])) variant = i;
   }
   switch (variant) {
     case 1: return walk_variant<256, 2>(v, b, num_sms, s);
@@ -1587,70 +1792,71 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
     case 4: return walk_variant<512, 1>(v, b, num_sms, s);
     case 5: return walk_variant<128, 2>(v, b, num_sms, s);
     case 6: return walk_variant<128, 8>(v, b, num_sms, s);
-    case 7: return walk_variant<64, 8>(v, b, num_sms, s);
+    case 7: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
     case 8: return walk_variant<256, 4>(v, b, num_sms, s);
     case 9: return walk_variant<64, 4>(v, b, num_sms, s);
-    case 10: return walk_tma_variant<4, 256>(v, b, num_sms, s);
-    case 11: return walk_tma_variant<3, 256>(v, b, num_sms, s);
-    case 12: return walk_tma_variant<8, 128>(v, b, num_sms, s);
-    case 13: return walk_tma_variant<6, 128>(v, b, num_sms, s);
-    case 14: return walk_tma_variant<2, 512>(v, b, num_sms, s);
-    case 15: return walk_variant<kWalkNT, kWalkU>(v, b, num_sms, s);
-    default: return walk_tma_variant<kTmaStages, kTmaChunk>(v, b, num_sms, s);
+    case 10: return walk_tma_variant<3, 256>(v, b, num_sms, s);
+    case 11: return walk_tma_variant<8, 128>(v, b, num_sms, s);
+    case 12: return walk_tma_variant<6, 128>(v, b, num_sms, s);
+    case 13: return walk_tma_variant<2, 512>(v, b, num_sms, s);
+    default: break;
   }
+#endif
+  return walk_tma_variant<kTmaStages, kTmaChunk>(v, b, num_sms, s);
 }
 
-template <int NT, int U, bool TMA = false, int MINB = 1>
-static cudaError_t record_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record<NT, U, TMA, MINB>, NT, 0);
-    if (occ < 1) occ = 1;
-  }
-  int64_t grid = (int64_t)num_sms * occ;
-  if (grid > a.nchains) grid = a.nchains;
-  if (grid < 1) grid = 1;
-  k_record<NT, U, TMA, MINB><<<(int)grid, NT, 0, s>>>(v, a);
+constexpr int kRecordCopyNT = 256;
+
+cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+  if (a.b.n < 1) return cudaSuccess;
+  // chunk <= NT entries per CTA (the allocation scan is one entry per thread)
+  const int64_t grid = std::max<int64_t>((a.b.n + kRecordCopyNT - 1) / kRecordCopyNT,
+                                         std::min<int64_t>(a.b.n, (int64_t)num_sms * 8));
+  const int64_t chunk = (a.b.n + grid - 1) / grid;
+  k_record_copy<kRecordCopyNT><<<(int)((a.b.n + chunk - 1) / chunk), kRecordCopyNT, 0, s>>>(v, a, chunk);
   return cudaGetLastError();
 }
 
-// Default: chains are serial inside, so K2 runs best with every chain resident at once and
-// as many bytes in flight per chain as that allows.  Up to 7 chains per SM: 128-thread
-// CTAs (<= 72 registers, 7 per SM; c2, 1,000 chains: 0.234 ms vs 0.255 for 64x4); more
-// chains: 64-thread CTAs, 14 per SM (c3, 4,000 chains: 0.065 ms vs 0.073-0.086).
-// TM_RECORD_VARIANT (tuning only): "64x4", "64x8", "32x8", "32x4", "tma", "128x4",
-// "128x2", "256x2", "64x4m"
+template <int S, int CHV, int MINB>
+static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record_tma<S, CHV, MINB>, 64, 0);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
+  k_record_tma<S, CHV, MINB><<<(int)grid, 64, 0, s>>>(v, a);
+  return cudaGetLastError();
+}
+
+// K2 = k_record_tma (chains: walk + commit, serial per session) + k_record_copy (arena
+// allocation, suffixes and runs, all entries in parallel).  A chain's compare is TMA-staged
+// (64-thread CTAs; the stages live in shared memory, not registers): 3 x 4 KB per stream
+// when at most 8 chains per SM, so every chain is resident at once with 24 KB in flight;
+// 2 x 2 KB (more CTAs per SM) for more chains.  Tuning builds (-DTM_TUNING) select other
+// ring shapes with TM_RECORD_VARIANT.
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+#ifdef TM_TUNING
   static int variant = -1;
   if (variant < 0) {
+    static const char *names[] = {"default", "tma3x256", "tma2x128", "tma4x256", "tma2x256", "tma4x128", "tma3x128"};
     const char *e = getenv("TM_RECORD_VARIANT");
     variant = 0;
-    if (e) {
-      if (!strcmp(e, "64x8")) variant = 1;
-      else if (!strcmp(e, "64x4")) variant = 9;
-      else if (!strcmp(e, "32x8")) variant = 2;
-      else if (!strcmp(e, "32x4")) variant = 3;
-      else if (!strcmp(e, "tma")) variant = 4;
-      else if (!strcmp(e, "128x4")) variant = 5;
-      else if (!strcmp(e, "128x2")) variant = 6;
-      else if (!strcmp(e, "256x2")) variant = 7;
-      else if (!strcmp(e, "64x4m")) variant = 8;
-    }
+    for (int i = 0; e && i < (int)(sizeof(names) / sizeof(names[0])); i++)
+      if (!strcmp(e, names[i])) variant = i;
   }
   switch (variant) {
-    case 1: return record_variant<64, 8>(v, a, num_sms, s);
-    case 2: return record_variant<32, 8>(v, a, num_sms, s);
-    case 3: return record_variant<32, 4>(v, a, num_sms, s);
-    case 4: return record_variant<64, 4, true>(v, a, num_sms, s);
-    case 5: return record_variant<128, 4, false, 7>(v, a, num_sms, s);
-    case 6: return record_variant<128, 2, false, 8>(v, a, num_sms, s);
-    case 7: return record_variant<256, 2, false, 4>(v, a, num_sms, s);
-    case 8: return record_variant<64, 4, false, 14>(v, a, num_sms, s);
-    case 9: return record_variant<64, 4>(v, a, num_sms, s);
-    default:
-      if (a.nchains <= (int64_t)num_sms * 7) return record_variant<128, 4, false, 7>(v, a, num_sms, s);
-      return record_variant<64, 4, false, 14>(v, a, num_sms, s);
+    case 1: return record_tma_variant<3, 256, 8>(v, a, num_sms, s);
+    case 2: return record_tma_variant<2, 128, 16>(v, a, num_sms, s);
+    case 3: return record_tma_variant<4, 256, 6>(v, a, num_sms, s);
+    case 4: return record_tma_variant<2, 256, 12>(v, a, num_sms, s);
+    case 5: return record_tma_variant<4, 128, 12>(v, a, num_sms, s);
+    case 6: return record_tma_variant<3, 128, 14>(v, a, num_sms, s);
+    default: break;
   }
+#endif
+  if (a.nchains <= (int64_t)num_sms * 8) return record_tma_variant<3, 256, 8>(v, a, num_sms, s);
+  return record_tma_variant<2, 128, 16>(v, a, num_sms, s);
 }
 
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {
@@ -1778,7 +1984,8 @@ static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, in
 
 cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sms, cudaStream_t s) {
   if (a.nranks > 1) {
-    // remote-query ring (TM_ROUTED_RING = stages x positions per stage; tuning knob)
+#ifdef TM_TUNING
+    // remote-query ring (TM_ROUTED_RING = stages x positions per stage; tuning builds only)
     static const int ring = [] {
       const char *e = getenv("TM_ROUTED_RING");
       return e ? atoi(e) : 0;
@@ -1787,8 +1994,10 @@ cudaError_t launch_walk_routed(const DevView &v, const RoutedArgs &a, int num_sm
       case 1: return walk_routed_variant<4, true, PackedRing<8, 1024>>(v, a, num_sms, s);
       case 2: return walk_routed_variant<4, true, PackedRing<4, 2048>>(v, a, num_sms, s);
       case 3: return walk_routed_variant<4, true, PackedRing<6, 1024>>(v, a, num_sms, s);
-      default: return walk_routed_variant<4, true, RoutedPackedRing, 8>(v, a, num_sms, s);
+      default: break;
     }
+#endif
+    return walk_routed_variant<4, true, RoutedPackedRing, 8>(v, a, num_sms, s);
   }
   // one rank: the register path with U = 8 (the TMA-staged int32 compare measured 6 % slower
   // here, 25.0-25.2 vs 26.7 M q/s on c5 at N=1; U = 4, which does not spill, 24.3 vs 26.6;

@@ -56,6 +56,11 @@ struct DevView {
   int64_t *ctr;  // [0]=arena_used [1]=n_rows [2]=n_runs [3]=first device error code
   // capacities (device-side bounds checks)
   int64_t arena_cap, row_cap, run_cap;
+  int64_t n_sess;  // sessions created: device-buffer matches treat any other id as unknown (matched 0)
+  // record launches: rows committed in the launch are read from their entry's query until
+  // k_record_copy moves them into the arena; their virtual bases fall in [qv_lo, qv_hi)
+  // (debug bounds checks only)
+  int64_t qv_lo, qv_hi;
 };
 
 // Device error codes (ctr[3]; first one wins; the host turns a nonzero code into TM_ECUDA).
@@ -165,6 +170,7 @@ struct RoutedArgs {
   int nranks, rank;
   const char *peer[kMaxRanks];  // every rank's region as mapped on this GPU (own included)
   const int32_t *g2l;           // global session id -> local session id (-1: not owned)
+  int64_t g2l_len;              // entries of g2l; ids outside it are not owned here
   Sched *sched;
   int64_t epoch;                // > 0: device-side barriers (wait for arrive, signal done)
   uint64_t timeout_ns;          // a peer silent this long is a device error, not a hang
@@ -230,10 +236,11 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t owner, uint64_t dt, uint64_
 __device__ __forceinline__ int64_t ht_find(const DevView &v, uint64_t owner, uint64_t dt) {
   uint64_t s = slot_of(owner, dt, v.ht_mask);
   for (uint64_t probes = 0; probes <= v.ht_mask; probes++) {
-    uint64_t k0 = v.hk0[s];
+    // all three words of the slot in one round trip (the value is read speculatively)
+    const uint64_t k0 = v.hk0[s], k1 = v.hk1[s];
+    const int64_t r = v.hval[s];
     if (k0 == kEmpty) return -1;
-    if (k0 == owner && v.hk1[s] == dt) {
-      const int64_t r = v.hval[s];
+    if (k0 == owner && k1 == dt) {
       TM_DCHECK(v, r >= 0 && r < v.row_cap, kErrRow);
       return r;
     }
@@ -266,6 +273,15 @@ __device__ __forceinline__ int4 ldg_stream(const int4 *p) {
   return r;
 }
 
+// Coherent 16-byte load (L2, no .nc): for arena lines written earlier in the SAME launch
+// (k_record: entry e+1 of a chain compares against the suffix / path copy entry e wrote;
+// .nc loads are only defined for data that stays read-only for the whole kernel).
+__device__ __forceinline__ int4 ldg_coh(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+
 // predicated streaming load / store (no branch, so the value stays in registers)
 __device__ __forceinline__ int4 ldg_stream_if(const int4 *p, bool pred) {
   int4 r = make_int4(0, 0, 0, 0);
@@ -280,11 +296,27 @@ __device__ __forceinline__ void stg_if(int4 *p, int4 x, bool pred) {
                ::"l"(p), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w), "r"((int)pred) : "memory");
 }
 
+// Whole-CTA int4 copy dst[i] = src[i], i in [i0, i1): every thread issues UC loads before
+// its stores, so NT*UC*16 bytes are in flight per round (a 2,048-token suffix moves in one
+// round at NT=128, UC=4; one load per thread and round was a chain of dependent round trips).
+// src must stay read-only for the launch (streaming .nc loads).
+template <int NT, int UC>
+__device__ __forceinline__ void block_copy4(int4 *__restrict__ dst, const int4 *__restrict__ src, int64_t i0, int64_t i1) {
+  for (int64_t base = i0 + threadIdx.x; base < i1; base += (int64_t)NT * UC) {
+    int4 x[UC];
+#pragma unroll
+    for (int k = 0; k < UC; k++) x[k] = ldg_stream_if(src + base + k * NT, base + k * NT < i1);
+#pragma unroll
+    for (int k = 0; k < UC; k++) stg_if(dst + base + k * NT, x[k], base + k * NT < i1);
+  }
+}
+
 // First mismatch position in [lo, hi) between q[] and a[] (both indexed by absolute
 // position, 16-byte congruent), or hi.  Whole-block call; all threads get the result.
 // Each warp owns 32*U consecutive int4 per chunk; the next chunk is prefetched into
 // registers while the current one is checked; __syncthreads_or gates early exit.
-template <int NT, int U>
+// COH: a[] may have been written earlier in this launch (k_record) -> coherent loads.
+template <int NT, int U, bool COH = false>
 __device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
                                                     int lo, int hi, int *s_red) {
   if (lo >= hi) return hi;
@@ -299,7 +331,7 @@ __device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ 
 #pragma unroll
   for (int k = 0; k < U; k++) {
     int idx = base + tb + k * 32;
-    if (idx < v1) { qa[k] = ldg_stream(q4 + idx); aa[k] = ldg_stream(a4 + idx); }
+    if (idx < v1) { qa[k] = ldg_stream(q4 + idx); aa[k] = COH ? ldg_coh(a4 + idx) : ldg_stream(a4 + idx); }
     else { qa[k] = make_int4(0, 0, 0, 0); aa[k] = qa[k]; }
   }
   for (;;) {
@@ -309,7 +341,7 @@ __device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ 
 #pragma unroll
       for (int k = 0; k < U; k++) {
         int idx = nb + tb + k * 32;
-        if (idx < v1) { qb[k] = ldg_stream(q4 + idx); ab[k] = ldg_stream(a4 + idx); }
+        if (idx < v1) { qb[k] = ldg_stream(q4 + idx); ab[k] = COH ? ldg_coh(a4 + idx) : ldg_stream(a4 + idx); }
         else { qb[k] = make_int4(0, 0, 0, 0); ab[k] = qb[k]; }
       }
     }
@@ -392,9 +424,13 @@ __device__ __forceinline__ void tma_ring_init(TmaRing<NT, S, CHV> &rg) {
   __syncthreads();
 }
 
+// s_cap (optional, int[2 * NT / 32 + 2]): also capture the query's and the history's token
+// at the first mismatch (out of the shared-memory stage that held it) into s_cap[2 * NT / 32]
+// and s_cap[2 * NT / 32 + 1], so the caller needs no global load for them.
 template <int NT, int S, int CHV>
 __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
-                                                        int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg) {
+                                                        int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg,
+                                                        int *s_cap = nullptr) {
   static_assert(NT == 64, "the TMA compare is written for 64-thread CTAs");
   static_assert(CHV % NT == 0, "chunk must split evenly over the CTA");
   if (lo >= hi) return hi;
@@ -421,6 +457,7 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
     mbar_wait(&rg.bar[s], ((base + c) / S) & 1);
     const int i0 = v0 + c * CHV;
     int first = 0x7fffffff;
+    int fq = 0, fa = 0;  // tokens at `first` (capture)
 #pragma unroll
     for (int k = CHV / NT - 1; k >= 0; k--) {
       const int li = k * NT + threadIdx.x;
@@ -433,16 +470,32 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
       if (p < lo) valid &= (0xfu << (lo - p)) & 0xfu;
       if (p + 4 > hi) valid &= (hi - p) <= 0 ? 0u : (0xfu >> (4 - (hi - p)));
       ne &= valid;
-      if (ne) first = min(first, p + __ffs(ne) - 1);
+      if (ne) {  // k runs downwards, so the last hit is this thread's lowest position
+        const int c = __ffs(ne) - 1;
+        first = p + c;
+        if (s_cap) {
+          fq = c == 0 ? x.x : c == 1 ? x.y : c == 2 ? x.z : x.w;
+          fa = c == 0 ? y.x : c == 1 ? y.y : c == 2 ? y.z : y.w;
+        }
+      }
     }
     if (__syncthreads_or(first != 0x7fffffff)) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       unsigned wmin = __reduce_min_sync(0xffffffffu, (unsigned)first);
       if (lane == 0) s_red[warp] = (int)wmin;
+      if (s_cap && first != 0x7fffffff && (unsigned)first == wmin) {  // the one thread holding it
+        s_cap[2 * warp] = fq;
+        s_cap[2 * warp + 1] = fa;
+      }
       __syncthreads();
-      int r = 0x7fffffff;
+      int r = 0x7fffffff, rw = 0;
 #pragma unroll
-      for (int w = 0; w < NT / 32; w++) r = min(r, s_red[w]);
+      for (int w = 0; w < NT / 32; w++)
+        if (s_red[w] < r) { r = s_red[w]; rw = w; }
+      if (s_cap && threadIdx.x == 0) {
+        s_cap[2 * (NT / 32)] = s_cap[2 * rw];
+        s_cap[2 * (NT / 32) + 1] = s_cap[2 * rw + 1];
+      }
       result = r;
       c++;
       break;

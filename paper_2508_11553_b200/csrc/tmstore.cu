@@ -131,6 +131,9 @@ struct tm_store {
   int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
   int64_t arena_used = 0, n_runs = 0, n_sess = 0;
   int64_t n_real_rows = 0;  // rows minus reserved-but-unused slots
+  // row ids an entry reserved but did not use (it re-recorded an existing sequence): handed
+  // out again before fresh ids, so the row table grows with distinct sequences, not calls
+  std::vector<int64_t> free_rows;
   // observability counters (tm_store_counters)
   int64_t c_record_calls = 0, c_records = 0, c_record_tokens = 0, c_match_calls = 0, c_queries = 0,
           c_export_calls = 0, c_export_rows = 0, c_export_tokens = 0;
@@ -176,7 +179,7 @@ struct tm_store {
   int plan_roots = 0;           // planner also resolves root rows (TM_PLAN_ROOTS=1)
   tms::Sched *sched = nullptr;  // walk scheduler block (self-cleaning)
   bool profile = false;
-  static constexpr int kProfKinds = 7;
+  static constexpr int kProfKinds = 8;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kProfKinds];
   size_t ev_used[kProfKinds] = {};
 };
@@ -777,6 +780,7 @@ int tm_session_create(tm_store *s, int32_t *out_sid) {
     s->sess_naive.push_back(0);
     s->sess_maxdepth.push_back(-1);
     *out_sid = (int32_t)s->n_sess++;
+    s->v.n_sess = s->n_sess;
   });
 }
 
@@ -848,10 +852,17 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     std::vector<int64_t> order(nchains);
     for (int64_t c = 0; c < nchains; c++) order[c] = c;
     std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return chain_tokens[x] > chain_tokens[y]; });
-    // ---- capacity (upper bounds); every entry reserves a row id (batch order)
+    // ---- capacity (upper bounds); every entry reserves a row id (batch order): holes left by
+    // earlier re-recorded sequences first, then fresh ids
     const int64_t row_base = (int64_t)s->rows.size();
+    std::vector<int64_t> reserved(n);
+    const int64_t n_reuse = std::min<int64_t>(n, (int64_t)s->free_rows.size());
+    for (int64_t e = 0; e < n_reuse; e++) reserved[e] = s->free_rows[s->free_rows.size() - 1 - e];
+    s->free_rows.resize(s->free_rows.size() - n_reuse);
+    for (int64_t e = n_reuse; e < n; e++) reserved[e] = row_base + (e - n_reuse);
+    const int64_t n_fresh = n - n_reuse;
     ensure_arena(s, s->arena_used + words_upper);
-    ensure_rows(s, row_base + n);
+    ensure_rows(s, row_base + n_fresh);
     ensure_runs(s, s->n_runs + total_runs);
     ensure_table(s, s->n_real_rows + n);
     wait_prev(s, s->stream);
@@ -896,7 +907,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       h_off[k] = doff[k];
       h_len[k] = tok_len[e];
       h_roff[k] = rr;
-      h_crow[k] = row_base + e;  // reserved id (batch order)
+      h_crow[k] = reserved[e];  // reserved id (batch order)
       int64_t r0 = run_off[e], r1 = run_off[e + 1];
       memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
       memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
@@ -933,8 +944,17 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       ra.chain_order = (const int64_t *)(d + o_cord);
       ra.nchains = nchains;
       ra.sched = s->sched;
-      ProfScope ps(s, 1, s->stream);
-      ck(tms::launch_record(s->v, ra, s->num_sms, s->stream), "record");
+      tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
+      int64_t qend = 0;
+      for (int64_t k = 0; k < n; k++) qend = std::max<int64_t>(qend, doff[k] + round_up(h_len[k], 4));
+      dv.qv_lo = (int64_t)(tok_base - s->v.arena);
+      dv.qv_hi = dv.qv_lo + qend;
+      {
+        ProfScope ps(s, 1, s->stream);
+        ck(tms::launch_record(dv, ra, s->num_sms, s->stream), "record");
+      }
+      ProfScope ps(s, 7, s->stream);
+      ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
     }
     // ---- results back (chain order), into the host mirror in batch order
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
@@ -949,13 +969,13 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                   *r_loc = (const int32_t *)(h + o_cloc);
     std::vector<int64_t> pos(n);  // batch index -> chain position
     for (int64_t k = 0; k < n; k++) pos[perm[k]] = k;
-    s->rows.resize(row_base + n, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
+    s->rows.resize(row_base + n_fresh, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
     for (int64_t e = 0; e < n; e++) {  // batch order: local ordinals are assigned in it
       const int64_t k = pos[e];
       const int32_t sid = sids[e];
       const int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
       if (r_dup[k] < 0) {
-        if (row != row_base + e) fail(TM_ECUDA, "row numbering out of sync");
+        if (row != reserved[e]) fail(TM_ECUDA, "row numbering out of sync");
         RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
         rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
         s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
@@ -965,6 +985,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         s->sess_rows[sid].push_back(row);
         s->sess_stored[sid] += L - m;
         s->n_real_rows++;
+      } else {
+        s->free_rows.push_back(reserved[e]);  // the reserved slot stayed empty: reuse it
       }
       s->sess_naive[sid] += L;
       if (out_matched) out_matched[e] = m;
@@ -1464,9 +1486,10 @@ int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *
 
 namespace {
 int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                 int64_t epoch, void *stream) {
+                 int64_t g2l_len, int64_t epoch, void *stream) {
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
+    if (g2l_len < 0 || (g2l_len > 0 && !g2l)) fail(TM_EINVAL, "bad g2l table");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
     tm_store::MatchSlot *slot = &s->slots[s->next_slot++ % tm_store::kSlots];
     ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
@@ -1476,6 +1499,7 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
     a.rank = rank;
     for (int p = 0; p < nranks; p++) a.peer[p] = (const char *)peer_regions[p];
     a.g2l = g2l;
+    a.g2l_len = g2l_len;
     a.sched = slot->sched;
     a.epoch = epoch;
     static const uint64_t timeout_ms = [] {  // TM_PEER_TIMEOUT_MS (default 20 s)
@@ -1499,19 +1523,19 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
 }  // namespace
 
 int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                    void *stream) {
+                    int64_t g2l_len, void *stream) {
   NvtxRange nvtx_("tm_match_routed");
-  return match_routed(s, nranks, rank, peer_regions, g2l, 0, stream);
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, 0, stream);
 }
 
 int tm_match_routed_sync(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                         int64_t epoch, void *stream) {
+                         int64_t g2l_len, int64_t epoch, void *stream) {
   NvtxRange nvtx_("tm_match_routed_sync");
   if (epoch <= 0) {
     g_err = "epoch must be positive and increase by one per routed call";
     return TM_EINVAL;
   }
-  return match_routed(s, nranks, rank, peer_regions, g2l, epoch, stream);
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, stream);
 }
 
 
@@ -1577,6 +1601,9 @@ int tm_store_load(tm_store *s, const char *path) {
       ensure_table(s, nreal);
       s->rows.resize(nrows);
       r.get(s->rows.data(), sizeof(RowHost) * nrows);
+      s->free_rows.clear();
+      for (int64_t i = 0; i < nrows; i++)
+        if (s->rows[i].sid < 0) s->free_rows.push_back(i);
       s->sess_rows.assign(nsess, {});
       s->sess_stored.assign(nsess, 0);
       s->sess_naive.assign(nsess, 0);
@@ -1608,6 +1635,7 @@ int tm_store_load(tm_store *s, const char *path) {
       r.get(m, 8);
       if (memcmp(m, kMagic, 8)) fail(TM_EINVAL, "snapshot trailer missing");
       s->n_sess = nsess;
+      s->v.n_sess = nsess;
       s->n_real_rows = nreal;
       s->arena_used = aused;
       s->n_runs = nruns;

@@ -166,11 +166,12 @@ class Router:
         g2l = C.c_void_p(self.g2l.data_ptr())
         if sync == "device" and self.nranks > 1:
             self._epoch += 1
-            check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self._epoch, st))
+            check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self.g2l.numel(),
+                                           self._epoch, st))
             return
         if self.nranks > 1:
             self._barrier()
-        check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, g2l, st))
+        check(lib.tm_match_routed(h, self.nranks, self.rank, self._peer_arr, g2l, self.g2l.numel(), st))
         if self.nranks > 1:
             self._barrier()
 

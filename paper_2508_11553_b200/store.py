@@ -160,7 +160,8 @@ class DeviceStore:
         check(st.lib.tm_store_load(st.h, str(path).encode()))
         return st
 
-    KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3, "route": 4, "route_pack": 5, "route_wait": 6}
+    KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3, "route": 4, "route_pack": 5, "route_wait": 6,
+               "record_copy": 7}
 
     def profile_begin(self):
         """Start recording CUDA events around every kernel launch of this store."""

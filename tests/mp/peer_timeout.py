@@ -24,7 +24,7 @@ for _ in range(2):  # this rank's region and a "peer" region nobody ever signals
 peers = (C.c_void_p * 2)(*regions)
 g2l = torch.full((4,), -1, dtype=torch.int32, device="cuda")
 check(store.lib.tm_route_prepare(store.h, C.c_void_p(regions[0]), 0, (C.c_int64 * 12)(*off), 2, 0, None))
-check(store.lib.tm_match_routed_sync(store.h, 2, 0, peers, C.c_void_p(g2l.data_ptr()), 1, None))
+check(store.lib.tm_match_routed_sync(store.h, 2, 0, peers, C.c_void_p(g2l.data_ptr()), g2l.numel(), 1, None))
 t0 = time.time()
 try:
     store.synchronize()
