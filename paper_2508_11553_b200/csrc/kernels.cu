@@ -800,6 +800,7 @@ __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m
 
 constexpr int kCopyU = 4;      // int4 loads in flight per thread in K2's copies
 constexpr int kRecPre = 64;    // entries whose offset / length / first token are fetched at once
+constexpr int kRecCache = 4;   // per-chain root-row and row-field cache entries
 
 struct RowFields {  // what the walk and the commit need of a row, read in one round trip
   long long vb, ext, ext_vb, jump;
@@ -819,8 +820,8 @@ __device__ __forceinline__ void load_row(const DevView &v, int64_t r, RowFields 
 }
 
 struct RecShared {
-  int red[2];
-  int cap[6];  // compare capture: per-warp (q, a) tokens, then the CTA's
+  int red[4];
+  int cap[10];  // compare capture: per-warp (q, a) tokens, then the CTA's (<= 4 warps)
   // the current entry
   long long off;
   int len, q0;
@@ -839,22 +840,60 @@ struct RecShared {
   // path-copy upkeep of the current entry
   long long pcw_vb;
   int pcw_from, pcw_len;
+  // per-chain caches (thread 0): root rows by first token and row fields.  Valid for the
+  // whole chain: root keys never change, and the only fields of this session's rows that
+  // change inside the launch are extension hints, which this CTA's commits set (and update
+  // here).  A 16-branch session walks root -> shared-prefix row without a global load.
+  int rc_tok[kRecCache];
+  long long rc_row[kRecCache];
+  long long fc_row[kRecCache];
+  RowFields fc[kRecCache];
+  int rc_next, fc_next;
   // entry prefetch
   long long pre_off[kRecPre];
   int pre_len[kRecPre], pre_q0[kRecPre];
 };
 
+__device__ __forceinline__ void rec_cache_row(RecShared &sh, int64_t r, const RowFields &f) {
+  for (int i = 0; i < kRecCache; i++)
+    if (sh.fc_row[i] == r) { sh.fc[i] = f; return; }
+  const int i = sh.fc_next++ % kRecCache;
+  sh.fc_row[i] = r;
+  sh.fc[i] = f;
+}
+
+__device__ __forceinline__ void rec_row(const DevView &v, RecShared &sh, int64_t r, RowFields &f) {
+  for (int i = 0; i < kRecCache; i++)
+    if (sh.fc_row[i] == r) { f = sh.fc[i]; return; }
+  load_row(v, r, f);
+  rec_cache_row(sh, r, f);
+}
+
+__device__ __forceinline__ int64_t rec_root(const DevView &v, RecShared &sh, int32_t t) {
+  for (int i = 0; i < kRecCache; i++)
+    if (sh.rc_row[i] >= 0 && sh.rc_tok[i] == t) return sh.rc_row[i];
+  const int64_t r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sh.sid, dt_key(0, t, false));
+  if (r >= 0) {
+    const int i = sh.rc_next++ % kRecCache;
+    sh.rc_tok[i] = t;
+    sh.rc_row[i] = r;
+  }
+  return r;
+}
+
 // Whole-CTA walk of the chain's current entry (sh.off / sh.len / sh.q0), the LPM walk of
 // trie.py:136-158 over rows (see walk_query): results into sh.m / parent / dup / tnext /
 // spar and the parent's fields into sh.pf.
-template <int S, int CHV>
+template <int NT, int S, int CHV>
 __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, RecShared &sh,
-                                            TmaRing<64, S, CHV> &rg) {
+                                            TmaRing<NT, S, CHV> &rg) {
+  static_assert(NT <= 128, "RecShared holds the compare scratch of <= 4 warps");
+  constexpr int kCapQ = 2 * (NT / 32);  // where the compare leaves the tokens at the mismatch
   const int32_t *q = b.tok + sh.off;
   const int L = sh.len;
   if (threadIdx.x == 0) {
     sh.pc_len = 0;
-    const int64_t r = ht_find(v, kRootTag | (uint64_t)(uint32_t)sh.sid, dt_key(0, sh.q0, false));
+    const int64_t r = rec_root(v, sh, sh.q0);
     if (sh.pc_row >= 0 && r >= 0) sh.pc_len = min(L, sh.pc_rlen);
     sh.row = r;
   }
@@ -879,7 +918,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
       sh.tnext = sh.q0;
       sh.spar = -1;
     } else {
-      load_row(v, r, sh.f);
+      rec_row(v, sh, r, sh.f);
     }
     sh.row = r;
     sh.lo = lo;
@@ -896,7 +935,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
     if (threadIdx.x == 0) {
       int64_t next = -1;
       if (j < L) {
-        const int32_t t = j < hi ? sh.cap[4] : q[j];  // j == hi == Lr: the row ended before the query
+        const int32_t t = j < hi ? sh.cap[kCapQ] : q[j];  // j == hi == Lr: the row ended before the query
         if (j == Lr && sh.f.ext >= 0 && t == sh.f.ext_tok) next = sh.f.ext;
         else next = ht_find(v, (uint64_t)r, dt_key(j, t, false));
         if (next < 0) {
@@ -904,10 +943,10 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
           sh.parent = r;
           sh.dup = -1;
           sh.tnext = t;
-          sh.spar = j < Lr ? sh.cap[5] : -1;
+          sh.spar = j < Lr ? sh.cap[kCapQ + 1] : -1;
           sh.pf = sh.f;
         } else {
-          load_row(v, next, sh.f);
+          rec_row(v, sh, next, sh.f);
         }
       } else {  // the query ended inside (or at the end of) row r
         sh.m = L;
@@ -977,6 +1016,31 @@ __device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, 
     v.row_ext_len[par] = (int32_t)L;
     v.row_ext_vb[par] = vbq;
     v.row_ext[par] = row;
+    for (int i = 0; i < kRecCache; i++)
+      if (sh.fc_row[i] == par) {
+        sh.fc[i].ext = row;
+        sh.fc[i].ext_tok = sh.tnext;
+        sh.fc[i].ext_len = (int32_t)L;
+        sh.fc[i].ext_vb = vbq;
+      }
+  }
+  {
+    RowFields nf;
+    nf.vb = vbq;
+    nf.len = (int)L;
+    nf.m = (int)m;
+    nf.ext = -1;
+    nf.ext_tok = 0;
+    nf.ext_len = 0;
+    nf.ext_vb = 0;
+    nf.depth = depth;
+    nf.jump = jmp;
+    rec_cache_row(sh, row, nf);
+    if (m == 0 && L > 0) {  // a new root row, keyed by its first token (tnext = q[0])
+      const int i = sh.rc_next++ % kRecCache;
+      sh.rc_tok[i] = sh.tnext;
+      sh.rc_row[i] = row;
+    }
   }
   const uint64_t owner = m > 0 ? (uint64_t)par : (kRootTag | (uint64_t)(uint32_t)sh.sid);
   if (L > m) ht_insert(v, owner, dt_key(m, sh.tnext, false), row);  // tnext = q[m]
@@ -1016,25 +1080,21 @@ __device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, 
   }
 }
 
-template <int S, int CHV, int MINB>
-__global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a) {
+template <int NT, int S, int CHV, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_record_tma(DevView v, RecordArgs a) {
   const Batch &b = a.b;
   __shared__ RecShared sh;
   __shared__ long long s_item;
-  __shared__ TmaRing<64, S, CHV> rg;
+  __shared__ TmaRing<NT, S, CHV> rg;
   tma_ring_init(rg);
+  // the first wave takes chains by CTA index; later chains come from the work counter,
+  // which k_record_copy (next on the stream) leaves zeroed for the next launch
+  long long it = blockIdx.x;
   for (;;) {
-    if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.sched->work, 1ull);
-    __syncthreads();
-    const int64_t it = s_item;
-    if (it >= a.nchains) {
-      sched_exit(a.sched);
-      return;
-    }
-    const int64_t c = a.chain_order[it];
-    const int64_t e0 = a.chain_beg[c], e1 = a.chain_beg[c + 1];
+    if (it >= a.nchains) return;
+    const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
     if (threadIdx.x == 0) {  // the session, cached for the whole chain
-      const int32_t sid = b.sids[e0];
+      const int32_t sid = (int32_t)a.chains[3 * it + 2];
       sh.sid = sid;
       sh.nrows = v.s_nrows[sid];
       sh.stored = v.s_stored[sid];
@@ -1046,17 +1106,21 @@ __global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a
         sh.pc_rlen = v.row_len[sh.pc_row];
         sh.pc_depth = v.row_depth[sh.pc_row];
       }
+      for (int i = 0; i < kRecCache; i++) {
+        sh.rc_row[i] = -1;
+        sh.fc_row[i] = -1;
+      }
+      sh.rc_next = sh.fc_next = 0;
     }
     for (int64_t e = e0; e < e1; e++) {
       const int k = (int)((e - e0) % kRecPre);
       if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
         __syncthreads();
-        const int64_t w = e + threadIdx.x;
-        if (threadIdx.x < kRecPre && w < e1) {
-          const int64_t off = b.off[w];
-          sh.pre_off[threadIdx.x] = off;
-          sh.pre_len[threadIdx.x] = (int)b.len[w];
-          sh.pre_q0[threadIdx.x] = b.tok[off];
+        for (int t = threadIdx.x; t < kRecPre && e + t < e1; t += NT) {
+          const int64_t off = b.off[e + t];
+          sh.pre_off[t] = off;
+          sh.pre_len[t] = (int)b.len[e + t];
+          sh.pre_q0[t] = b.tok[off];
         }
       }
       __syncthreads();
@@ -1070,7 +1134,7 @@ __global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a
       if (threadIdx.x == 0) record_commit(v, b, e, sh);
       __syncthreads();
       if (sh.pcw_len > 0) {  // path copy: [from, L) of the entry's query (congruent layout)
-        block_copy4<64, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
+        block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
                                 reinterpret_cast<const int4 *>(b.tok + sh.off), sh.pcw_from >> 2, (sh.pcw_len + 3) >> 2);
         // generic-proxy arena writes -> visible to the next entry's cp.async.bulk reads
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1084,7 +1148,10 @@ __global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a
       v.s_pc_row[sid] = sh.pc_row;
       v.s_pc_vb[sid] = sh.pc_vb;
       v.s_pc_cap[sid] = sh.pc_cap;
+      s_item = (long long)gridDim.x + (long long)atomicAdd(&a.sched->work, 1ull);
     }
+    __syncthreads();
+    it = s_item;
     __syncthreads();
   }
 }
@@ -1094,26 +1161,38 @@ __global__ void __launch_bounds__(64, MINB) k_record_tma(DevView v, RecordArgs a
 // [m, L) from the query into the arena (congruent mod 32 words; edge words land in the
 // row's own padding) and its metadata runs into the run table (first run clamped to m),
 // then switch the row's virtual base - and a parent's extension hint pointing at it - to
-// the arena.  CTA b owns entries [b*chunk, (b+1)*chunk), chunk <= NT.
+// the arena.  CTA b owns entries [b*chunk, (b+1)*chunk), chunk <= NT: one thread per entry
+// for the allocation (one round trip of loads, then the scan and the atomics; an entry with
+// at most 4 runs reserves slots for all of them, so the search for the run holding m is
+// not on the way to the token copy), then one warp per entry for the copy, 8 int4 loads in
+// flight per lane.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_record_copy(DevView v, RecordArgs a, int64_t chunk) {
   const Batch &b = a.b;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.sched->work = 0;  // k_record's work counter, for the next launch
   __shared__ long long s_words[NT / 32], s_runs[NT / 32];
   __shared__ long long s_base_w, s_base_r;
+  __shared__ long long s_vb[NT], s_src[NT], s_run0[NT], s_r0[NT], s_row[NT], s_par[NT];
+  __shared__ int s_m[NT], s_L[NT], s_nr[NT];
   const int64_t e0 = blockIdx.x * chunk;
   const int64_t e = e0 + threadIdx.x;
   long long words = 0, runs = 0;
-  int fr = 0;
   bool isnew = false;
-  int64_t m = 0, L = 0;
-  if (threadIdx.x < chunk && e < b.n) {
-    isnew = b.o_dup[e] < 0;
+  int64_t m = 0, L = 0, off = 0, r0 = 0, row = 0, par = 0;
+  if (threadIdx.x < chunk && e < b.n) {  // one round trip: every load is independent
+    const int64_t dup = b.o_dup[e];
     m = b.o_m[e];
     L = b.len[e];
+    off = b.off[e];
+    r0 = b.run_off[e];
+    const int64_t r1 = b.run_off[e + 1];
+    row = b.c_row[e];
+    par = b.o_parent[e];
+    isnew = dup < 0;
     if (isnew && L > m) {
       words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
-      fr = first_run_at(b, e, m);
-      runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
+      if (r1 - r0 > 4) r0 += first_run_at(b, e, m);  // many runs (deep chains): skip those before m now
+      runs = r1 - r0;
     }
   }
   // block-wide exclusive scans of words and runs
@@ -1139,36 +1218,61 @@ __global__ void __launch_bounds__(NT) k_record_copy(DevView v, RecordArgs a, int
     s_base_r = tr ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)tr) : 0;
   }
   __syncthreads();
+  s_L[threadIdx.x] = 0;  // L <= m: nothing to copy for this slot
+  s_m[threadIdx.x] = 0;
+  s_nr[threadIdx.x] = -1;  // -1: no row to finish
   if (isnew) {
     const long long vb = words ? s_base_w + s_words[warp] + iw - words - (m / kAlignWords) * kAlignWords : -m;
     const long long run0 = runs ? s_base_r + s_runs[warp] + ir - runs : 0;
     TM_DCHECK(v, !words || (vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap), kErrArena);
     TM_DCHECK(v, run0 >= 0 && run0 + runs <= v.run_cap, kErrRun);
-    b.c_vb[e] = vb;
-    b.c_run0[e] = run0;
-    b.c_firstrun[e] = fr;
+    s_vb[threadIdx.x] = vb;
+    s_src[threadIdx.x] = off;
+    s_run0[threadIdx.x] = run0;
+    s_r0[threadIdx.x] = r0;
+    s_nr[threadIdx.x] = (int)runs;
+    s_m[threadIdx.x] = (int)m;
+    s_L[threadIdx.x] = (int)L;
+    s_row[threadIdx.x] = row;
+    s_par[threadIdx.x] = par;
   }
   __syncthreads();
-  const int64_t e_end = min(e0 + chunk, b.n);
-  for (int64_t x = e0; x < e_end; x++) {
-    if (b.o_dup[x] >= 0) continue;
-    const int64_t mx = b.o_m[x], Lx = b.len[x], row = b.c_row[x], vb = b.c_vb[x];
+  for (int x = warp; x < (int)chunk; x += NT / 32) {
+    if (s_nr[x] < 0) continue;
+    const int64_t mx = s_m[x], Lx = s_L[x];
+    int fr = 0;
     if (Lx > mx) {
-      block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + vb), reinterpret_cast<const int4 *>(b.tok + b.off[x]),
-                              mx >> 2, (Lx + 3) >> 2);
-      const int64_t r0 = b.run_off[x] + b.c_firstrun[x], nr = b.run_off[x + 1] - r0, d0 = b.c_run0[x];
-      for (int64_t k = threadIdx.x; k < nr; k += NT) {
-        const int32_t st = b.run_start[r0 + k];
+      const int4 *src = reinterpret_cast<const int4 *>(b.tok + s_src[x]);
+      int4 *dst = reinterpret_cast<int4 *>(v.arena + s_vb[x]);
+      const int64_t i1 = (Lx + 3) >> 2;
+      for (int64_t base = (mx >> 2) + lane; base < i1; base += 32 * 8) {
+        int4 t[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) t[k] = ldg_stream_if(src + base + 32 * k, base + 32 * k < i1);
+#pragma unroll
+        for (int k = 0; k < 8; k++) stg_if(dst + base + 32 * k, t[k], base + 32 * k < i1);
+      }
+      // runs overlapping [m, L) (the first clamped to m) keep their slot offsets inside the
+      // entry's reservation: the row's runs are [run0 + fr, run0 + nr)
+      const int64_t rb = s_r0[x], d0 = s_run0[x];
+      int64_t lo = 0, hi = s_nr[x];  // last run with start <= m
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (b.run_start[rb + mid] <= mx) lo = mid; else hi = mid;
+      }
+      fr = (int)lo;
+      for (int k = fr + lane; k < s_nr[x]; k += 32) {
+        const int32_t st = b.run_start[rb + k];
         v.run_start[d0 + k] = (int32_t)(st > mx ? (int64_t)st : mx);
-        v.run_origin[d0 + k] = b.run_origin[r0 + k];
-        v.run_version[d0 + k] = b.run_version[r0 + k];
+        v.run_origin[d0 + k] = b.run_origin[rb + k];
+        v.run_version[d0 + k] = b.run_version[rb + k];
       }
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
+      const int64_t row = s_row[x], par = s_par[x], vb = s_vb[x];
       v.row_vb[row] = vb;
-      v.row_run0[row] = b.c_run0[x];
-      v.row_nrun[row] = Lx > mx ? (int32_t)(b.run_off[x + 1] - b.run_off[x] - b.c_firstrun[x]) : 0;
-      const int64_t par = b.o_parent[x];
+      v.row_run0[row] = s_run0[x] + fr;
+      v.row_nrun[row] = Lx > mx ? (int32_t)(s_nr[x] - fr) : 0;
       if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
     }
   }
@@ -1809,37 +1913,43 @@ constexpr int kRecordCopyNT = 256;
 
 cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
   if (a.b.n < 1) return cudaSuccess;
-  // chunk <= NT entries per CTA (the allocation scan is one entry per thread)
+  // chunk <= NT entries per CTA (the allocation scan is one entry per thread), a multiple
+  // of the CTA's warps (one warp per entry in the copy)
+  constexpr int kWarps = kRecordCopyNT / 32;
   const int64_t grid = std::max<int64_t>((a.b.n + kRecordCopyNT - 1) / kRecordCopyNT,
                                          std::min<int64_t>(a.b.n, (int64_t)num_sms * 8));
-  const int64_t chunk = (a.b.n + grid - 1) / grid;
+  int64_t chunk = (a.b.n + grid - 1) / grid;
+  chunk = std::min<int64_t>(kRecordCopyNT, (chunk + kWarps - 1) / kWarps * kWarps);
   k_record_copy<kRecordCopyNT><<<(int)((a.b.n + chunk - 1) / chunk), kRecordCopyNT, 0, s>>>(v, a, chunk);
   return cudaGetLastError();
 }
 
-template <int S, int CHV, int MINB>
+template <int S, int CHV, int MINB, int NT = 64>
 static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record_tma<S, CHV, MINB>, 64, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record_tma<NT, S, CHV, MINB>, NT, 0);
     if (occ < 1) occ = 1;
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
-  k_record_tma<S, CHV, MINB><<<(int)grid, 64, 0, s>>>(v, a);
+  k_record_tma<NT, S, CHV, MINB><<<(int)grid, NT, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 
 // K2 = k_record_tma (chains: walk + commit, serial per session) + k_record_copy (arena
 // allocation, suffixes and runs, all entries in parallel).  A chain's compare is TMA-staged
-// (64-thread CTAs; the stages live in shared memory, not registers): 3 x 4 KB per stream
-// when at most 8 chains per SM, so every chain is resident at once with 24 KB in flight;
-// 2 x 2 KB (more CTAs per SM) for more chains.  Tuning builds (-DTM_TUNING) select other
-// ring shapes with TM_RECORD_VARIANT.
+// (the stages live in shared memory, not registers).  At most 8 chains per SM: 128-thread
+// CTAs with 3 x 4 KB stages per stream, every chain resident at once with 24 KB in flight
+// (c2: 0.776 of peak vs 0.733 with 64 threads); more chains: one-warp CTAs, 32 per SM,
+// 2 x 1 KB stages, so up to 4,736 chains are resident in one wave (c3, 4,000 chains: 0.517
+// vs 0.459 for 64-thread CTAs in two waves).  Tuning builds (-DTM_TUNING) select other
+// shapes with TM_RECORD_VARIANT.
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
 #ifdef TM_TUNING
   static int variant = -1;
   if (variant < 0) {
-    static const char *names[] = {"default", "tma3x256", "tma2x128", "tma4x256", "tma2x256", "tma4x128", "tma3x128"};
+    static const char *names[] = {"default", "tma3x256", "tma2x128", "tma4x256", "tma2x256", "tma4x128", "tma3x128",
+                                  "t128x3x256", "t128x2x128", "t128x2x256", "t32x2x64", "t32x3x64", "t32x2x128"};
     const char *e = getenv("TM_RECORD_VARIANT");
     variant = 0;
     for (int i = 0; e && i < (int)(sizeof(names) / sizeof(names[0])); i++)
@@ -1852,11 +1962,17 @@ cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cu
     case 4: return record_tma_variant<2, 256, 12>(v, a, num_sms, s);
     case 5: return record_tma_variant<4, 128, 12>(v, a, num_sms, s);
     case 6: return record_tma_variant<3, 128, 14>(v, a, num_sms, s);
+    case 7: return record_tma_variant<3, 256, 8, 128>(v, a, num_sms, s);
+    case 8: return record_tma_variant<2, 128, 12, 128>(v, a, num_sms, s);
+    case 9: return record_tma_variant<2, 256, 8, 128>(v, a, num_sms, s);
+    case 10: return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s);
+    case 11: return record_tma_variant<3, 64, 28, 32>(v, a, num_sms, s);
+    case 12: return record_tma_variant<2, 128, 24, 32>(v, a, num_sms, s);
     default: break;
   }
 #endif
-  if (a.nchains <= (int64_t)num_sms * 8) return record_tma_variant<3, 256, 8>(v, a, num_sms, s);
-  return record_tma_variant<2, 128, 16>(v, a, num_sms, s);
+  if (a.nchains <= (int64_t)num_sms * 8) return record_tma_variant<3, 256, 8, 128>(v, a, num_sms, s);
+  return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s);
 }
 
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {

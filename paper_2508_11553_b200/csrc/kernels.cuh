@@ -208,8 +208,7 @@ struct Batch {
 
 struct RecordArgs {
   Batch b;                    // entries grouped by session chain, batch order inside a chain
-  const int64_t *chain_beg;   // nchains + 1 entry offsets
-  const int64_t *chain_order; // chains in processing order (longest first)
+  const int64_t *chains;      // per chain in processing order (longest first): first entry, end, session
   int64_t nchains;
   Sched *sched;               // work counter (self-cleaning)
 };
@@ -431,7 +430,7 @@ template <int NT, int S, int CHV>
 __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
                                                         int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg,
                                                         int *s_cap = nullptr) {
-  static_assert(NT == 64, "the TMA compare is written for 64-thread CTAs");
+  static_assert(NT % 32 == 0 && NT <= CHV, "whole warps, at least one int4 per thread and chunk");
   static_assert(CHV % NT == 0, "chunk must split evenly over the CTA");
   if (lo >= hi) return hi;
   const int4 *q4 = reinterpret_cast<const int4 *>(q);
@@ -458,6 +457,23 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
     const int i0 = v0 + c * CHV;
     int first = 0x7fffffff;
     int fq = 0, fa = 0;  // tokens at `first` (capture)
+    if (4 * i0 >= lo && 4 * (i0 + CHV) <= hi) {  // a full chunk inside [lo, hi): no masking (uniform)
+#pragma unroll
+      for (int k = CHV / NT - 1; k >= 0; k--) {
+        const int li = k * NT + threadIdx.x;
+        const int4 x = rg.q[s][li], y = rg.a[s][li];
+        const unsigned ne =
+            (x.x != y.x ? 1u : 0u) | (x.y != y.y ? 2u : 0u) | (x.z != y.z ? 4u : 0u) | (x.w != y.w ? 8u : 0u);
+        if (ne) {
+          const int c = __ffs(ne) - 1;
+          first = (i0 + li) * 4 + c;
+          if (s_cap) {
+            fq = c == 0 ? x.x : c == 1 ? x.y : c == 2 ? x.z : x.w;
+            fa = c == 0 ? y.x : c == 1 ? y.y : c == 2 ? y.z : y.w;
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int k = CHV / NT - 1; k >= 0; k--) {
       const int li = k * NT + threadIdx.x;

@@ -887,7 +887,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     Layout lay;
     size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
            o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs),
-           o_crow = lay.add(8 * n), o_cbeg = lay.add(8 * (nchains + 1)), o_cord = lay.add(8 * nchains);
+           o_crow = lay.add(8 * n), o_chains = lay.add(24 * nchains);
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
            o_sp = lay.add(4 * n), o_cloc = lay.add(4 * n);
@@ -915,8 +915,15 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       rr += r1 - r0;
     }
     h_roff[n] = rr;
-    memcpy(h + o_cbeg, chain_beg.data(), 8 * (nchains + 1));
-    memcpy(h + o_cord, order.data(), 8 * nchains);
+    {  // chains in processing order: first entry, end, session
+      int64_t *hc = (int64_t *)(h + o_chains);
+      for (int64_t it = 0; it < nchains; it++) {
+        const int64_t c = order[it];
+        hc[3 * it] = chain_beg[c];
+        hc[3 * it + 1] = chain_beg[c + 1];
+        hc[3 * it + 2] = sids[perm[chain_beg[c]]];
+      }
+    }
     ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
     {
       tms::RecordArgs ra{};
@@ -940,8 +947,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       b.c_run0 = (int64_t *)(d + o_cr0);
       b.c_firstrun = (int32_t *)(d + o_cfr);
       b.c_local = (int32_t *)(d + o_cloc);
-      ra.chain_beg = (const int64_t *)(d + o_cbeg);
-      ra.chain_order = (const int64_t *)(d + o_cord);
+      ra.chains = (const int64_t *)(d + o_chains);
       ra.nchains = nchains;
       ra.sched = s->sched;
       tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
