@@ -1,23 +1,28 @@
 """Benchmark: prefix-match queries/s and tokens compared/s (HBM GB/s vs peak) on B200.
 
-Workload (BASELINE.json configs[3]): per GPU, 10,000 sessions
-each holding one 32,768-token history (8 turns of input/output metadata runs), and
-batches of 4,096 read-only longest-prefix-match queries — 75% full history + 256 new
-tokens, 25% branches at a uniform depth with a forced mismatch.  One step = one
-batch through the K1 match kernel.
+One JSON line (rank 0).  Headline workload by GPU count (BASELINE.json configs):
 
-  value      queries/s with queries resident in HBM (device-timed, CUDA events on the
-             launching stream, max over ranks)
-  e2e        the same through the C-ABI host-buffer call (the query tokens cross PCIe
-             inside the timed region - as 18-bit planes packed by the library's host
-             threads - and the results come back)
-  roofline   K1 algorithmic bytes (8 B per compared token, c_q = min(m+1,|q|,|parent|))
-             / K1 device time, against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the C restatement of the reference radix tree (oracle/, "port"),
-             timed on this box's host cores over the same batch
+  N = 1  c4 (configs[3]): 10,000 sessions x one 32,768-token history, batches of 4,096
+         read-only match queries (75 % full history + 256 new tokens, 25 % branches at a
+         uniform depth with a forced mismatch).  One step = one batch through K1.
+  N > 1  c5 (configs[4]): 1,000,000 sessions, log-uniform 1k-128k histories, sharded by
+         session hash; every rank originates 4,096 queries for sessions owned anywhere,
+         routed over NVLink by the fused P2P match (pipelined batches).  One step = one
+         batch per rank.  The c4 weak-scaling shards are measured beside it (c4_shards).
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling — every rank owns its own
-session shard and matches its own batch; no collective on the data path.
+  value         queries/s with queries resident in HBM (device-timed, CUDA events on the
+                launching stream, max over ranks; W warm-up steps, then exactly K)
+  e2e           (N = 1) the same through the C-ABI host-buffer call: query tokens cross PCIe
+                inside the timed region, results come back
+  roofline      K1 algorithmic bytes (8 B per compared token, c_q = min(m+1,|q|,|parent|)) /
+                device time per batch, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C restatement of the reference trie (oracle/, "port"), all host threads,
+                same batch; reference_unmodified: the reference's own Python trie from
+                baseline/_ref, one process and a pool over all cores, on a query sample
+  configs       (N = 1) c1 / c2 / c3: record (K2), export (K3), NDJSON and - c3 - the
+                include_partials export, device and call rates with their rooflines, next to
+                the C port and the unmodified reference
+  c5_routed     (N = 1) config 5 at one GPU (1M sessions in one 107 GB store, routed path)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
@@ -36,8 +41,11 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # NCCL's "NCCL version ..." banner would land on stdout beside the JSON line
 
 METRIC = "prefix-match queries/s (c4: 10k sessions x 32k-token histories, 4096-query batches)"
+METRIC_C5 = "prefix-match queries/s (c5: 1M sessions, 1k-128k tokens, routed)"
+LINK_PEAK = 670.0  # GB/s per GPU, SM peer reads with both directions busy (tools/p2p_probe)
 
 
 def parse():
@@ -51,9 +59,10 @@ def parse():
     ap.add_argument("--queries", type=int, default=4096)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
-                    help="c4 (default): per-rank 10k x 32k shard, host-routed; c5: 1M-session store sharded "
-                         "by session hash with GPU-originated batches routed over NVLink (fused P2P K1)")
+    ap.add_argument("--no-configs", action="store_true", help="N=1: skip the c1-c3 record/export measurements")
+    ap.add_argument("--no-c5", action="store_true", help="N=1: skip the config-5 routed measurement")
+    ap.add_argument("--workload", default=None, choices=["c4", "c5"],
+                    help="headline workload (default: c4 at N=1, c5 at N>1)")
     ap.add_argument("--c5-sessions", type=int, default=1_000_000)
     ap.add_argument("--pipeline", action=argparse.BooleanOptionalAction, default=True,
                     help="c5, N>1, fused routing: two routing regions, batch k+1 bucketed + packed while batch k "
@@ -62,7 +71,10 @@ def parse():
                     help="c5 exchange: fused P2P K1 (product) or NCCL all-to-all + local match (baseline)")
     ap.add_argument("--mixed", default=None,
                     help="lo,hi: log-uniform history lengths (config-5 shard) instead of fixed --hist")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return a
 
 
 def dist_env():
@@ -79,6 +91,10 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
 
 
 class Clocks:
@@ -128,43 +144,31 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def c4_config(args, world, wl, mixed=None):
+# ---------------------------------------------------------------------------------- configs
+
+def c4_config(args, world, mixed=None):
     """The config object both arms print (the driver compares the arms on it)."""
+    arena_gb = args.sessions * ((args.hist + 31) // 32 * 32) * 4 / 1e9
+    query_gb = args.queries * (0.75 * (args.hist + 256) + 0.25 * (args.hist / 2 + 256)) * 4 / 1e9
     return {"workload": "c4" if mixed is None else "c5-shard", "sessions": args.sessions,
             "history_tokens": args.hist if mixed is None else f"log-uniform {mixed}",
             "batch_queries": args.queries, "ext_frac": 0.75, "parallelism": f"session-shard x{world}",
-            "l2": "inputs larger than L2 (arena %.2f GB + queries %.2f GB per rank)" % (
-                wl.hist_off[-1] * 4 / 1e9, wl.q_off[-1] * 4 / 1e9)}
+            "l2": "inputs larger than L2 (arena %.2f GB + queries ~%.2f GB per rank)" % (arena_gb, query_gb)}
 
 
-def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    from workloads import MatchWorkload
+def c5_config(args, world):
+    return {"workload": "c5", "sessions_total": args.c5_sessions, "history_tokens": "log-uniform [1024, 131072]",
+            "batch_queries_per_rank": args.queries, "owner": "splitmix64(gsid) mod N", "n_ranks": world,
+            "routing": {"fused": "fused P2P K1: owners read requester HBM over NVLink, write results back; "
+                                 "device-side epoch-flag barriers (no collective call per batch)",
+                        "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
+                        "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
+                args.routing] if world > 1 else "one rank: every query is local",
+            "pipelined": bool(args.pipeline and world > 1 and args.routing == "fused"),
+            "l2": "inputs larger than L2 (~%.0f GB arena per rank)" % (107.0 / world)}
 
-    wl = MatchWorkload(args.sessions, args.hist, args.queries)
-    cores = os.cpu_count() or 1
-    times = []
-    cpu_port_bench_reuse(wl, cores)  # warm: build the C store + one pass
-    for _ in range(max(1, args.steps)):
-        _, dt, _ = cpu_port_bench_reuse(wl, cores)
-        times.append(dt)
-    total = sum(times)
-    v = wl.n_queries * len(times) / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": c4_config(args, world, wl),
-        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
-                         "sample": f"full c4 batch ({wl.n_queries} queries) per step, C radix-tree restatement (oracle/radix_oracle.c), {cores} threads"},
-        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    if args.sessions == 10_000 and args.hist == 32_768:
-        line["reference_python_sample"] = python_reference_sample(wl)
-    print(json.dumps(line))
 
+# ------------------------------------------------------------------------- CPU baselines
 
 _cpu_store = {}
 
@@ -191,216 +195,120 @@ def cpu_port_bench_reuse(wl, nthreads):
     return wl.n_queries, time.perf_counter() - t0, res
 
 
-def python_reference_sample(wl, nq=64):
-    """The reference trie's own algorithm in its own language (oracle/radix.py restates
-    rolloutlab/trie.py in pure Python) on a sample of the batch: one lpm_insert per query
-    into a trie holding that query's session history, one process.  Informational: the
-    reference arm and cpu_baseline use the C restatement, which is far faster."""
-    from oracle.radix import RadixOracle
+def reference_match_sample(hist_of, qlist, per_core=16):
+    """The UNMODIFIED reference (baseline/_ref) on a sample of match queries: one process
+    and a pool over all cores.  Falls back to the pure-Python restatement (oracle/radix.py,
+    labelled) when baseline/_ref is not installed."""
+    from tools.refbench import time_reference_match
 
-    def per_token(s):
+    cores = os.cpu_count() or 1
+    q = qlist[: max(8, per_core * cores)]
+    r = time_reference_match(hist_of, q)
+    if r is not None:
+        return {"value": r["pool"], "unit": "queries/s", "cores": r["procs"], "kind": "reference",
+                "single_process": r["single"],
+                "sample": f"{r['queries_pool']} queries (pool of {r['procs']} processes over session-disjoint "
+                          f"shards) / {r['queries_single']} (one process): one lpm_insert each into a trie holding "
+                          "the query's session history, the unmodified reference rolloutlab.trie from baseline/_ref"}
+    from oracle.radix import RadixOracle  # restatement fallback (labelled)
+
+    tries, work = {}, []
+    for s, toks in q[:64]:
+        if s not in tries:
+            t, o, v = hist_of(s)
+            tries[s] = RadixOracle()
+            tries[s].insert(t, o, v)
+        work.append((s, toks))
+    t0 = time.perf_counter()
+    for s, toks in work:
+        tries[s].insert(toks, [0] * len(toks), [0] * len(toks))
+    dt = time.perf_counter() - t0
+    return {"value": len(work) / dt, "unit": "queries/s", "cores": 1, "kind": "port",
+            "sample": f"{len(work)} queries, pure-Python restatement (oracle/radix.py): baseline/_ref not installed"}
+
+
+def c4_hist_sampler(wl):
+    def hist_of(s):
         a, b = wl.run_off[s], wl.run_off[s + 1]
         st = np.r_[wl.run_start[a:b], wl.hist_len[s]]
         org = np.repeat(wl.run_origin[a:b].astype(np.int64), np.diff(st)).tolist()
         ver = np.repeat(wl.run_version[a:b].astype(np.int64), np.diff(st)).tolist()
-        return org, ver
-
-    tries, qs = {}, []
-    for i in range(min(nq, wl.n_queries)):
-        s = int(wl.q_sess[i])
-        if s not in tries:
-            org, ver = per_token(s)
-            tries[s] = RadixOracle()
-            tries[s].insert(wl.hist_tokens[wl.hist_off[s]: wl.hist_off[s] + wl.hist_len[s]].tolist(), org, ver)
-        q = wl.q_tokens[wl.q_off[i]: wl.q_off[i] + wl.q_len[i]].tolist()
-        qs.append((s, q, [0] * len(q)))
-    t0 = time.perf_counter()
-    for s, q, z in qs:
-        tries[s].insert(q, z, z)
-    dt = time.perf_counter() - t0
-    return {"value": len(qs) / dt, "unit": "queries/s", "cores": 1, "kind": "port",
-            "sample": f"{len(qs)} c4 queries, one lpm_insert each into its session's trie, pure-Python restatement "
-                      "of the reference trie (oracle/radix.py), one process; sessions are independent, so all "
-                      "cores would give at most cores x this"}
+        return wl.hist_tokens[wl.hist_off[s]: wl.hist_off[s] + wl.hist_len[s]].tolist(), org, ver
+    qlist = [(int(wl.q_sess[i]), wl.q_tokens[wl.q_off[i]: wl.q_off[i] + wl.q_len[i]].tolist())
+             for i in range(min(wl.n_queries, 4096))]
+    return hist_of, qlist
 
 
-LINK_PEAK = 670.0  # GB/s per GPU, SM peer reads with both directions busy (tools/p2p_probe, DESIGN.md)
+# ----------------------------------------------------------------------------- reference arm
 
+def run_reference(args):
+    """--impl reference: the CPU implementation of the path on this box's host cores, same
+    config / metric / unit as the b200 arm (rank 0 only; other ranks exit 0)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from workloads import MatchWorkload
 
-def run_c5(args):
-    """Config 5: 1M sessions (log-uniform 1k-128k tokens) sharded by session hash; every
-    rank originates 4096 queries for sessions owned anywhere; Router.match routes them
-    (fused P2P K1 over NVLink).  value = all ranks' queries / max-over-ranks time."""
-    import torch
-    import torch.distributed as dist
+    cores = os.cpu_count() or 1
+    workload = args.workload or ("c5" if world > 1 else "c4")
+    if workload == "c5":
+        from workloads import C5CpuSample
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if not dist.is_initialized():
-        if world == 1:
-            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1, device_id=dev)
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-    from paper_2508_11553_b200 import DeviceStore
-    from paper_2508_11553_b200.routing import Router
-    from workloads import C5Workload
-
-    wl = C5Workload(args.c5_sessions, nranks=world, rank=rank, n_queries=args.queries)
-    owned_tokens = int(((wl.lens[wl.owned] + 31) // 32 * 32).sum())
-    store = DeviceStore(local, arena_words=owned_tokens + (1 << 22), row_capacity=len(wl.owned) + 64,
-                        run_capacity=16 * len(wl.owned) + 64, session_capacity=len(wl.owned) + 16)
-    t0 = time.perf_counter()
-    wl.build_shard(store)
-    build_s = time.perf_counter() - t0
-    tok_need = torch.tensor([int(wl.q_off[-1])], device=dev)
-    dist.all_reduce(tok_need, op=dist.ReduceOp.MAX)
-    router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
-    wl.fill_queries(router)
-    routers = [router]
-    if args.pipeline and world > 1 and args.routing == "fused":
-        # a second region: the next batch is bucketed + packed while this one is matched
-        routers.append(Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()),
-                              g2l=wl.g2l))
-        wl.fill_queries(routers[1])
-    torch.cuda.synchronize()
-    if len(routers) > 1:
-        from paper_2508_11553_b200.routing import match_pipelined
-
-        side = torch.cuda.Stream(dev)
-        run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side)  # noqa: E731
-    else:
-        route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
-                 "nccl": router.match_nccl}[args.routing]
-
-        def run_batches(k):
-            for _ in range(k):
-                route(wl.n_queries)
-    n_warm = max(3, args.warmup, args.steps)  # profiled, so the timed region's event pairs exist
-    store.profile_begin()
-    run_batches(n_warm)
-    torch.cuda.synchronize()
-    store.profile_end("walk")
-    m = np.concatenate([r.out_matched[: wl.n_queries].cpu().numpy() for r in routers])
-    bad = np.flatnonzero(m != np.tile(wl.q_depth, len(routers))) % wl.n_queries
-    if len(bad):
-        print(f"rank {rank}: {len(bad)} mismatches, e.g.", [(int(i), int(m[i]), int(wl.q_depth[i]), int(wl.lens[wl.q_g[i]]),
-              int(wl.q_g[i]), int(wl.owner[wl.q_g[i]])) for i in bad[:8]], file=sys.stderr)
-    assert len(bad) == 0, "routed matched length != constructed depth"
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    stream = torch.cuda.current_stream(dev)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        time.sleep(0.3)
-        t_wall = time.perf_counter()
-        store.profile_begin()
-        # no device-side gate here (unlike c4): routed batches are device-bound (host enqueue
-        # ~50 us per batch vs 280-380 us on the GPU) and a per-rank gate only adds the ranks'
-        # gate-end skew to the routed barriers (profiles/r01_bench_c5_gate_check.txt)
-        e0.record(stream)
-        t_enq = time.perf_counter()
-        run_batches(args.steps)
-        e1.record(stream)
-        t_enq = time.perf_counter() - t_enq
-        torch.cuda.synchronize()
-        walk_ms, walk_n = store.profile_end("walk")
-        phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
-        # keep the clocks sampler running for >= 1 s under load; every rank must make the
-        # same number of (collective) routed calls, so the count is agreed on first
-        left = torch.tensor([max(0.0, 1.0 - (time.perf_counter() - t_wall))], device=dev, dtype=torch.float64)
-        per = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev, dtype=torch.float64)
-        dist.all_reduce(left, op=dist.ReduceOp.MAX)
-        dist.all_reduce(per, op=dist.ReduceOp.MAX)
-        run_batches(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1)
-        torch.cuda.synchronize()
-    elapsed = e0.elapsed_time(e1) / 1e3
-    print(f"[bench] rank {rank}: device-timed region {1e3 * elapsed:.3f} ms for {args.steps} routed batches "
-          f"(host enqueue {1e3 * t_enq:.3f} ms)", file=sys.stderr)
-    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed = float(t.item())
-    L = wl.lens[wl.q_g]
-    cq = np.minimum(np.minimum(wl.q_depth + 1, wl.q_len), L)
-    remote = wl.owner[wl.q_g] != rank
-    stats = torch.tensor([float(cq.sum()), float(cq[remote].sum())], device=dev, dtype=torch.float64)
-    dist.all_reduce(stats)
-    toks, remote_toks = float(stats[0]), float(stats[1])
-    value = world * wl.n_queries * args.steps / elapsed
-    wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
-    peak, peak_kind = peaks()
-    per_gpu_alg = 8.0 * toks / world  # HBM+link bytes per rank per batch (average)
-    line = {
-        "metric": METRIC.replace("c4: 10k sessions x 32k-token histories", "c5: 1M sessions, 1k-128k tokens, routed"),
-        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": n_warm,
-        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "c5", "sessions_total": args.c5_sessions, "history_tokens": "log-uniform [1024, 131072]",
-                   "batch_queries_per_rank": wl.n_queries, "owner": "splitmix64(gsid) mod N",
-                   "routing": {"fused": "fused P2P K1: owners read requester HBM over NVLink, write results back; "
-                                        "device-side epoch-flag barriers (no collective call per batch)",
-                               "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
-                               "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
-                                   args.routing],
-                   "pipelined": len(routers) > 1,
-                   "cross_shard_frac": float(remote.mean()), "shard_build_s": build_s,
-                   "arena_GB_per_rank": owned_tokens * 4 / 1e9},
-        "tokens_compared_per_s": toks * args.steps / elapsed,
-        "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * args.steps / elapsed / 1e9,
-        # bytes that actually cross the links: remote queries move as 18-bit planes (2.25 B per
-        # compared position) unless the exchange is the NCCL baseline (int32)
-        "nvlink_wire_bytes_per_position": wire_b,
-        "nvlink_wire_GBps_per_rank": wire_b * remote_toks / world * args.steps / elapsed / 1e9,
-        "routed_walk_ms_avg_rank0": walk_ms / max(walk_n, 1),
-        "phase_ms_avg_rank0": {k: (ms / n if n else 0.0) for k, (ms, n) in phase_ms.items()},
-        "nvlink_query_GBps_during_walk_rank0": 4.0 * remote_toks / world / (walk_ms / max(walk_n, 1)) / 1e6,
-        "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
-                     "achieved": (wire_b * remote_toks / world if world > 1 else per_gpu_alg) * args.steps / elapsed / 1e9,
-                     "peak": LINK_PEAK if world > 1 else peak, "unit": "GB/s",
-                     "frac": ((wire_b * remote_toks / world) / LINK_PEAK if world > 1 else per_gpu_alg / peak)
-                     * args.steps / elapsed / 1e9,
-                     "peak_kind": "measured SM peer reads per GPU with both directions busy (tools/p2p_probe)"
-                     if world > 1 else peak_kind,
-                     "traffic": None,
-                     "note": "N>1: achieved = bytes on the wire (remote compared positions x nvlink_wire_bytes_per_"
-                             "position) over the whole step; history bytes come from local HBM (tools/p2p_probe: SM "
-                             "peer reads 780 GB/s one direction, 670 GB/s per GPU both directions at once)"},
-        # ours per batch: k_route + k_walk_routed (+ k_route_pack with peers, + k_route_arrive +
-        # k_route_wait_done with device barriers)
-        "gpu_launches": args.steps * ((4 if args.routing == "fused" else 2) + (1 if world > 1 and
-                                                                             args.routing != "nccl" else 0)),
-        "clocks": clk.summary(),
-    }
-    if rank == 0:
+        smp = C5CpuSample(world, n_sessions=10_000, n_queries=args.queries)
+        st, qt, qo = smp.build_port(cores)
+        times = []
+        st.match_batch(smp.q_sess, qt, qo, nthreads=cores)
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            st.match_batch(smp.q_sess, qt, qo, nthreads=cores)
+            times.append(time.perf_counter() - t0)
+        v = smp.n_queries * len(times) / sum(times)
+        line = {"impl": "reference", "metric": METRIC_C5, "value": v, "unit": "queries/s", "n_gpus": world,
+                "steps": len(times), "warmup": 1, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": c5_config(args, world),
+                "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                                 "sample": f"sampled: {smp.n_sessions} of the 1M config-5 sessions (same length law), "
+                                           f"{smp.n_queries}-query batches per step on their sessions, C radix-tree "
+                                           f"restatement (oracle/radix_oracle.c), {cores} threads; the store is one "
+                                           "host's memory, so N GPUs' batches run on the same cores"},
+                "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
-    for r in routers:
-        r.close()
-    store.close()
-    dist.destroy_process_group()
+        return
+    wl = MatchWorkload(args.sessions, args.hist, args.queries)
+    times = []
+    cpu_port_bench_reuse(wl, cores)  # warm: build the C store + one pass
+    for _ in range(max(1, args.steps)):
+        _, dt, _ = cpu_port_bench_reuse(wl, cores)
+        times.append(dt)
+    total = sum(times)
+    v = wl.n_queries * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
+        "steps": len(times), "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": c4_config(args, world),
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                         "sample": f"full c4 batch ({wl.n_queries} queries) per step, C radix-tree restatement "
+                                   f"(oracle/radix_oracle.c), {cores} threads"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    if not args.no_cpu and args.sessions >= 1000:
+        hist_of, qlist = c4_hist_sampler(wl)
+        line["reference_unmodified"] = reference_match_sample(hist_of, qlist)
+    print(json.dumps(line))
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    if args.workload == "c5":
-        run_c5(args)
-        return
+# ------------------------------------------------------------------------------- c4 (N = 1)
+
+def measure_c4(args, rank, world, local, dev):
     import torch
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
     from paper_2508_11553_b200 import DeviceStore
     from workloads import SEED0, MatchWorkload
 
     mixed = tuple(int(x) for x in args.mixed.split(",")) if args.mixed else None
+    t0 = time.perf_counter()
     wl = MatchWorkload(args.sessions, args.hist, args.queries, seed=SEED0 + 4 + 1000 * rank, mixed=mixed)
     store = DeviceStore(local, arena_words=int(wl.hist_off[-1]) + (1 << 20), row_capacity=args.sessions + 64,
                         run_capacity=len(wl.run_start) + 64, session_capacity=args.sessions + 16)
@@ -410,6 +318,7 @@ def main():
                               wl.hist_len, wl.run_off, wl.run_start, wl.run_origin, wl.run_version)
     assert np.all(rec.matched == 0) and np.all(rec.added == wl.hist_len)
     row_len = wl.hist_len  # row id == session id here (one row per session, recorded in order)
+    log(f"rank {rank}: c4 store built in {time.perf_counter() - t0:.1f} s")
 
     # two device-resident batches with different queries (A is the workload's own batch);
     # consecutive steps alternate A / B so no batch re-reads what the previous one did
@@ -422,15 +331,12 @@ def main():
 
     dq = [to_dev(q) for q in qsets]
     om = torch.empty(wl.n_queries, dtype=torch.int64, device=dev)
-    op = torch.empty_like(om)
-    od = torch.empty_like(om)
     # Batches are independent and read-only, so consecutive batches alternate between two
-    # streams (each its own output buffers): batch k+1's planner and ramp-up overlap batch
-    # k's tail.  Timing events go on stream 0 after it has waited for stream 1.
+    # streams (each its own output buffers): batch k+1's ramp-up overlaps batch k's tail.
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     stream = streams[0]
     torch.cuda.set_stream(stream)
-    outs = [(om, op, od), tuple(torch.empty_like(om) for _ in range(3))]
+    outs = [(om, torch.empty_like(om), torch.empty_like(om)), tuple(torch.empty_like(om) for _ in range(3))]
     nstep = [0]
 
     def step():
@@ -439,22 +345,15 @@ def main():
         o = outs[i]
         store.match_device(*dq[i], o[0], o[1], o[2], stream=streams[i].cuda_stream)
 
-    def join():
-        streams[0].wait_stream(streams[1])
-
-    # warm-up runs under the store's launch profiler too, at least K steps, so the per-launch
-    # event pairs the timed region records already exist (creating them inside the timed
-    # region stalled the enqueue by tens of ms on a 4-rank box)
-    n_warm = max(3, args.warmup, args.steps)
-    store.profile_begin()
-    for _ in range(n_warm):
+    # exactly W warm-up steps; the launch profiler's event pairs for the timed region are
+    # created up front (cudaEventCreate inside the timed region made N>1 host-bound)
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    store.profile_end("walk")
     nstep[0] = 0
-    # correctness of the benchmarked batch (size-independent properties)
+    # correctness of the benchmarked batches (size-independent truth) and their bytes
     alg = []
-    for i in range(2):  # check both batches (size-independent truth) and count their bytes
+    for i in range(2):
         m = outs[i][0].cpu().numpy()
         par = outs[i][1].cpu().numpy()
         assert np.array_equal(m, qsets[i]["q_depth"]), "matched length != constructed depth"
@@ -468,28 +367,32 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    store.profile_begin()
+    store.profile_begin(reserve=args.steps + 64)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         time.sleep(0.3)  # let the sampler start before the timed region
         t_wall = time.perf_counter()
         # Device-side gate before e0: the host enqueues all K steps while the GPU spins, so
-        # the events time the steps back to back and not the host's launch jitter (with
-        # small K under torchrun a late first launch on one rank otherwise sets the max).
+        # the events time the steps back to back and not the host's launch jitter.
         if os.environ.get("BENCH_GATE", "1") != "0":
             torch.cuda._sleep(int(1.9e6 * min(1000.0, 20.0 + 2.0 * args.steps)))
+        prof = os.environ.get("BENCH_PROFILE_RANGE") == "1"  # ncu --replay-mode range over exactly this region
+        if prof:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         e0.record(stream)
         streams[1].wait_stream(streams[0])
         t_enq = time.perf_counter()
         for _ in range(args.steps):
             step()
-        join()
+        streams[0].wait_stream(streams[1])
         e1.record(stream)
         t_enq = time.perf_counter() - t_enq
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         walk_ms, walk_n = store.profile_end("walk")
-        phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
         plan_ms, plan_n = store.profile_end("plan")
         # short regions: keep the identical load running so the sampler sees >= 1 s of it
         while time.perf_counter() - t_wall < 1.0:
@@ -497,14 +400,13 @@ def main():
                 step()
             torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
-    print(f"[bench] rank {rank}: device-timed region {1e3 * elapsed:.3f} ms for {args.steps} steps "
-          f"(walk {walk_ms:.3f} ms over {walk_n} launches; host enqueue {1e3 * t_enq:.3f} ms)", file=sys.stderr)
+    log(f"rank {rank}: c4 device-timed region {1e3 * elapsed:.3f} ms for {args.steps} steps (walk {walk_ms:.3f} ms "
+        f"over {walk_n} launches; host enqueue {1e3 * t_enq:.3f} ms)")
     if world > 1:
         t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(t.item())
     value = world * wl.n_queries * args.steps / elapsed
-    wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
     toks_per_s = world * float(cq.sum()) * args.steps / elapsed
 
     # e2e: the public host-buffer API, pinned inputs, copies inside the timed region
@@ -529,10 +431,21 @@ def main():
     # DESIGN.md "PCIe path") + the per-query session ids, offsets and lengths
     h2d = (store.h2d_stats()["token_bytes"] - tok_bytes0) // args.e2e_steps + wl.n_queries * (4 + 8 + 8)
     d2h = wl.n_queries * 24
+    # e2e from Python-list callers (the reference's own argument type): tokens as lists
+    lists = None
+    if world == 1 and not args.no_cpu:
+        qtl = [wl.q_tokens[wl.q_off[i]: wl.q_off[i] + wl.q_len[i]].tolist() for i in range(wl.n_queries)]
+        t0 = time.perf_counter()
+        mh2, _, _ = store.match_lists(wl.q_sess, qtl)
+        dt_l = time.perf_counter() - t0
+        assert np.array_equal(mh2, wl.q_depth)
+        lists = {"value": wl.n_queries / dt_l, "unit": "queries/s",
+                 "note": "one batch of Python int lists (the reference's lpm_insert argument type) through "
+                         "DeviceStore.match_lists: list -> int32 conversion and PCIe inside the timed call"}
 
     peak, peak_kind = peaks()
     traffic = None
-    try:  # DRAM bytes per k_walk launch from the committed ncu --set full capture of this workload
+    try:  # DRAM bytes per K1 launch from the committed ncu capture of this command (profiles/traffic.json)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get("k_walk:c4")
         if tr and args.sessions == 10_000 and args.hist == 32_768 and args.queries == 4096:
@@ -546,15 +459,17 @@ def main():
     achieved = alg_bytes / k_avg / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-        "warmup": n_warm, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": c4_config(args, world, wl, mixed),
+        "config": c4_config(args, world, mixed),
         "tokens_compared_per_s": toks_per_s,
         "alg_GBps": world * alg_bytes * args.steps / elapsed / 1e9,
         "roofline": {"bound": "hbm", "kernel": "k_walk_tma", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0,
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": k_avg * 1e3, "traffic": traffic,
-                     "kernel_time_basis": "timed region / batches (batches overlap on 2 streams; includes planner)",
+                     "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per k_walk_tma "
+                                       "launch, ncu --set full of this command (profiles/r02_*)",
+                     "kernel_time_basis": "timed region / batches (batches overlap on 2 streams)",
                      "event_ms_avg_per_launch": walk_ms / max(walk_n, 1),
                      "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -565,6 +480,8 @@ def main():
                    "CUDA events on the launching stream around K steps as launched; max over ranks"),
         "clocks": clk.summary(),
     }
+    if lists:
+        line["e2e_python_lists"] = lists
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
         n, dt, res = cpu_port_bench_reuse(wl, cores)
@@ -574,11 +491,360 @@ def main():
         line["cpu_baseline"] = {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
                                 "sample": f"full c4 batch ({n} queries), best of 2, C radix-tree restatement "
                                           f"(oracle/radix_oracle.c), {cores} threads"}
-        if args.sessions == 10_000 and not args.mixed:
-            line["reference_python_sample"] = python_reference_sample(wl)
+        if args.sessions >= 1000 and not args.mixed:
+            hist_of, qlist = c4_hist_sampler(wl)
+            line["reference_unmodified"] = reference_match_sample(hist_of, qlist)
+    store.close()
+    _cpu_store.clear()
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
+    return line
+
+
+# ------------------------------------------------------------------------- c1-c3 (N = 1)
+
+def measure_config(cfg, reps=3, with_cpu=True):
+    """Record (K2 = k_record + k_record_copy), export (K3), NDJSON and - c3 - the
+    include_partials export on one BASELINE config, device time (CUDA events around the
+    launches) and call time (host arrays through the C ABI), with rooflines."""
+    import torch
+
+    from paper_2508_11553_b200 import DeviceStore
+    from workloads import RecordWorkload
+
+    peak, _ = peaks()
+    wl = RecordWorkload(cfg)
+    sids, tok, off, roff, rs, ro, rv = wl.packed()
+    lens = np.diff(off)
+    pad = (lens + 31) // 32 * 32
+    aoff = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(pad, out=aoff[1:])
+    atok = np.zeros(int(aoff[-1]), np.int32)
+    for k in range(len(lens)):
+        atok[aoff[k]: aoff[k] + lens[k]] = tok[off[k]: off[k + 1]]
+    dtok = torch.from_numpy(atok).cuda()
+    n_rec = len(lens)
+    store = DeviceStore(0, arena_words=(2 * reps + 3) * int(aoff[-1]) + (1 << 22), row_capacity=(2 * reps + 3) * n_rec + 64,
+                        run_capacity=(2 * reps + 3) * len(rs) + 64, session_capacity=(2 * reps + 3) * wl.n_sessions + 16)
+    store.profile_begin(reserve=64)
+    best: dict = {}
+
+    def keep(k, v):
+        best[k] = min(best.get(k, v), v)
+
+    rng = np.random.default_rng(20251021)
+    paused = np.sort(rng.choice(wl.n_sessions, wl.n_sessions // 10, replace=False)) if cfg == 3 else None
+    for rep in range(reps + 1):
+        smap = [store.new_session() for _ in range(wl.n_sessions)]
+        g_sids = np.asarray([smap[s] for s in sids], np.int32)
+        torch.cuda.synchronize()
+        store.profile_begin()
+        t0 = time.perf_counter()
+        r = store.record_device(g_sids, dtok, aoff[:-1], lens, roff, rs, ro, rv)
+        t_dev_call = time.perf_counter() - t0
+        k2_ms, _ = store.profile_end("commit")
+        cp_ms, _ = store.profile_end("record_copy")
+        # the same records through the host-array call (PCIe inside), into fresh sessions
+        smap2 = [store.new_session() for _ in range(wl.n_sessions)]
+        g2 = np.asarray([smap2[s] for s in sids], np.int32)
+        t0 = time.perf_counter()
+        store.record_packed(g2, tok, off[:-1], lens, roff, rs, ro, rv)
+        t_call = time.perf_counter() - t0
+        rows = np.asarray(r.row, np.int64) if cfg != 1 else np.asarray(store.session_rows(smap[0], "lex"), np.int64)
+        n_out = int(store.rows_total(rows))
+        torch.cuda.synchronize()
+        store.profile_begin()
+        t0 = time.perf_counter()
+        p = store.export_device(rows)
+        torch.cuda.synchronize()
+        t_exp_dev = time.perf_counter() - t0
+        ex_ms, _ = store.profile_end("export")
+        t0 = time.perf_counter()
+        store.export(rows, total=n_out)
+        t_exp_host = time.perf_counter() - t0
+        names = [f"sess-{int(s)}" for s in sids] if cfg != 1 else ["sess-0"] * len(rows)
+        t0 = time.perf_counter()
+        text = store.export_ndjson(rows, names, as_array=True)
+        t_json = time.perf_counter() - t0
+        part = None
+        if cfg == 3:  # 10 % of the sessions paused inside turn 2: completed rows + partials
+            keep_rows, host_rows = [], []
+            pset = set(paused.tolist())
+            for s in range(wl.n_sessions):
+                keep_rows.append(int(r.row[2 * s]))
+                if s in pset:
+                    t2 = wl.seqs[2 * s + 1]
+                    k = wl.split[s]
+                    host_rows.append((t2[: 2560 + k], 2560, 0, [0] * k))
+                else:
+                    keep_rows.append(int(r.row[2 * s + 1]))
+            torch.cuda.synchronize()
+            store.profile_begin()
+            t0 = time.perf_counter()
+            pp = store.export_device_with_host_rows(keep_rows, host_rows)
+            torch.cuda.synchronize()
+            t_part = time.perf_counter() - t0
+            part_ms, _ = store.profile_end("export")
+            part = (t_part, part_ms, int(pp.offsets[-1]), len(keep_rows) + len(host_rows),
+                    sum(len(h[0]) for h in host_rows))
+        del p
+        if rep == 0:
+            continue  # warm-up
+        keep("k2_ms", k2_ms + cp_ms)
+        keep("k_record_ms", k2_ms)
+        keep("copy_ms", cp_ms)
+        keep("t_dev_call", t_dev_call)
+        keep("t_call", t_call)
+        keep("ex_ms", ex_ms)
+        keep("t_exp_dev", t_exp_dev)
+        keep("t_exp_host", t_exp_host)
+        keep("t_json", t_json)
+        if part:
+            keep("t_part", part[0])
+            keep("part_ms", part[1])
+    m = r.matched.astype(np.int64)
+    # |parent| per record: lengths of each session's rows by local ordinal (rows are new in order)
+    by_local: dict = {}
+    plen = np.zeros(n_rec, np.int64)
+    for k in range(n_rec):
+        rows_s = by_local.setdefault(int(sids[k]), [])
+        if r.parent_local[k] >= 0:
+            plen[k] = rows_s[int(r.parent_local[k])]
+        if int(r.local[k]) == len(rows_s):
+            rows_s.append(int(lens[k]))
+    cq = np.where(r.parent_local >= 0, np.minimum(np.minimum(m + 1, lens), plen), 0)
+    novel = (lens - m).astype(np.float64)
+    rec_bytes = float((8 * cq + 8 * novel).sum())
+    exp_bytes = 13.0 * n_out + 8.0 * len(rows)
+
+    def roof(nbytes, ms, kernel):
+        a = nbytes / ms / 1e6
+        return {"bound": "hbm", "kernel": kernel, "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak,
+                "alg_bytes": nbytes}
+
+    out = {
+        "records": n_rec, "sessions": wl.n_sessions, "record_tokens": int(lens.sum()), "novel_tokens": int(novel.sum()),
+        "record": {"device_ms": best["k2_ms"], "k_record_ms": best["k_record_ms"], "k_record_copy_ms": best["copy_ms"],
+                   "records_per_s_device": n_rec / best["k2_ms"] * 1e3,
+                   "call_ms_device_tokens": 1e3 * best["t_dev_call"], "call_ms_host_arrays": 1e3 * best["t_call"],
+                   "records_per_s_call": n_rec / best["t_call"],
+                   "roofline": roof(rec_bytes, best["k2_ms"], "k_record_tma + k_record_copy")},
+        "export": {"rows": int(len(rows)), "tokens": n_out, "device_ms": best["ex_ms"],
+                   "call_ms_device_out": 1e3 * best["t_exp_dev"], "call_ms_host_out": 1e3 * best["t_exp_host"],
+                   "host_GBps": 9.0 * n_out / best["t_exp_host"] / 1e9,
+                   "roofline": roof(exp_bytes, best["ex_ms"], "k_export_plan + k_export_tma")},
+        "ndjson": {"call_ms": 1e3 * best["t_json"], "bytes": int(len(text)), "tokens_per_s": n_out / best["t_json"]},
+    }
+    if cfg == 3:
+        _, _, ptok, prow, htok = part
+        out["export_include_partials"] = {
+            "rows": prow, "tokens": ptok, "partial_rows": len(paused), "partial_tokens": htok,
+            "device_ms": best["part_ms"], "call_ms": 1e3 * best["t_part"],
+            "roofline": roof(13.0 * ptok + 8.0 * prow, best["part_ms"], "k_export_tma + k_fill_host_rows"),
+            "note": "10 % of the sessions paused inside turn 2: their turn-1 rows from the store plus the open "
+                    "request (input + first leg) assembled on the GPU (trajectory.py:317-340)"}
+    store.close()
+    if with_cpu:
+        from tools.refbench import time_port_records, time_reference_records
+
+        cores = os.cpu_count() or 1
+        port, _ = time_port_records(wl, cores)
+        out["cpu_baseline"] = {"value": port["records_per_s"], "unit": "records/s", "cores": cores, "kind": "port",
+                               "export_tokens_per_s": port["export_tokens_per_s"],
+                               "sample": f"all {n_rec} records then every row exported, C restatement "
+                                         f"(oracle/radix_oracle.c), {cores} threads"}
+        n1 = {1: 1, 2: 4, 3: 40}[cfg]
+        refd = time_reference_records(wl, n1, n1 * cores)
+        if refd is not None:
+            out["reference_unmodified"] = dict(refd, unit="records/s and tokens/s", kind="reference",
+                                               sample="sessions of this config recorded in order (lpm_insert), then "
+                                                      "extract() and trajectory_to_line, unmodified rolloutlab from "
+                                                      "baseline/_ref: one process, and a pool over all cores")
+    return out
+
+
+# ------------------------------------------------------------------------------------- c5
+
+def measure_c5(args, steps, warmup):
+    """Config 5: 1M sessions (log-uniform 1k-128k tokens) sharded by session hash; every
+    rank originates 4096 queries for sessions owned anywhere; Router.match routes them
+    (fused P2P K1 over NVLink).  value = all ranks' queries / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    own_pg = False
+    if not dist.is_initialized():
+        own_pg = True
+        if world == 1:
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1, device_id=dev)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    from paper_2508_11553_b200 import DeviceStore
+    from paper_2508_11553_b200.routing import Router
+    from workloads import C5Workload
+
+    wl = C5Workload(args.c5_sessions, nranks=world, rank=rank, n_queries=args.queries)
+    owned_tokens = int(((wl.lens[wl.owned] + 31) // 32 * 32).sum())
+    store = DeviceStore(local, arena_words=owned_tokens + (1 << 22), row_capacity=len(wl.owned) + 64,
+                        run_capacity=16 * len(wl.owned) + 64, session_capacity=len(wl.owned) + 16)
+    t0 = time.perf_counter()
+    wl.build_shard(store)
+    build_s = time.perf_counter() - t0
+    log(f"rank {rank}: c5 shard ({len(wl.owned)} sessions, {owned_tokens * 4 / 1e9:.1f} GB) built in {build_s:.1f} s")
+    tok_need = torch.tensor([int(wl.q_off[-1])], device=dev)
+    dist.all_reduce(tok_need, op=dist.ReduceOp.MAX)
+    router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
+    wl.fill_queries(router)
+    routers = [router]
+    if args.pipeline and world > 1 and args.routing == "fused":
+        # a second region: the next batch is bucketed + packed while this one is matched
+        routers.append(Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()),
+                              g2l=wl.g2l))
+        wl.fill_queries(routers[1])
+    torch.cuda.synchronize()
+    if len(routers) > 1:
+        from paper_2508_11553_b200.routing import match_pipelined
+
+        side = torch.cuda.Stream(dev)
+        run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side)  # noqa: E731
+    else:
+        route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
+                 "nccl": router.match_nccl}[args.routing]
+
+        def run_batches(k):
+            for _ in range(k):
+                route(wl.n_queries)
+    run_batches(warmup)
+    torch.cuda.synchronize()
+    m = np.concatenate([r.out_matched[: wl.n_queries].cpu().numpy() for r in routers])
+    bad = np.flatnonzero(m != np.tile(wl.q_depth, len(routers))) % wl.n_queries
+    if len(bad):
+        print(f"rank {rank}: {len(bad)} mismatches, e.g.", [(int(i), int(m[i]), int(wl.q_depth[i])) for i in bad[:8]],
+              file=sys.stderr)
+    assert len(bad) == 0, "routed matched length != constructed depth"
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream(dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    store.profile_begin(reserve=steps + 64)
+    with Clocks(local) as clk:
+        time.sleep(0.3)
+        t_wall = time.perf_counter()
+        # no device-side gate here (unlike c4): routed batches are device-bound (host enqueue
+        # ~50 us per batch vs 280-380 us on the GPU) and a per-rank gate only adds the ranks'
+        # gate-end skew to the routed barriers (profiles/r01_bench_c5_gate_check.txt)
+        e0.record(stream)
+        t_enq = time.perf_counter()
+        run_batches(steps)
+        e1.record(stream)
+        t_enq = time.perf_counter() - t_enq
+        torch.cuda.synchronize()
+        walk_ms, walk_n = store.profile_end("walk")
+        phase_ms = {k: store.profile_end(k) for k in ("route", "route_pack", "route_wait")}
+        # keep the clocks sampler running for >= 1 s under load; every rank must make the
+        # same number of (collective) routed calls, so the count is agreed on first
+        left = torch.tensor([max(0.0, 1.0 - (time.perf_counter() - t_wall))], device=dev, dtype=torch.float64)
+        per = torch.tensor([e0.elapsed_time(e1) / 1e3 / steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(left, op=dist.ReduceOp.MAX)
+        dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        run_batches(int(float(left.item()) / max(float(per.item()), 1e-6)) + 1)
+        torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    log(f"rank {rank}: c5 device-timed region {1e3 * elapsed:.3f} ms for {steps} routed batches "
+        f"(host enqueue {1e3 * t_enq:.3f} ms)")
+    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    L = wl.lens[wl.q_g]
+    cq = np.minimum(np.minimum(wl.q_depth + 1, wl.q_len), L)
+    remote = wl.owner[wl.q_g] != rank
+    stats = torch.tensor([float(cq.sum()), float(cq[remote].sum()), float(remote.mean())], device=dev,
+                         dtype=torch.float64)
+    dist.all_reduce(stats)
+    toks, remote_toks, xfrac = float(stats[0]), float(stats[1]), float(stats[2]) / world
+    value = world * wl.n_queries * steps / elapsed
+    wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
+    peak, peak_kind = peaks()
+    per_gpu_alg = 8.0 * toks / world  # HBM+link bytes per rank per batch (average)
+    line = {
+        "metric": METRIC_C5, "value": value, "unit": "queries/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": 1e3 * elapsed / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": c5_config(args, world),
+        "cross_shard_frac": xfrac, "shard_build_s": build_s, "arena_GB_per_rank": owned_tokens * 4 / 1e9,
+        "tokens_compared_per_s": toks * steps / elapsed,
+        "alg_GBps_per_rank": per_gpu_alg * steps / elapsed / 1e9,
+        "nvlink_query_GBps_per_rank": 4.0 * remote_toks / world * steps / elapsed / 1e9,
+        # bytes that actually cross the links: remote queries move as 18-bit planes (2.25 B per
+        # compared position) unless the exchange is the NCCL baseline (int32)
+        "nvlink_wire_bytes_per_position": wire_b,
+        "nvlink_wire_GBps_per_rank": wire_b * remote_toks / world * steps / elapsed / 1e9,
+        "routed_walk_ms_avg_rank0": walk_ms / max(walk_n, 1),
+        "phase_ms_avg_rank0": {k: (ms / n if n else 0.0) for k, (ms, n) in phase_ms.items()},
+        "roofline": {"bound": "nvlink" if world > 1 else "hbm", "kernel": "k_walk_routed",
+                     "achieved": (wire_b * remote_toks / world if world > 1 else per_gpu_alg) * steps / elapsed / 1e9,
+                     "peak": LINK_PEAK if world > 1 else peak, "unit": "GB/s",
+                     "frac": ((wire_b * remote_toks / world) / LINK_PEAK if world > 1 else per_gpu_alg / peak)
+                     * steps / elapsed / 1e9,
+                     "peak_kind": "measured SM peer reads per GPU with both directions busy (tools/p2p_probe)"
+                     if world > 1 else peak_kind,
+                     "hbm_frac": per_gpu_alg * steps / elapsed / 1e9 / peak,
+                     "traffic": None,
+                     "note": "N>1: achieved = bytes on the wire (remote compared positions x nvlink_wire_bytes_per_"
+                             "position) over the whole step; history bytes come from local HBM (tools/p2p_probe: SM "
+                             "peer reads 780 GB/s one direction, 670 GB/s per GPU both directions at once)"},
+        # ours per batch: k_route + k_walk_routed (+ k_route_pack with peers, + k_route_arrive +
+        # k_route_wait_done with device barriers)
+        "gpu_launches": steps * ((4 if args.routing == "fused" else 2) + (1 if world > 1 and
+                                                                        args.routing != "nccl" else 0)),
+        "clocks": clk.summary(),
+        "timing": "CUDA events on the launching stream around K routed batches; max over ranks",
+    }
+    for r in routers:
+        r.close()
+    store.close()
+    if own_pg:
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    workload = args.workload or ("c5" if world > 1 else "c4")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    if workload == "c5":
+        line = measure_c5(args, args.steps, args.warmup)
+        if world > 1:  # the host-routed weak-scaling shards beside it (every rank its own c4 shard)
+            line["c4_shards"] = {k: v for k, v in measure_c4(args, rank, world, local, dev).items()
+                                 if k in ("value", "ms_per_step", "config", "roofline", "e2e", "tokens_compared_per_s")}
+    else:
+        line = measure_c4(args, rank, world, local, dev)
+        if world == 1 and not args.no_configs:
+            line["configs"] = {}
+            for cfg in (1, 2, 3):
+                t0 = time.perf_counter()
+                line["configs"][f"c{cfg}"] = measure_config(cfg, with_cpu=not args.no_cpu)
+                log(f"c{cfg} record/export measured in {time.perf_counter() - t0:.1f} s")
+        if world == 1 and not args.no_c5:
+            c5 = measure_c5(args, args.steps, args.warmup)
+            line["c5_routed"] = {k: c5[k] for k in ("value", "unit", "ms_per_step", "config", "roofline",
+                                                    "tokens_compared_per_s", "shard_build_s", "arena_GB_per_rank")}
     if rank == 0:
         print(json.dumps(line))
-    store.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -124,6 +124,22 @@ int tm_export_rows(tm_store *store, int64_t n, const int64_t *rows, int32_t mem_
                    int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
                    void *stream);
 
+/* Rows that live on the host - open or paused requests exported with include_partials
+ * (TrajectoryManager._partial_trajectory, trajectory.py:329-340) - written into a packed
+ * DEVICE batch next to rows exported by tm_export_rows:
+ *   row k = tokens[tok_off[k] : tok_off[k+1]] (host array): the first n_input[k] positions
+ *   are AGENT_INPUT at ctx_version[k]; the rest MODEL_OUTPUT, versions given as runs
+ *   run_start[run_off[k] : run_off[k+1]] (relative to the row; the first equals n_input[k])
+ *   with run_version[...]
+ *   out_off[k]   where row k starts in out_tokens / out_mask / out_versions (device)
+ *   out_resp_start[k] (device, may be NULL) = n_input[k]
+ * Asynchronous on `stream`.  Errors: non-parallel runs -> TM_EINVAL. */
+int tm_export_host_rows(tm_store *store, int64_t n, const int32_t *tokens, const int64_t *tok_off,
+                        const int64_t *n_input, const int32_t *ctx_version, const int64_t *run_off,
+                        const int32_t *run_start, const int32_t *run_version, const int64_t *out_off,
+                        int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
+                        void *stream);
+
 /* Canonical NDJSON of rows, formatted on the GPU and byte-identical to
  * "".join(trajectory_to_line(t) + "\n") (core.py:182-183; the /traj/export payload of
  * api.py:248-254).  sid_json/sid_off[n+1]: per row, the session id as a JSON string
@@ -223,6 +239,9 @@ enum {
   TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6, TM_KERNEL_RECORD_COPY = 7
 };
 int tm_profile_begin(tm_store *store);
+/* Create the event pairs of `pairs` launches per kernel kind up front (so a timed region
+ * never calls cudaEventCreate). */
+int tm_profile_reserve(tm_store *store, int64_t pairs);
 int tm_profile_end(tm_store *store, int32_t kind, double *total_ms, int64_t *launches);
 
 /* Block until all work queued on the store's stream is done. */

@@ -39,6 +39,7 @@ SIGNATURES = {
     "tm_export_rows": (C.c_int, [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "tm_session_stats": (C.c_int, [_P, _I32, _P, _P, _P]),
     "tm_export_ndjson": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _P, _P]),
+    "tm_export_host_rows": (C.c_int, [_P, _I64] + [_P] * 13),
     "tm_session_rows": (C.c_int, [_P, _I32, _I32, _P, _I64, _P]),
     "tm_row_info": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "tm_store_stats": (C.c_int, [_P, _P, _P, _P, _P]),
@@ -47,6 +48,7 @@ SIGNATURES = {
     "tm_store_h2d_stats": (C.c_int, [_P, _P]),
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
+    "tm_profile_reserve": (C.c_int, [_P, _I64]),
     "tm_store_save": (C.c_int, [_P, C.c_char_p]),
     "tm_store_load": (C.c_int, [_P, C.c_char_p]),
     "tm_route_desc_bytes": (C.c_int, [_P]),

@@ -2004,6 +2004,40 @@ cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms
   return cudaGetLastError();
 }
 
+// Rows that live on the host - open / paused requests (trajectory.py:329-340): the input
+// span at the request's context version, then MODEL_OUTPUT runs by version.  One CTA per
+// row (grid-stride): tokens move from the staged copy into the packed outputs, mask and
+// versions are written from the row's few runs.
+__global__ void __launch_bounds__(256) k_fill_host_rows(HostRowsArgs a) {
+  for (int64_t k = blockIdx.x; k < a.n; k += gridDim.x) {
+    const int64_t t0 = a.tok_off[k], L = a.tok_off[k + 1] - t0, o = a.out_off[k], ni = a.n_input[k];
+    const int32_t cv = a.ctx_version[k];
+    const int64_t r0 = a.run_off[k], r1 = a.run_off[k + 1];
+    for (int64_t p = threadIdx.x; p < L; p += blockDim.x) {
+      a.tokens[o + p] = a.src[t0 + p];
+      a.mask[o + p] = p >= ni ? 1 : 0;
+      int32_t ver = cv;
+      if (p >= ni) {  // last run starting at or before p (runs ascend; a row has a handful)
+        int64_t lo = r0, hi = r1;
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (a.run_start[mid] <= p) lo = mid; else hi = mid;
+        }
+        ver = a.run_version[lo];
+      }
+      a.versions[o + p] = ver;
+    }
+    if (a.resp && threadIdx.x == 0) a.resp[k] = ni;  // 1 + the last AGENT_INPUT position
+  }
+}
+
+cudaError_t launch_fill_host_rows(const HostRowsArgs &a, int num_sms, cudaStream_t s) {
+  if (a.n < 1) return cudaSuccess;
+  const int64_t grid = std::min<int64_t>(a.n, (int64_t)num_sms * 8);
+  k_fill_host_rows<<<(int)grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 int64_t export_plan_bytes(int64_t ntiles) {
   return ntiles * (int64_t)sizeof(TilePlan);
 }

@@ -22,6 +22,24 @@ struct ExportArgsHost {
 };
 int64_t export_plan_bytes(int64_t ntiles);
 
+// rows that live on the host (open / paused requests): tokens already in device memory
+struct HostRowsArgs {
+  int64_t n;
+  const int32_t *src;        // tokens, row k at src[tok_off[k] .. tok_off[k+1])
+  const int64_t *tok_off;    // n + 1
+  const int64_t *n_input;    // n: AGENT_INPUT prefix length
+  const int32_t *ctx_version;// n: version of the input prefix
+  const int64_t *run_off;    // n + 1: version runs of the MODEL_OUTPUT part
+  const int32_t *run_start;  // relative to the row
+  const int32_t *run_version;
+  const int64_t *out_off;    // n: where row k starts in the outputs
+  int32_t *tokens;
+  uint8_t *mask;
+  int32_t *versions;
+  int64_t *resp;             // n, may be null
+};
+cudaError_t launch_fill_host_rows(const HostRowsArgs &a, int num_sms, cudaStream_t s);
+
 // expand 18-bit split planes (hostpack.h) into int32 tokens for positions [p0, p1)
 // (multiples of 32)
 cudaError_t launch_unpack18(const uint16_t *lo, const uint8_t *hi, int32_t *out, int64_t p0, int64_t p1, int num_sms,

@@ -86,10 +86,24 @@ struct DevBytes {
   ~DevBytes() { if (p) cudaFree(p); }
 };
 
+// Pinned staging buffer.  Asynchronous calls return while a host->device copy out of the
+// buffer may still be queued: mark() records the copy, and the next need() waits for it
+// before the buffer is rewritten.
 struct PinBytes {
   void *p = nullptr;
   size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+  void mark(cudaStream_t st) {
+    if (!ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(ev, st), "cudaEventRecord(staging)");
+    pending = true;
+  }
   void *need(size_t n) {
+    if (pending) {
+      ck(cudaEventSynchronize(ev), "staging reuse");
+      pending = false;
+    }
     if (n > cap) {
       if (p) cudaFreeHost(p);
       p = nullptr;
@@ -99,7 +113,10 @@ struct PinBytes {
     }
     return p;
   }
-  ~PinBytes() { if (p) cudaFreeHost(p); }
+  ~PinBytes() {
+    if (p) cudaFreeHost(p);
+    if (ev) cudaEventDestroy(ev);
+  }
 };
 
 // lay out several arrays in one buffer
@@ -582,6 +599,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
     memset(h + doff[k] + L, 0, sizeof(int32_t) * (size_t)pad);
   }
   if (total > 0) ck(cudaMemcpyAsync(d, h, sizeof(int32_t) * total, cudaMemcpyHostToDevice, st), "H2D tokens");
+  s->ptok.mark(st);
 }
 
 // Lexicographic order of the subtree of row r.  kids[local] =
@@ -1063,6 +1081,7 @@ int tm_match_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, con
       memcpy(h + o_off, doff.data(), 8 * n);
       memcpy(h + o_len, tok_len, 8 * n);
       ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D batch");
+      s->pin.mark(st);
       b.sids = (const int32_t *)(d + o_sid);
       b.tok = (const int32_t *)s->dtok.p;
       b.off = (const int64_t *)(d + o_off);
@@ -1163,6 +1182,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
     memcpy(h + o_off, out_offsets, 8 * (n + 1));
     memcpy(h + o_tile, tile.data(), 8 * (n + 1));
     ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D export plan");
+    s->pin.mark(st);
     tms::ExportArgsHost e{};
     e.n = n;
     e.rows = (const int64_t *)(d + o_rows);
@@ -1211,6 +1231,74 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
   });
 }
 
+int tm_export_host_rows(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *tok_off,
+                        const int64_t *n_input, const int32_t *ctx_version, const int64_t *run_off,
+                        const int32_t *run_start, const int32_t *run_version, const int64_t *out_off,
+                        int32_t *out_tokens, uint8_t *out_mask, int32_t *out_versions, int64_t *out_resp_start,
+                        void *stream) {
+  NvtxRange nvtx_("tm_export_host_rows");
+  return guarded(s, [&] {
+    if (n < 0) fail(TM_EINVAL, "negative batch size");
+    if (n == 0) return;
+    if (!out_tokens || !out_mask || !out_versions) fail(TM_EINVAL, "device output arrays required");
+    const int64_t total = tok_off[n] - tok_off[0];
+    for (int64_t k = 0; k < n; k++) {
+      const int64_t L = tok_off[k + 1] - tok_off[k];
+      if (L < 0 || n_input[k] < 0 || n_input[k] > L) fail(TM_EINVAL, "bad row extent");
+      const int64_t r0 = run_off[k], r1 = run_off[k + 1];
+      if (L > n_input[k] && (r1 <= r0 || run_start[r0] != n_input[k]))
+        fail(TM_EINVAL, "tokens, origins, versions must be parallel");
+      for (int64_t r = r0 + 1; r < r1; r++)
+        if (run_start[r] <= run_start[r - 1] || run_start[r] >= L) fail(TM_EINVAL, "tokens, origins, versions must be parallel");
+    }
+    const int64_t nruns = run_off[n] - run_off[0];
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    wait_prev(s, st);
+    Layout lay;
+    size_t o_tok = lay.add(4 * (size_t)std::max<int64_t>(total, 1)), o_toff = lay.add(8 * (n + 1)),
+           o_nin = lay.add(8 * n), o_cv = lay.add(4 * n), o_roff = lay.add(8 * (n + 1)),
+           o_rs = lay.add(4 * (size_t)std::max<int64_t>(nruns, 1)), o_rv = lay.add(4 * (size_t)std::max<int64_t>(nruns, 1)),
+           o_out = lay.add(8 * n);
+    char *h = (char *)s->pin.need(lay.bytes);
+    char *d = (char *)s->scratch.need(lay.bytes);
+    memcpy(h + o_tok, tokens + tok_off[0], 4 * (size_t)total);
+    int64_t *h_toff = (int64_t *)(h + o_toff), *h_roff = (int64_t *)(h + o_roff);
+    for (int64_t k = 0; k <= n; k++) {
+      h_toff[k] = tok_off[k] - tok_off[0];
+      h_roff[k] = run_off[k] - run_off[0];
+    }
+    memcpy(h + o_nin, n_input, 8 * n);
+    memcpy(h + o_cv, ctx_version, 4 * n);
+    memcpy(h + o_rs, run_start + run_off[0], 4 * (size_t)nruns);
+    memcpy(h + o_rv, run_version + run_off[0], 4 * (size_t)nruns);
+    memcpy(h + o_out, out_off, 8 * n);
+    ck(cudaMemcpyAsync(d, h, lay.bytes, cudaMemcpyHostToDevice, st), "H2D host rows");
+    s->pin.mark(st);
+    tms::HostRowsArgs a{};
+    a.n = n;
+    a.src = (const int32_t *)(d + o_tok);
+    a.tok_off = (const int64_t *)(d + o_toff);
+    a.n_input = (const int64_t *)(d + o_nin);
+    a.ctx_version = (const int32_t *)(d + o_cv);
+    a.run_off = (const int64_t *)(d + o_roff);
+    a.run_start = (const int32_t *)(d + o_rs);
+    a.run_version = (const int32_t *)(d + o_rv);
+    a.out_off = (const int64_t *)(d + o_out);
+    a.tokens = out_tokens;
+    a.mask = out_mask;
+    a.versions = out_versions;
+    a.resp = out_resp_start;
+    {
+      ProfScope ps(s, 2, st);
+      ck(tms::launch_fill_host_rows(a, s->num_sms, st), "fill host rows");
+    }
+    mark_done(s, st);
+    s->c_export_calls++;
+    s->c_export_rows += n;
+    s->c_export_tokens += total;
+  });
+}
+
 int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *sid_json, const int64_t *sid_off,
                      int32_t mem_out, char *out, int64_t cap, int64_t *out_bytes, void *stream) {
   NvtxRange nvtx_("tm_export_ndjson");
@@ -1243,6 +1331,7 @@ int tm_export_ndjson(tm_store *s, int64_t n, const int64_t *rows, const char *si
     memcpy(h + o_off, off.data(), 8 * (n + 1));
     memcpy(h + o_tile, tile.data(), 8 * (n + 1));
     ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st), "H2D ndjson plan");
+    s->pin.mark(st);
     tms::ExportArgsHost e{};
     e.n = n;
     e.rows = (const int64_t *)(d + o_rows);
@@ -1656,6 +1745,18 @@ int tm_store_load(tm_store *s, const char *path) {
       throw;
     }
     fclose(f);
+  });
+}
+
+int tm_profile_reserve(tm_store *s, int64_t pairs) {
+  return guarded(s, [&] {
+    for (int k = 0; k < tm_store::kProfKinds; k++)
+      while ((int64_t)s->ev[k].size() < pairs) {
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+        s->ev[k].push_back({a, b});
+      }
   });
 }
 

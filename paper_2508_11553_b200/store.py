@@ -163,8 +163,11 @@ class DeviceStore:
     KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3, "route": 4, "route_pack": 5, "route_wait": 6,
                "record_copy": 7}
 
-    def profile_begin(self):
-        """Start recording CUDA events around every kernel launch of this store."""
+    def profile_begin(self, reserve: int = 0):
+        """Start recording CUDA events around every kernel launch of this store (with
+        ``reserve``: create the event pairs of that many launches per kernel kind now)."""
+        if reserve:
+            check(self.lib.tm_profile_reserve(self.h, int(reserve)))
         check(self.lib.tm_profile_begin(self.h))
 
     def profile_end(self, kernel: str = "walk") -> tuple[float, int]:
@@ -265,6 +268,23 @@ class DeviceStore:
                                       _ptr(m), _ptr(p), _ptr(d), None))
         return m, p, d
 
+    def match_lists(self, sids, seqs):
+        """match() for Python callers holding token lists (the reference's argument type):
+        the lists are flattened into one int32 buffer at C speed (array.array over a chain),
+        then one host-buffer match call."""
+        import array
+        import itertools
+
+        lens = np.fromiter((len(q) for q in seqs), np.int64, len(seqs))
+        off = np.zeros(len(seqs) + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        try:
+            buf = array.array("i", itertools.chain.from_iterable(seqs))
+        except OverflowError:
+            raise ValueError("token ids must fit in int32") from None
+        tokens = np.frombuffer(buf, np.int32) if len(buf) else np.zeros(1, np.int32)
+        return self.match(sids, tokens, off[:-1], lens)
+
     @staticmethod
     def _stream_arg(stream):
         # torch reports the legacy default stream as 0; the C ABI reads NULL as "the
@@ -347,6 +367,57 @@ class DeviceStore:
                                       _tptr(resp), self._stream_arg(stream)))
         return Packed(off, tok, msk, ver, resp)
 
+
+    def export_device_with_host_rows(self, rows, host_rows, stream=None) -> Packed:
+        """export_device of ``rows`` followed, in the same packed device batch, by rows that
+        live on the host (open / paused requests, trajectory.py:329-340): ``host_rows`` is a
+        list of (tokens, n_input, context_version, versions_of_the_output) - the input span
+        at the context version, then MODEL_OUTPUT positions at their per-token versions
+        (tm_export_host_rows)."""
+        import torch
+
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = len(rows)
+        total = self.rows_total(rows) if n else 0
+        nh = len(host_rows)
+        hl = np.fromiter((len(t) for t, *_ in host_rows), np.int64, nh)
+        tok_off = np.zeros(nh + 1, np.int64)
+        np.cumsum(hl, out=tok_off[1:])
+        htotal = int(tok_off[-1])
+        dev = torch.device("cuda", self.device)
+        tok = torch.empty(total + htotal, dtype=torch.int32, device=dev)
+        msk = torch.empty(total + htotal, dtype=torch.uint8, device=dev)
+        ver = torch.empty(total + htotal, dtype=torch.int32, device=dev)
+        resp = torch.empty(n + nh, dtype=torch.int64, device=dev)
+        off = np.zeros(n + nh + 1, np.int64)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        sa = self._stream_arg(stream)
+        if n:
+            check(self.lib.tm_export_rows(self.h, n, _ptr(rows), TM_MEM_DEVICE, _ptr(off), _tptr(tok), _tptr(msk),
+                                          _tptr(ver), _tptr(resp), sa))
+        off[n + 1:] = total + tok_off[1:]
+        if nh:
+            tokens = np.concatenate([np.asarray(t, np.int32) for t, *_ in host_rows]) if htotal else np.zeros(1, np.int32)
+            n_in = np.fromiter((int(x[1]) for x in host_rows), np.int64, nh)
+            cv = np.fromiter((int(x[2]) for x in host_rows), np.int32, nh)
+            starts, vers, roff = [], [], [0]
+            for (t, ni, _, v) in host_rows:
+                v = np.asarray(v, np.int64)
+                if len(v):
+                    cut = np.flatnonzero(v[1:] != v[:-1]) + 1
+                    st = np.concatenate(([0], cut))
+                    starts.append(st + int(ni))
+                    vers.append(v[st])
+                roff.append(roff[-1] + (len(starts[-1]) if len(v) else 0))
+            rs = np.concatenate(starts).astype(np.int32) if starts else np.zeros(1, np.int32)
+            rv = np.concatenate(vers).astype(np.int32) if vers else np.zeros(1, np.int32)
+            roff = np.asarray(roff, np.int64)
+            out_off = np.ascontiguousarray(off[n:n + nh])
+            check(self.lib.tm_export_host_rows(self.h, nh, _ptr(tokens), _ptr(tok_off), _ptr(n_in), _ptr(cv),
+                                               _ptr(roff), _ptr(rs), _ptr(rv), _ptr(out_off), _tptr(tok), _tptr(msk),
+                                               _tptr(ver), C.c_void_p(resp.data_ptr() + 8 * n), sa))
+        return Packed(off, tok, msk, ver, resp)
 
 _default: dict[int, DeviceStore] = {}
 

@@ -163,6 +163,24 @@ def test_config3_include_partials_vs_reference(store):
             e1 = ref.extract_trajectories(sid, include_partials=True, min_version=mv)
             assert [t.tokens for t in g1] == [t.tokens for t in e1]
     assert n_partial == n // 10
+    # the same export in tensor form, assembled on the GPU (completed rows: K3; partials:
+    # k_fill_host_rows), against the reference's objects in extract_trajectories order
+    names = [f"c3-{s}" for s in sorted(paused)]
+    row_sids, packed, order = tm.export_packed(names, include_partials=True)
+    exp = [t for sid in names for t in ref.extract_trajectories(sid, include_partials=True)]
+    assert len(order) == len(exp) == 2 * len(names)
+    off = packed.offsets
+    tok = packed.tokens.cpu().numpy()
+    msk = packed.loss_mask.cpu().numpy()
+    ver = packed.versions.cpu().numpy()
+    resp = packed.resp_start.cpu().numpy()
+    for i, e in zip(order, exp):
+        a, b = off[i], off[i + 1]
+        assert row_sids[i] == e.session_id
+        assert tok[a:b].tolist() == e.tokens
+        assert msk[a:b].astype(bool).tolist() == e.loss_mask
+        assert ver[a:b].tolist() == e.version_tags
+        assert resp[i] == (max([k for k, x in enumerate(e.loss_mask) if not x], default=-1) + 1)
     # sessions that completed both turns: no partials, two completed rows each
     for s in range(0, n, 97):
         if s in paused:

@@ -339,3 +339,62 @@ class C5Workload:
         forced = ((hist.to(torch.int64) + 1 + synth_tokens(gi, pos, salt=2).to(torch.int64) % (VOCAB - 1)) % VOCAB).to(torch.int32)
         tok = torch.where(pos < d, hist, torch.where((pos == d) & (d < Lh), forced, fresh))
         router.tokens[:tot].copy_(tok)
+
+
+class C5CpuSample:
+    """A config-5-shaped sample for the CPU baseline (the 1M-session store
+    does not fit the host as Python objects, so a seeded sample of sessions with the same
+    log-uniform length law is timed): histories from synth_tokens (the same counter-based
+    generator as the GPU shards, on the CPU), a batch of queries on those sessions,
+    75 % extensions + 256 new tokens / 25 % branches with a forced mismatch."""
+
+    def __init__(self, nranks=1, n_sessions=10_000, n_queries=4096, lo=1024, hi=131072, ext_frac=0.75,
+                 new_tokens=256):
+        import torch
+
+        rng = np.random.default_rng(SEED0 + 5)
+        lens_all = np.exp(rng.uniform(np.log(lo), np.log(hi), 1_000_000)).astype(np.int64)
+        self.g = np.arange(n_sessions, dtype=np.int64)  # the first sessions of the 1M (same lengths)
+        self.lens = lens_all[: n_sessions]
+        self.n_sessions, self.n_queries = n_sessions, n_queries
+        q = np.random.default_rng(SEED0 + 56)
+        self.q_sess = q.integers(0, n_sessions, n_queries).astype(np.int32)
+        L = self.lens[self.q_sess]
+        ext = q.random(n_queries) < ext_frac
+        self.q_depth = np.where(ext, L, (q.random(n_queries) * L).astype(np.int64))
+        self.q_len = self.q_depth + new_tokens
+        self._torch = torch
+
+    def _hist(self, s):
+        t = self._torch
+        return synth_tokens(t.full((int(self.lens[s]),), int(self.g[s]), dtype=t.int64),
+                            t.arange(int(self.lens[s]), dtype=t.int64)).numpy()
+
+    def build_port(self, nthreads):
+        """(C port store holding the sample's histories, query tokens, query offsets)."""
+        from oracle.cport import CRadixStore
+
+        t = self._torch
+        off = np.zeros(self.n_sessions + 1, np.int64)
+        np.cumsum(self.lens, out=off[1:])
+        g = t.repeat_interleave(t.as_tensor(self.g), t.as_tensor(self.lens))
+        base = t.repeat_interleave(t.as_tensor(off[:-1]), t.as_tensor(self.lens))
+        pos = t.arange(int(off[-1]), dtype=t.int64) - base
+        toks = synth_tokens(g, pos).numpy()
+        roff, rs, ro, rv = turn_runs_batch(self.lens)
+        st = CRadixStore()
+        st.insert_batch(np.arange(self.n_sessions, dtype=np.int32), toks, off, roff, rs, ro, rv, nthreads=nthreads)
+        qo = np.zeros(self.n_queries + 1, np.int64)
+        np.cumsum(self.q_len, out=qo[1:])
+        qt = np.empty(int(qo[-1]), np.int32)
+        qrng = np.random.default_rng(SEED0 + 57)
+        for i in range(self.n_queries):
+            s, d = int(self.q_sess[i]), int(self.q_depth[i])
+            h = toks[off[s]: off[s + 1]]
+            tail = qrng.integers(0, VOCAB, self.q_len[i] - d, dtype=np.int32)
+            if d < len(h):
+                tail[0] = (int(h[d]) + 1) % VOCAB
+            qt[qo[i]: qo[i] + d] = h[:d]
+            qt[qo[i] + d: qo[i + 1]] = tail
+        self.qt, self.qo = qt, qo
+        return st, qt, qo
