@@ -561,10 +561,16 @@ def measure_config(cfg, reps=3, with_cpu=True):
         t0 = time.perf_counter()
         store.export(rows, total=n_out)
         t_exp_host = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        store.export(rows, total=n_out, pinned=True)
+        t_exp_pin = time.perf_counter() - t0
         names = [f"sess-{int(s)}" for s in sids] if cfg != 1 else ["sess-0"] * len(rows)
         t0 = time.perf_counter()
         text = store.export_ndjson(rows, names, as_array=True)
         t_json = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        store.export_ndjson(rows, names, as_array=True, pinned=True)
+        t_json_pin = time.perf_counter() - t0
         part = None
         if cfg == 3:  # 10 % of the sessions paused inside turn 2: completed rows + partials
             keep_rows, host_rows = [], []
@@ -597,7 +603,9 @@ def measure_config(cfg, reps=3, with_cpu=True):
         keep("ex_ms", ex_ms)
         keep("t_exp_dev", t_exp_dev)
         keep("t_exp_host", t_exp_host)
+        keep("t_exp_pin", t_exp_pin)
         keep("t_json", t_json)
+        keep("t_json_pin", t_json_pin)
         if part:
             keep("t_part", part[0])
             keep("part_ms", part[1])
@@ -631,8 +639,11 @@ def measure_config(cfg, reps=3, with_cpu=True):
         "export": {"rows": int(len(rows)), "tokens": n_out, "device_ms": best["ex_ms"],
                    "call_ms_device_out": 1e3 * best["t_exp_dev"], "call_ms_host_out": 1e3 * best["t_exp_host"],
                    "host_GBps": 9.0 * n_out / best["t_exp_host"] / 1e9,
+                   "call_ms_host_pinned_out": 1e3 * best["t_exp_pin"],
+                   "host_pinned_GBps": 9.0 * n_out / best["t_exp_pin"] / 1e9,
                    "roofline": roof(exp_bytes, best["ex_ms"], "k_export_plan + k_export_tma")},
-        "ndjson": {"call_ms": 1e3 * best["t_json"], "bytes": int(len(text)), "tokens_per_s": n_out / best["t_json"]},
+        "ndjson": {"call_ms": 1e3 * best["t_json"], "bytes": int(len(text)), "tokens_per_s": n_out / best["t_json"],
+                   "call_ms_pinned_out": 1e3 * best["t_json_pin"], "pinned_GBps": len(text) / best["t_json_pin"] / 1e9},
     }
     if cfg == 3:
         _, _, ptok, prow, htok = part

@@ -1276,6 +1276,10 @@ __global__ void __launch_bounds__(NT) k_record_copy(DevView v, RecordArgs a, int
       if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
     }
   }
+  if (a.ctr_out && gridDim.x == 1) {  // the only CTA: every counter update is done (one D2H for the host)
+    __syncthreads();
+    if (threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
+  }
 }
 
 // ----------------------------------------------------------------------------------
@@ -1916,8 +1920,11 @@ cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sm
   // chunk <= NT entries per CTA (the allocation scan is one entry per thread), a multiple
   // of the CTA's warps (one warp per entry in the copy)
   constexpr int kWarps = kRecordCopyNT / 32;
-  const int64_t grid = std::max<int64_t>((a.b.n + kRecordCopyNT - 1) / kRecordCopyNT,
-                                         std::min<int64_t>(a.b.n, (int64_t)num_sms * 8));
+  // a.ctr_out (small host batches): one CTA, which also snapshots the counters
+  const int64_t grid = a.ctr_out && a.b.n <= kRecordCopyNT
+                           ? 1
+                           : std::max<int64_t>((a.b.n + kRecordCopyNT - 1) / kRecordCopyNT,
+                                               std::min<int64_t>(a.b.n, (int64_t)num_sms * 8));
   int64_t chunk = (a.b.n + grid - 1) / grid;
   chunk = std::min<int64_t>(kRecordCopyNT, (chunk + kWarps - 1) / kWarps * kWarps);
   k_record_copy<kRecordCopyNT><<<(int)((a.b.n + chunk - 1) / chunk), kRecordCopyNT, 0, s>>>(v, a, chunk);

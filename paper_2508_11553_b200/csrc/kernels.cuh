@@ -209,6 +209,7 @@ struct Batch {
 struct RecordArgs {
   Batch b;                    // entries grouped by session chain, batch order inside a chain
   const int64_t *chains;      // per chain in processing order (longest first): first entry, end, session
+  int64_t *ctr_out;           // non-null: k_record_copy runs as ONE CTA and copies the 4 counters here
   int64_t nchains;
   Sched *sched;               // work counter (self-cleaning)
 };

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -143,6 +144,7 @@ struct tm_store {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t last = nullptr;
+  cudaStream_t last_stream = (cudaStream_t)-1;  // stream `last` was recorded on (-1: none yet)
   std::mutex mu;
   DevView v{};
   int64_t arena_cap = 0, row_cap = 0, run_cap = 0, sess_cap = 0, ht_cap = 0;
@@ -325,15 +327,19 @@ struct ProfScope {
 };
 
 // exclusive operations (record, export, host-buffer match) wait for everything before them
-// Device -> pageable host copy of a large result: the driver stages pageable copies
-// through a small bounce buffer (measured ~1.5-5 GB/s here), so pipeline 64 MB chunks
-// through two pinned slots and spread the pinned->pageable memcpy over host threads.
+// Device -> host copy of a large result.  A page-locked destination (DeviceStore's pinned
+// export pool) is written by the copy engine directly.  For pageable memory the driver
+// stages through a small bounce buffer (measured ~1.5-5 GB/s here), so pipeline 64 MB
+// chunks through two pinned slots and spread the pinned->pageable memcpy over host threads.
 void d2h_pageable(tm_store *s, void *dst, const void *src, int64_t bytes, cudaStream_t st) {
   static const int64_t CH = [] {  // TM_D2H_CHUNK_MB (tuning only)
     const char *e = getenv("TM_D2H_CHUNK_MB");
     return (e ? std::max(1, atoi(e)) : 64) * (int64_t(1) << 20);
   }();
-  if (bytes <= (8ll << 20)) {
+  cudaPointerAttributes pa{};
+  const bool pinned_dst = cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  if (!pinned_dst) cudaGetLastError();  // clear the (harmless) error for unregistered memory
+  if (bytes <= (8ll << 20) || pinned_dst) {  // page-locked destination: the copy engine writes it directly
     ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "D2H sync");
     return;
@@ -388,7 +394,7 @@ void check_ctr_error(const tm_store *s) {
 bool valid_row(const tm_store *s, int64_t r) { return r >= 0 && r < (int64_t)s->rows.size() && s->rows[r].sid >= 0; }
 
 void wait_prev(tm_store *s, cudaStream_t st) {
-  ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");
+  if (s->last_stream != st) ck(cudaStreamWaitEvent(st, s->last, 0), "cudaStreamWaitEvent");  // same stream: ordered
   for (auto &sl : s->slots)
     if (sl.used) {
       ck(cudaStreamWaitEvent(st, sl.done, 0), "cudaStreamWaitEvent");
@@ -396,7 +402,34 @@ void wait_prev(tm_store *s, cudaStream_t st) {
     }
 }
 
-void mark_done(tm_store *s, cudaStream_t st) { ck(cudaEventRecord(s->last, st), "cudaEventRecord"); }
+void mark_done(tm_store *s, cudaStream_t st) {
+  ck(cudaEventRecord(s->last, st), "cudaEventRecord");
+  s->last_stream = st;
+}
+
+// TM_TRACE_CALLS=1: per-phase host time of record calls on stderr (latency work only)
+struct PhaseTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  char buf[512];
+  int len = 0;
+  PhaseTrace() {
+    static const bool env = getenv("TM_TRACE_CALLS") != nullptr;
+    on = env;
+    if (on) t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char *name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    len += snprintf(buf + len, sizeof(buf) - len, " %s=%.1f", name,
+                    std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+  ~PhaseTrace() {
+    if (on) fprintf(stderr, "[tm trace]%s total=%.1f us\n", buf,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
 
 // NVTX range around every C-ABI call (visible in nsys / ncu timelines)
 struct NvtxRange {
@@ -812,6 +845,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                     int64_t *out_matched, int64_t *out_row, int32_t *out_local, int64_t *out_parent,
                     int32_t *out_parent_local, int64_t *out_added, void *stream) {
   NvtxRange nvtx_("tm_record_batch");
+  PhaseTrace tr;
   return guarded(s, [&] {
     if (n < 0) fail(TM_EINVAL, "negative batch size");
     if (n == 0) return;
@@ -883,6 +917,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     ensure_rows(s, row_base + n_fresh);
     ensure_runs(s, s->n_runs + total_runs);
     ensure_table(s, s->n_real_rows + n);
+    tr.mark("validate+capacity");
     wait_prev(s, s->stream);
     if (mem == TM_MEM_DEVICE && stream && (cudaStream_t)stream != s->stream) {  // order after the producer
       cudaEvent_t ev;
@@ -891,28 +926,53 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       ck(cudaStreamWaitEvent(s->stream, ev, 0), "wait");
       cudaEventDestroy(ev);
     }
-    // ---- stage tokens and per-entry arrays (chain order)
+    // ---- stage tokens and per-entry arrays (chain order).  Small host batches (the per-request
+    // lpm_insert path) carry their tokens inside the batch staging: one H2D for everything,
+    // and a single-CTA copy kernel snapshots the counters next to the results: one D2H.
     std::vector<int64_t> doff;
-    const int32_t *tok_base;
+    const int32_t *tok_base = nullptr;
+    int64_t small_words = 0;
+    if (mem == TM_MEM_HOST && n <= 256) {
+      for (int64_t k = 0; k < n; k++) small_words += round_up(std::max<int64_t>(tok_len[k], 1), tms::kAlignWords);
+      if (small_words > (int64_t(1) << 18) || use_packed(s, small_words)) small_words = 0;
+    }
+    const bool small = small_words > 0;
     if (mem == TM_MEM_DEVICE) {  // tokens already in HBM (e.g. produced by the engine)
       doff.resize(n);
       for (int64_t k = 0; k < n; k++) doff[k] = tok_off[perm[k]];
       tok_base = tokens;
-    } else {
+    } else if (!small) {
       stage_tokens(s, n, tokens, tok_off, tok_len, doff, &perm, s->stream);
       tok_base = (const int32_t *)s->dtok.p;
     }
     Layout lay;
     size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
            o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs),
+           o_tok = lay.add(4 * (size_t)(small_words + tms::kAlignWords)),
            o_crow = lay.add(8 * n), o_chains = lay.add(24 * nchains);
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
-           o_sp = lay.add(4 * n), o_cloc = lay.add(4 * n);
+           o_sp = lay.add(4 * n), o_cloc = lay.add(4 * n), o_ctr = lay.add(8 * 4);
     size_t out_end = lay.bytes;
     size_t o_cvb = lay.add(8 * n), o_cr0 = lay.add(8 * n), o_cfr = lay.add(4 * n);
     char *h = (char *)s->pin.need(lay.bytes);
     char *d = (char *)s->scratch.need(lay.bytes);
+    if (small) {
+      doff.resize(n);
+      int32_t *ht = (int32_t *)(h + o_tok);
+      int64_t w = 0;
+      for (int64_t k = 0; k < n; k++) {
+        const int64_t e = perm[k], L = tok_len[e], P = round_up(std::max<int64_t>(L, 1), tms::kAlignWords);
+        doff[k] = w;
+        memcpy(ht + w, tokens + tok_off[e], 4 * (size_t)L);
+        memset(ht + w + L, 0, 4 * (size_t)(P - L));
+        w += P;
+      }
+      tok_base = (const int32_t *)(d + o_tok);
+      s->c_raw_calls++;
+      s->c_raw_tokens += small_words;
+      s->c_h2d_bytes += 4 * small_words;
+    }
     int32_t *h_sid = (int32_t *)(h + o_sid);
     int64_t *h_off = (int64_t *)(h + o_off), *h_len = (int64_t *)(h + o_len), *h_roff = (int64_t *)(h + o_roff);
     int64_t *h_crow = (int64_t *)(h + o_crow);
@@ -942,7 +1002,9 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         hc[3 * it + 2] = sids[perm[chain_beg[c]]];
       }
     }
+    tr.mark("stage");
     ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
+    tr.mark("h2d");
     {
       tms::RecordArgs ra{};
       Batch &b = ra.b;
@@ -966,6 +1028,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       b.c_firstrun = (int32_t *)(d + o_cfr);
       b.c_local = (int32_t *)(d + o_cloc);
       ra.chains = (const int64_t *)(d + o_chains);
+      ra.ctr_out = small ? (int64_t *)(d + o_ctr) : nullptr;  // single-CTA copy: counters beside the results
       ra.nchains = nchains;
       ra.sched = s->sched;
       tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
@@ -977,16 +1040,20 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         ProfScope ps(s, 1, s->stream);
         ck(tms::launch_record(dv, ra, s->num_sms, s->stream), "record");
       }
+      tr.mark("launch1");
       ProfScope ps(s, 7, s->stream);
       ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
+      tr.mark("launch2");
     }
     // ---- results back (chain order), into the host mirror in batch order
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
-    enqueue_ctr_readback(s, s->stream);
+    if (!small) enqueue_ctr_readback(s, s->stream);
     mark_done(s, s->stream);
+    tr.mark("d2h+event");
     ck(cudaStreamSynchronize(s->stream), "record sync");
-    check_ctr_error(s);
-    const int64_t *ctr = s->pin_ctr;
+    tr.mark("sync");
+    const int64_t *ctr = small ? (const int64_t *)(h + o_ctr) : s->pin_ctr;
+    if (ctr[3]) raise_device_error(ctr[3]);
     const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
     const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),

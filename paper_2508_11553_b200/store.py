@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import array
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -237,8 +238,8 @@ class DeviceStore:
         out = (C.c_int64 * 6)()
         check(self.lib.tm_record_one(self.h, sid, pt, len(kt), ps, po, pv, len(ks), C.addressof(out)))
         m, row, local, par, par_local, added = out
-        return RecordResult(np.array([m]), np.array([row]), np.array([local], np.int32), np.array([par]),
-                            np.array([par_local], np.int32), np.array([added]))
+        # one-element lists, not arrays: this is the per-request path and every microsecond shows
+        return RecordResult([m], [row], [local], [par], [par_local], [added])
 
     def record(self, sids, seqs, runs) -> RecordResult:
         """seqs: list of int sequences; runs: list of (starts, origins, versions)."""
@@ -270,20 +271,13 @@ class DeviceStore:
 
     def match_lists(self, sids, seqs):
         """match() for Python callers holding token lists (the reference's argument type):
-        the lists are flattened into one int32 buffer at C speed (array.array over a chain),
-        then one host-buffer match call."""
-        import array
-        import itertools
+        the lists are flattened into one int32 buffer by host threads (csrc/tmfast.c), then
+        one host-buffer match call."""
+        from . import _tmfast
 
-        lens = np.fromiter((len(q) for q in seqs), np.int64, len(seqs))
-        off = np.zeros(len(seqs) + 1, np.int64)
-        np.cumsum(lens, out=off[1:])
-        try:
-            buf = array.array("i", itertools.chain.from_iterable(seqs))
-        except OverflowError:
-            raise ValueError("token ids must fit in int32") from None
-        tokens = np.frombuffer(buf, np.int32) if len(buf) else np.zeros(1, np.int32)
-        return self.match(sids, tokens, off[:-1], lens)
+        tok, off = _tmfast.pack_lists(seqs, os.cpu_count() or 1)
+        off = np.frombuffer(off, np.int64)
+        return self.match(sids, np.frombuffer(tok, np.int32), off[:-1], np.diff(off))
 
     @staticmethod
     def _stream_arg(stream):
@@ -309,23 +303,48 @@ class DeviceStore:
         check(self.lib.tm_rows_total(self.h, len(rows), _ptr(rows), C.byref(t)))
         return t.value
 
-    def export(self, rows, total: int | None = None) -> Packed:
+    def _pinned_views(self, specs):
+        """Numpy arrays carved out of this store's page-locked export pool (grown x2 on
+        demand): the copy engine writes them at full PCIe rate, with no pinned -> pageable
+        pass.  The views are reused by the next pinned export of this store."""
+        import torch
+
+        sizes = [((int(n) * np.dtype(dt).itemsize + 255) // 256) * 256 for n, dt in specs]
+        need = max(256, sum(sizes))
+        pool = getattr(self, "_pin_pool", None)
+        if pool is None or pool.numel() < need:
+            self._pin_pool = pool = torch.empty(max(need, 2 * (pool.numel() if pool is not None else 0)),
+                                                dtype=torch.uint8, pin_memory=True)
+        base = pool.numpy()
+        out, o = [], 0
+        for (n, dt), sz in zip(specs, sizes):
+            out.append(base[o: o + int(n) * np.dtype(dt).itemsize].view(dt))
+            o += sz
+        return out
+
+    def export(self, rows, total: int | None = None, *, pinned: bool = False) -> Packed:
         """Packed trajectories of ``rows`` in host numpy arrays (``total``: their summed
-        length when the caller already knows it, saving a round trip)."""
+        length when the caller already knows it, saving a round trip).  ``pinned``: the
+        arrays are views of the store's page-locked export pool (written directly by the
+        copy engine; valid until the next pinned export of this store - copy to keep)."""
         rows = np.ascontiguousarray(rows, np.int64)
         n = len(rows)
         if total is None:
             total = self.rows_total(rows) if n else 0
         off = np.zeros(n + 1, np.int64)
-        tok = np.empty(total, np.int32)
-        msk = np.empty(total, np.uint8)
-        ver = np.empty(total, np.int32)
-        resp = np.empty(n, np.int64)
+        if pinned:
+            tok, msk, ver, resp = self._pinned_views([(total, np.int32), (total, np.uint8), (total, np.int32),
+                                                       (n, np.int64)])
+        else:
+            tok = np.empty(total, np.int32)
+            msk = np.empty(total, np.uint8)
+            ver = np.empty(total, np.int32)
+            resp = np.empty(n, np.int64)
         check(self.lib.tm_export_rows(self.h, n, _ptr(rows), TM_MEM_HOST, _ptr(off), _ptr(tok), _ptr(msk), _ptr(ver),
                                       _ptr(resp), None))
         return Packed(off, tok, msk, ver, resp)
 
-    def export_ndjson(self, rows, session_ids, *, as_array: bool = False):
+    def export_ndjson(self, rows, session_ids, *, as_array: bool = False, pinned: bool = False):
         """Canonical NDJSON lines of ``rows`` (one per row, "\n"-terminated), formatted on
         the GPU; byte-identical to trajectory_to_line (core.py:182-183).  ``session_ids``:
         the session id string of each row."""
@@ -342,7 +361,7 @@ class DeviceStore:
         size = C.c_int64()
         check(self.lib.tm_export_ndjson(self.h, n, _ptr(rows), _ptr(sid), _ptr(sid_off), TM_MEM_HOST, None, 0,
                                         C.byref(size), None))
-        out = np.empty(max(size.value, 1), np.uint8)
+        out = self._pinned_views([(max(size.value, 1), np.uint8)])[0] if pinned else np.empty(max(size.value, 1), np.uint8)
         got = C.c_int64()
         check(self.lib.tm_export_ndjson(self.h, n, _ptr(rows), _ptr(sid), _ptr(sid_off), TM_MEM_HOST, _ptr(out),
                                         size.value, C.byref(got), None))

@@ -26,6 +26,11 @@ import numpy as np
 from .core import ORIGIN_CODE, ModelVersion, SpanOrigin, TokenId, Trajectory
 from .store import DeviceStore, default_store, runs_from_per_token
 
+try:  # host-side argument marshalling in C (csrc/tmfast.c); the pure-Python paths below remain
+    from . import _tmfast
+except ImportError:  # pragma: no cover - the extension is built with libtmstore.so
+    _tmfast = None
+
 MetaRun = tuple[int, SpanOrigin, ModelVersion]
 
 
@@ -70,6 +75,8 @@ def _as_int32(values):
         if values.size and (values.min() < -(2**31) or values.max() >= 2**31):
             raise ValueError("token ids must fit in int32")
         return np.ascontiguousarray(values, np.int32)
+    if _tmfast is not None and isinstance(values, (list, tuple)):
+        return np.frombuffer(_tmfast.pack_i32(values), np.int32)
     try:
         return array.array("i", values)
     except OverflowError:
@@ -82,6 +89,9 @@ def meta_runs(origins, versions):
     Runs are found at C speed: origin changes with list.index (two values), version
     changes from an int64 view (skipped when every token has the same version)."""
     n = len(origins)
+    if _tmfast is not None and n and isinstance(origins, (list, tuple)) and isinstance(versions, (list, tuple)):
+        st, org, ver, k = _tmfast.meta_runs(origins, versions, SpanOrigin.MODEL_OUTPUT, SpanOrigin.AGENT_INPUT)
+        return np.frombuffer(st, np.int32, k), np.frombuffer(org, np.uint8, k), np.frombuffer(ver, np.int32, k)
     if isinstance(origins, np.ndarray) or not n:
         o = np.asarray([ORIGIN_CODE.get(x, 1 if getattr(x, "value", x) in (1, True, "model_output") else 0)
                         for x in origins] if not isinstance(origins, np.ndarray) else origins, np.int64)

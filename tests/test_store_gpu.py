@@ -403,6 +403,24 @@ def test_edge_cases_long_sequences_and_extremes(store):
         trie.lpm_insert([2**31], [SpanOrigin.AGENT_INPUT], [0])
 
 
+def test_pinned_export_views_match_pageable(store):
+    """export(pinned=True) / export_ndjson(pinned=True) write the store's page-locked pool
+    directly (large results skip the pinned->pageable pass) and equal the pageable path."""
+    rng = np.random.default_rng(21)
+    sid = store.new_session()
+    seqs = [rng.integers(0, 151936, 3_000_000).tolist()] + [rng.integers(0, 151936, 700).tolist() for _ in range(3)]
+    runs = [(np.array([0, 5], np.int32), np.array([0, 1], np.uint8), np.array([2, 3], np.int32))] * len(seqs)
+    r = store.record([sid] * len(seqs), seqs, runs)
+    rows = list(r.row) * 3
+    a = store.export(rows)
+    b = store.export(rows, pinned=True)
+    for x, y in ((a.tokens, b.tokens), (a.loss_mask, b.loss_mask), (a.versions, b.versions), (a.resp_start, b.resp_start)):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.offsets, b.offsets)
+    names = ["s"] * len(rows)
+    assert store.export_ndjson(rows, names) == store.export_ndjson(rows, names, as_array=True, pinned=True).tobytes()
+
+
 def test_large_host_exports_stream_through_pinned_chunks(store):
     """Exports and NDJSON larger than the single-copy limit (8 MB) come back through the
     chunked pinned pipeline (several chunks, odd sizes); every byte must match."""
