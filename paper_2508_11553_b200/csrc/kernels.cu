@@ -801,6 +801,7 @@ __device__ __forceinline__ int first_run_at(const Batch &b, int64_t w, int64_t m
 constexpr int kCopyU = 4;      // int4 loads in flight per thread in K2's copies
 constexpr int kRecPre = 64;    // entries whose offset / length / first token are fetched at once
 constexpr int kRecCache = 4;   // per-chain root-row and row-field cache entries
+constexpr int kRecQ = 32;      // copy queue slots (warp-specialised K2)
 
 struct RowFields {  // what the walk and the commit need of a row, read in one round trip
   long long vb, ext, ext_vb, jump;
@@ -849,6 +850,11 @@ struct RecShared {
   long long fc_row[kRecCache];
   RowFields fc[kRecCache];
   int rc_next, fc_next;
+  // copy warp queue (warp-specialised k_record_tma): committed entries whose novel suffix the
+  // copy warp moves into the arena while the walk warps go on with the chain
+  int q_e[kRecQ], q_m[kRecQ], q_L[kRecQ];
+  long long q_off[kRecQ];
+  int q_head, q_read, q_closed;
   // entry prefetch
   long long pre_off[kRecPre];
   int pre_len[kRecPre], pre_q0[kRecPre];
@@ -884,7 +890,7 @@ __device__ __forceinline__ int64_t rec_root(const DevView &v, RecShared &sh, int
 // Whole-CTA walk of the chain's current entry (sh.off / sh.len / sh.q0), the LPM walk of
 // trie.py:136-158 over rows (see walk_query): results into sh.m / parent / dup / tnext /
 // spar and the parent's fields into sh.pf.
-template <int NT, int S, int CHV>
+template <int NT, int BAR, int S, int CHV>
 __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, RecShared &sh,
                                             TmaRing<NT, S, CHV> &rg) {
   static_assert(NT <= 128, "RecShared holds the compare scratch of <= 4 warps");
@@ -897,9 +903,9 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
     if (sh.pc_row >= 0 && r >= 0) sh.pc_len = min(L, sh.pc_rlen);
     sh.row = r;
   }
-  __syncthreads();
+  group_sync<NT, BAR>();
   int jpc = 0;
-  if (sh.pc_len > 0) jpc = block_first_mismatch_tma(q, v.arena + sh.pc_vb, 0, sh.pc_len, sh.red, rg);
+  if (sh.pc_len > 0) jpc = block_first_mismatch_tma<NT, S, CHV, BAR>(q, v.arena + sh.pc_vb, 0, sh.pc_len, sh.red, rg);
   if (threadIdx.x == 0) {
     int64_t r = sh.row;
     int lo = 1;
@@ -923,7 +929,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
     sh.row = r;
     sh.lo = lo;
   }
-  __syncthreads();
+  group_sync<NT, BAR>();
   while (sh.row >= 0) {
     const int64_t r = sh.row;
     const int lo = sh.lo, Lr = sh.f.len;
@@ -931,7 +937,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
     TM_DCHECK(v, (sh.f.vb + sh.f.m >= 0 && sh.f.vb + ((Lr + 3) & ~3) <= v.arena_cap) ||
                      (sh.f.vb + sh.f.m >= v.qv_lo && sh.f.vb + ((Lr + 3) & ~3) <= v.qv_hi), kErrArena);
     const int32_t *a = v.arena + sh.f.vb;
-    const int j = block_first_mismatch_tma(q, a, lo, hi, sh.red, rg, sh.cap);
+    const int j = block_first_mismatch_tma<NT, S, CHV, BAR>(q, a, lo, hi, sh.red, rg, sh.cap);
     if (threadIdx.x == 0) {
       int64_t next = -1;
       if (j < L) {
@@ -959,7 +965,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
       sh.row = next;
       sh.lo = j + 1;
     }
-    __syncthreads();
+    group_sync<NT, BAR>();
   }
 }
 
@@ -1080,18 +1086,105 @@ __device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, 
   }
 }
 
-template <int NT, int S, int CHV, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_record_tma(DevView v, RecordArgs a) {
+// The copy warp of the warp-specialised K2: takes committed entries from the queue in
+// order, allocates their arena lines and run slots (atomics off the chain's serial path),
+// moves the novel suffix [m, L) from the query into the arena (8 int4 loads in flight per
+// lane) and the runs (first clamped to m) into the run table.  The row keeps reading its
+// query until k_record_finish switches its virtual base.
+__device__ void record_copy_warp(const DevView &v, const Batch &b, RecShared &sh) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0;; i++) {
+    int e = -1, m = 0, L = 0;
+    long long off = 0;
+    if (lane == 0) {
+      for (;;) {
+        const int head = *(volatile int *)&sh.q_head;
+        if (i < head) break;
+        if (*(volatile int *)&sh.q_closed && i >= *(volatile int *)&sh.q_head) { i = -1; break; }
+        __nanosleep(100);
+      }
+      if (i >= 0) {
+        __threadfence_block();
+        const int slot = i % kRecQ;
+        e = *(volatile int *)&sh.q_e[slot];
+        m = *(volatile int *)&sh.q_m[slot];
+        L = *(volatile int *)&sh.q_L[slot];
+        off = *(volatile long long *)&sh.q_off[slot];
+        __threadfence_block();
+        *(volatile int *)&sh.q_read = i + 1;  // the slot may be reused (one reader, in order)
+      }
+    }
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (__shfl_sync(0xffffffffu, i, 0) < 0) return;
+    m = __shfl_sync(0xffffffffu, m, 0);
+    L = __shfl_sync(0xffffffffu, L, 0);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    long long vb = 0, run0 = 0;
+    int fr = 0, nr = 0;
+    if (lane == 0) {
+      const long long words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - ((long long)m / kAlignWords) * kAlignWords;
+      vb = (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)words) - (m / kAlignWords) * kAlignWords;
+      fr = first_run_at(b, e, m);
+      nr = (int)(b.run_off[e + 1] - b.run_off[e]) - fr;
+      run0 = (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)nr);
+      TM_DCHECK(v, vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap, kErrArena);
+      TM_DCHECK(v, run0 >= 0 && run0 + nr <= v.run_cap, kErrRun);
+    }
+    vb = __shfl_sync(0xffffffffu, vb, 0);
+    run0 = __shfl_sync(0xffffffffu, run0, 0);
+    fr = __shfl_sync(0xffffffffu, fr, 0);
+    nr = __shfl_sync(0xffffffffu, nr, 0);
+    const int4 *src = reinterpret_cast<const int4 *>(b.tok + off);
+    int4 *dst = reinterpret_cast<int4 *>(v.arena + vb);
+    const int64_t i1 = (L + 3) >> 2;
+    for (int64_t base = (m >> 2) + lane; base < i1; base += 32 * 8) {
+      int4 t[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) t[k] = ldg_stream_if(src + base + 32 * k, base + 32 * k < i1);
+#pragma unroll
+      for (int k = 0; k < 8; k++) stg_if(dst + base + 32 * k, t[k], base + 32 * k < i1);
+    }
+    const int64_t r0 = b.run_off[e] + fr;
+    for (int k = lane; k < nr; k += 32) {
+      const int32_t st = b.run_start[r0 + k];
+      v.run_start[run0 + k] = st > m ? st : m;
+      v.run_origin[run0 + k] = b.run_origin[r0 + k];
+      v.run_version[run0 + k] = b.run_version[r0 + k];
+    }
+    if (lane == 0) {
+      b.c_vb[e] = vb;
+      b.c_run0[e] = run0;
+      b.c_firstrun[e] = fr;
+    }
+  }
+}
+
+// K2, chain part.  NCW = 0: NT walk threads do everything on the chain's path and
+// k_record_copy moves the suffixes afterwards.  NCW = 1: a 32-thread copy warp beside the
+// NT walk threads (named barrier 1 keeps it out of theirs) moves each committed entry's
+// suffix while the chain goes on, and k_record_finish only switches the rows' bases.
+template <int NT, int NCW, int S, int CHV, int MINB>
+__global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, RecordArgs a) {
+  static_assert(NCW == 0 || NCW == 1, "one copy warp: the queue has one reader");
+  constexpr int BAR = NCW ? 1 : 0;
   const Batch &b = a.b;
   __shared__ RecShared sh;
   __shared__ long long s_item;
   __shared__ TmaRing<NT, S, CHV> rg;
-  tma_ring_init(rg);
+  tma_ring_init(rg);  // every thread: __syncthreads inside
+  if (NCW && threadIdx.x == 0) {
+    sh.q_head = sh.q_read = sh.q_closed = 0;
+  }
+  __syncthreads();
+  if (NCW && threadIdx.x >= NT) {
+    record_copy_warp(v, b, sh);
+    return;
+  }
   // the first wave takes chains by CTA index; later chains come from the work counter,
-  // which k_record_copy (next on the stream) leaves zeroed for the next launch
+  // which the next kernel on the stream leaves zeroed for the next launch
   long long it = blockIdx.x;
   for (;;) {
-    if (it >= a.nchains) return;
+    if (it >= a.nchains) break;
     const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
     if (threadIdx.x == 0) {  // the session, cached for the whole chain
       const int32_t sid = (int32_t)a.chains[3 * it + 2];
@@ -1115,7 +1208,7 @@ __global__ void __launch_bounds__(NT, MINB) k_record_tma(DevView v, RecordArgs a
     for (int64_t e = e0; e < e1; e++) {
       const int k = (int)((e - e0) % kRecPre);
       if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
-        __syncthreads();
+        group_sync<NT, BAR>();
         for (int t = threadIdx.x; t < kRecPre && e + t < e1; t += NT) {
           const int64_t off = b.off[e + t];
           sh.pre_off[t] = off;
@@ -1123,16 +1216,29 @@ __global__ void __launch_bounds__(NT, MINB) k_record_tma(DevView v, RecordArgs a
           sh.pre_q0[t] = b.tok[off];
         }
       }
-      __syncthreads();
+      group_sync<NT, BAR>();
       if (threadIdx.x == 0) {
         sh.off = sh.pre_off[k];
         sh.len = sh.pre_len[k];
         sh.q0 = sh.pre_q0[k];
       }
-      __syncthreads();
-      record_walk(v, b, sh, rg);
-      if (threadIdx.x == 0) record_commit(v, b, e, sh);
-      __syncthreads();
+      group_sync<NT, BAR>();
+      record_walk<NT, BAR>(v, b, sh, rg);
+      if (threadIdx.x == 0) {
+        record_commit(v, b, e, sh);
+        if (NCW && sh.dup < 0 && sh.len > sh.m) {  // hand the suffix copy to the copy warp
+          const int head = sh.q_head;
+          while (head - *(volatile int *)&sh.q_read >= kRecQ) __nanosleep(100);
+          const int slot = head % kRecQ;
+          sh.q_e[slot] = (int)e;
+          sh.q_m[slot] = (int)sh.m;
+          sh.q_L[slot] = sh.len;
+          sh.q_off[slot] = sh.off;
+          __threadfence_block();
+          *(volatile int *)&sh.q_head = head + 1;
+        }
+      }
+      group_sync<NT, BAR>();
       if (sh.pcw_len > 0) {  // path copy: [from, L) of the entry's query (congruent layout)
         block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
                                 reinterpret_cast<const int4 *>(b.tok + sh.off), sh.pcw_from >> 2, (sh.pcw_len + 3) >> 2);
@@ -1150,9 +1256,35 @@ __global__ void __launch_bounds__(NT, MINB) k_record_tma(DevView v, RecordArgs a
       v.s_pc_cap[sid] = sh.pc_cap;
       s_item = (long long)gridDim.x + (long long)atomicAdd(&a.sched->work, 1ull);
     }
-    __syncthreads();
+    group_sync<NT, BAR>();
     it = s_item;
+    group_sync<NT, BAR>();
+  }
+  if (NCW && threadIdx.x == 0) {
+    __threadfence_block();
+    *(volatile int *)&sh.q_closed = 1;
+  }
+}
+
+// K2b after the warp-specialised K2: every new row switches to its arena copy (virtual
+// base, runs; a prefix row has none), a parent's extension hint pointing at it follows.
+__global__ void __launch_bounds__(256) k_record_finish(DevView v, RecordArgs a) {
+  const Batch &b = a.b;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.sched->work = 0;  // k_record's work counter, for the next launch
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b.n; e += (int64_t)gridDim.x * blockDim.x) {
+    if (b.o_dup[e] >= 0) continue;
+    const int64_t m = b.o_m[e], L = b.len[e], row = b.c_row[e];
+    const bool own = L > m;
+    const int64_t vb = own ? b.c_vb[e] : -m;
+    v.row_vb[row] = vb;
+    v.row_run0[row] = own ? b.c_run0[e] : 0;
+    v.row_nrun[row] = own ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
+    const int64_t par = b.o_parent[e];
+    if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
+  }
+  if (a.ctr_out && gridDim.x == 1) {  // the only CTA, and k_record is done: counters beside the results
     __syncthreads();
+    if (threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
   }
 }
 
@@ -1931,55 +2063,76 @@ cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sm
   return cudaGetLastError();
 }
 
-template <int S, int CHV, int MINB, int NT = 64>
-static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record_tma<NT, S, CHV, MINB>, NT, 0);
-    if (occ < 1) occ = 1;
-  }
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
-  k_record_tma<NT, S, CHV, MINB><<<(int)grid, NT, 0, s>>>(v, a);
+cudaError_t launch_record_finish(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+  if (a.b.n < 1) return cudaSuccess;
+  const int64_t grid = a.ctr_out && a.b.n <= 256 ? 1 : std::min<int64_t>((a.b.n + 255) / 256, (int64_t)num_sms * 4);
+  k_record_finish<<<(int)grid, 256, 0, s>>>(v, a);
   return cudaGetLastError();
 }
 
-// K2 = k_record_tma (chains: walk + commit, serial per session) + k_record_copy (arena
-// allocation, suffixes and runs, all entries in parallel).  A chain's compare is TMA-staged
-// (the stages live in shared memory, not registers).  At most 8 chains per SM: 128-thread
-// CTAs with 3 x 4 KB stages per stream, every chain resident at once with 24 KB in flight
-// (c2: 0.776 of peak vs 0.733 with 64 threads); more chains: one-warp CTAs, 32 per SM,
-// 2 x 1 KB stages, so up to 4,736 chains are resident in one wave (c3, 4,000 chains: 0.517
-// vs 0.459 for 64-thread CTAs in two waves).  Tuning builds (-DTM_TUNING) select other
-// shapes with TM_RECORD_VARIANT.
-cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
+template <int S, int CHV, int MINB, int NT = 64, int NCW = 0>
+static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s,
+                                      int *copy_warp) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_record_tma<NT, NCW, S, CHV, MINB>, NT + 32 * NCW, 0);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
+  k_record_tma<NT, NCW, S, CHV, MINB><<<(int)grid, NT + 32 * NCW, 0, s>>>(v, a);
+  *copy_warp = NCW;
+  return cudaGetLastError();
+}
+
+// K2 = k_record_tma (chains: walk + commit, serial per session) + either k_record_copy
+// (arena allocation, suffixes and runs, all entries in parallel, after the chains) or -
+// with a copy warp in every chain CTA moving each entry's suffix while the chain goes on -
+// k_record_finish (the rows' bases only).  A chain's compare is TMA-staged (the stages
+// live in shared memory, not registers).
+//   <= 8 chains per SM (c2, 1,000 chains): 64 walk threads + 1 copy warp, 3 x 4 KB stages
+//     per stream, every chain resident; the copies ride under the chains' latency-bound
+//     walks: c2 0.859 of peak (0.764 with the copies after the chains, 128 walk threads)
+//   more chains (c3, 4,000 chains of 2 entries): one-warp CTAs, 32 per SM, 2 x 1 KB stages,
+//     so up to 4,736 chains are resident at once; registers leave no room for copy warps
+//     (16 CTAs per SM with them: two waves), so k_record_copy follows: c3 0.524 (0.500 with
+//     copy warps)
+// Tuning builds (-DTM_TUNING) select other shapes with TM_RECORD_VARIANT.
+cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s, int *copy_warp) {
+  *copy_warp = 0;
 #ifdef TM_TUNING
   static int variant = -1;
   if (variant < 0) {
     static const char *names[] = {"default", "tma3x256", "tma2x128", "tma4x256", "tma2x256", "tma4x128", "tma3x128",
-                                  "t128x3x256", "t128x2x128", "t128x2x256", "t32x2x64", "t32x3x64", "t32x2x128"};
+                                  "t128x3x256", "t128x2x128", "t128x2x256", "t32x2x64", "t32x3x64", "t32x2x128",
+                                  "ws64x3x256", "ws64x2x256", "ws32x2x64", "ws32x2x128", "ws64x2x128"};
     const char *e = getenv("TM_RECORD_VARIANT");
     variant = 0;
     for (int i = 0; e && i < (int)(sizeof(names) / sizeof(names[0])); i++)
       if (!strcmp(e, names[i])) variant = i;
   }
   switch (variant) {
-    case 1: return record_tma_variant<3, 256, 8>(v, a, num_sms, s);
-    case 2: return record_tma_variant<2, 128, 16>(v, a, num_sms, s);
-    case 3: return record_tma_variant<4, 256, 6>(v, a, num_sms, s);
-    case 4: return record_tma_variant<2, 256, 12>(v, a, num_sms, s);
-    case 5: return record_tma_variant<4, 128, 12>(v, a, num_sms, s);
-    case 6: return record_tma_variant<3, 128, 14>(v, a, num_sms, s);
-    case 7: return record_tma_variant<3, 256, 8, 128>(v, a, num_sms, s);
-    case 8: return record_tma_variant<2, 128, 12, 128>(v, a, num_sms, s);
-    case 9: return record_tma_variant<2, 256, 8, 128>(v, a, num_sms, s);
-    case 10: return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s);
-    case 11: return record_tma_variant<3, 64, 28, 32>(v, a, num_sms, s);
-    case 12: return record_tma_variant<2, 128, 24, 32>(v, a, num_sms, s);
+    case 1: return record_tma_variant<3, 256, 8>(v, a, num_sms, s, copy_warp);
+    case 2: return record_tma_variant<2, 128, 16>(v, a, num_sms, s, copy_warp);
+    case 3: return record_tma_variant<4, 256, 6>(v, a, num_sms, s, copy_warp);
+    case 4: return record_tma_variant<2, 256, 12>(v, a, num_sms, s, copy_warp);
+    case 5: return record_tma_variant<4, 128, 12>(v, a, num_sms, s, copy_warp);
+    case 6: return record_tma_variant<3, 128, 14>(v, a, num_sms, s, copy_warp);
+    case 7: return record_tma_variant<3, 256, 8, 128>(v, a, num_sms, s, copy_warp);
+    case 8: return record_tma_variant<2, 128, 12, 128>(v, a, num_sms, s, copy_warp);
+    case 9: return record_tma_variant<2, 256, 8, 128>(v, a, num_sms, s, copy_warp);
+    case 10: return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s, copy_warp);
+    case 11: return record_tma_variant<3, 64, 28, 32>(v, a, num_sms, s, copy_warp);
+    case 12: return record_tma_variant<2, 128, 24, 32>(v, a, num_sms, s, copy_warp);
+    case 13: return record_tma_variant<3, 256, 8, 64, 1>(v, a, num_sms, s, copy_warp);
+    case 14: return record_tma_variant<2, 256, 8, 64, 1>(v, a, num_sms, s, copy_warp);
+    case 15: return record_tma_variant<2, 64, 16, 32, 1>(v, a, num_sms, s, copy_warp);
+    case 16: return record_tma_variant<2, 128, 16, 32, 1>(v, a, num_sms, s, copy_warp);
+    case 17: return record_tma_variant<2, 128, 12, 64, 1>(v, a, num_sms, s, copy_warp);
     default: break;
   }
 #endif
-  if (a.nchains <= (int64_t)num_sms * 8) return record_tma_variant<3, 256, 8, 128>(v, a, num_sms, s);
-  return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s);
+  if (a.nchains <= (int64_t)num_sms * 8) return record_tma_variant<3, 256, 8, 64, 1>(v, a, num_sms, s, copy_warp);
+  return record_tma_variant<2, 64, 32, 32>(v, a, num_sms, s, copy_warp);
 }
 
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms, cudaStream_t s) {

@@ -375,6 +375,26 @@ __device__ __forceinline__ int block_first_mismatch(const int32_t *__restrict__ 
   }
 }
 
+// ---- barriers over a subset of the CTA ---------------------------------------------------
+// BAR == 0: the whole CTA (__syncthreads); otherwise named barrier BAR over the first NT
+// threads - a warp-specialised kernel keeps its other warps out of the compare's barriers.
+template <int NT, int BAR>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+template <int NT, int BAR>
+__device__ __forceinline__ int group_or(int pred) {
+  if constexpr (BAR == 0) {
+    return __syncthreads_or(pred);
+  } else {
+    int r;
+    asm volatile("{ .reg .pred p, q; setp.ne.s32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.s32 %0, 1, 0, q; }"
+                 : "=r"(r) : "r"(pred), "n"(BAR), "n"(NT) : "memory");
+    return r;
+  }
+}
+
 // ---- TMA (cp.async.bulk) staged compare ---------------------------------------------------
 // Same contract as block_first_mismatch, but the query and history chunks are moved into a
 // ring of shared-memory stages by the bulk-copy engine (one elected thread issues, an
@@ -427,7 +447,7 @@ __device__ __forceinline__ void tma_ring_init(TmaRing<NT, S, CHV> &rg) {
 // s_cap (optional, int[2 * NT / 32 + 2]): also capture the query's and the history's token
 // at the first mismatch (out of the shared-memory stage that held it) into s_cap[2 * NT / 32]
 // and s_cap[2 * NT / 32 + 1], so the caller needs no global load for them.
-template <int NT, int S, int CHV>
+template <int NT, int S, int CHV, int BAR = 0>
 __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restrict__ q, const int32_t *__restrict__ a,
                                                         int lo, int hi, int *s_red, TmaRing<NT, S, CHV> &rg,
                                                         int *s_cap = nullptr) {
@@ -496,7 +516,7 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
         }
       }
     }
-    if (__syncthreads_or(first != 0x7fffffff)) {
+    if (group_or<NT, BAR>(first != 0x7fffffff)) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       unsigned wmin = __reduce_min_sync(0xffffffffu, (unsigned)first);
       if (lane == 0) s_red[warp] = (int)wmin;
@@ -504,7 +524,7 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
         s_cap[2 * warp] = fq;
         s_cap[2 * warp + 1] = fa;
       }
-      __syncthreads();
+      group_sync<NT, BAR>();
       int r = 0x7fffffff, rw = 0;
 #pragma unroll
       for (int w = 0; w < NT / 32; w++)
@@ -523,9 +543,9 @@ __device__ __forceinline__ int block_first_mismatch_tma(const int32_t *__restric
   // in a stage after it is reused)
   const int issued = min(nch, c - 1 + S);  // prologue issued S, each consumed chunk one more
   for (int d = c; d < issued; d++) mbar_wait(&rg.bar[(base + d) % S], ((base + d) / S) & 1);
-  __syncthreads();
+  group_sync<NT, BAR>();
   if (threadIdx.x == 0) rg.chunks = base + (uint32_t)issued;
-  __syncthreads();
+  group_sync<NT, BAR>();
   return result;
 }
 

@@ -1036,13 +1036,15 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       for (int64_t k = 0; k < n; k++) qend = std::max<int64_t>(qend, doff[k] + round_up(h_len[k], 4));
       dv.qv_lo = (int64_t)(tok_base - s->v.arena);
       dv.qv_hi = dv.qv_lo + qend;
+      int copy_warp = 0;
       {
         ProfScope ps(s, 1, s->stream);
-        ck(tms::launch_record(dv, ra, s->num_sms, s->stream), "record");
+        ck(tms::launch_record(dv, ra, s->num_sms, s->stream, &copy_warp), "record");
       }
       tr.mark("launch1");
       ProfScope ps(s, 7, s->stream);
-      ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
+      if (copy_warp) ck(tms::launch_record_finish(dv, ra, s->num_sms, s->stream), "record finish");
+      else ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
       tr.mark("launch2");
     }
     // ---- results back (chain order), into the host mirror in batch order
