@@ -400,6 +400,18 @@ def measure_c4(args, rank, world, local, dev):
                 step()
             torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) / 1e3
+    # A/B of the north star's hash-first filter: the per-128-token block
+    # hashes of the query batch it would have to compute before it could filter anything
+    nq = (dq[0][1].numel() // 128) * 128
+    hashes = torch.empty(nq // 128, dtype=torch.int64, device=dev)
+    for _ in range(3):
+        store.block_hashes(dq[0][1][:nq], hashes, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    store.profile_begin(reserve=64)
+    for _ in range(args.steps):
+        store.block_hashes(dq[0][1][:nq], hashes, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    hash_ms, hash_n = store.profile_end("block_hash")
     log(f"rank {rank}: c4 device-timed region {1e3 * elapsed:.3f} ms for {args.steps} steps (walk {walk_ms:.3f} ms "
         f"over {walk_n} launches; host enqueue {1e3 * t_enq:.3f} ms)")
     if world > 1:
@@ -473,6 +485,12 @@ def measure_c4(args, rank, world, local, dev):
                      "event_ms_avg_per_launch": walk_ms / max(walk_n, 1),
                      "planner_ms_avg": plan_ms / max(plan_n, 1)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "hash_filter_ab": {"k1_ms_per_batch": k_avg * 1e3, "block_hash_ms_per_batch": hash_ms / max(hash_n, 1),
+                           "hash_first_ms_per_batch_lower_bound": k_avg * 1e3 + hash_ms / max(hash_n, 1),
+                           "query_words_hashed": nq,
+                           "note": "tm_block_hashes over the batch's query buffer (what a hash-first filter computes "
+                                   "before it can prune); an equal hash never proves a match, so the exact compare "
+                                   "that follows reads the same 8 B per compared token: hash-first can only add time"},
         "gpu_launches": int(walk_n + plan_n),  # our kernels in the timed region (CUDA-event bracketed)
         "timing": ("CUDA events on the launching stream around K back-to-back steps, enqueued behind a "
                    "device-side spin gate (host launch jitter excluded); max over ranks"

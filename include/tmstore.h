@@ -231,12 +231,20 @@ int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *co
 int tm_store_save(tm_store *store, const char *path);
 int tm_store_load(tm_store *store, const char *path);
 
+/* Per-block token hashes of a device buffer: out[b] = hash of words [128 b, 128 b + 128)
+ * (n_words a multiple of 128; device pointers; asynchronous on `stream`).  The building
+ * block of the north star's hash-first candidate filter, kept to measure it against the
+ * exact walk (hashing the query costs a full extra read of it, and an equal
+ * hash never proves a match, so the filter cannot remove bytes from an exact LPM). */
+int tm_block_hashes(tm_store *store, const int32_t *tokens, int64_t n_words, uint64_t *out, void *stream);
+
 /* Per-kernel CUDA-event timing for benchmarks.  tm_profile_begin starts recording an
  * event pair around every launch; tm_profile_end(kind) waits for them and returns the
  * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */
 enum {
   TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3,
-  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6, TM_KERNEL_RECORD_COPY = 7
+  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6, TM_KERNEL_RECORD_COPY = 7,
+  TM_KERNEL_BLOCK_HASH = 8
 };
 int tm_profile_begin(tm_store *store);
 /* Create the event pairs of `pairs` launches per kernel kind up front (so a timed region

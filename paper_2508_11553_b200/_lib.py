@@ -49,6 +49,7 @@ SIGNATURES = {
     "tm_synchronize": (C.c_int, [_P]),
     "tm_profile_begin": (C.c_int, [_P]),
     "tm_profile_reserve": (C.c_int, [_P, _I64]),
+    "tm_block_hashes": (C.c_int, [_P, _P, _I64, _P, _P]),
     "tm_store_save": (C.c_int, [_P, C.c_char_p]),
     "tm_store_load": (C.c_int, [_P, C.c_char_p]),
     "tm_route_desc_bytes": (C.c_int, [_P]),

@@ -2241,6 +2241,36 @@ cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Per-block token hashes (the north star's "per-block prefix hashes", measured as an A/B
+// against the exact walk): one warp per 128-word block, each lane mixes its
+// int4, xor-reduce, finalise.  out[b] = hash of words [128 b, 128 b + 128).
+__global__ void __launch_bounds__(256) k_block_hash(const int32_t *__restrict__ tok, int64_t nblocks, uint64_t *out) {
+  constexpr int U = 8;  // blocks per warp and round: 8 int4 loads in flight per lane
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * U; b0 < nblocks; b0 += warps * U) {
+    int4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      x[u] = ldg_stream_if(reinterpret_cast<const int4 *>(tok) + (b0 + u) * 32 + lane, b0 + u < nblocks);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      uint64_t h = mix64(((uint64_t)(uint32_t)x[u].x << 32 | (uint32_t)x[u].y) + 0x9e3779b97f4a7c15ull * (2 * lane + 1));
+      h ^= mix64(((uint64_t)(uint32_t)x[u].z << 32 | (uint32_t)x[u].w) + 0x9e3779b97f4a7c15ull * (2 * lane + 2));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+      if (lane == 0 && b0 + u < nblocks) out[b0 + u] = mix64(h);
+    }
+  }
+}
+
+cudaError_t launch_block_hash(const int32_t *tok, int64_t nblocks, uint64_t *out, int num_sms, cudaStream_t s) {
+  if (nblocks < 1) return cudaSuccess;
+  const int64_t grid = std::min<int64_t>((nblocks * 32 / 8 + 255) / 256, (int64_t)num_sms * 8);
+  k_block_hash<<<(int)std::max<int64_t>(grid, 1), 256, 0, s>>>(tok, nblocks, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s) {
   k_fill_u64<<<1024, 256, 0, s>>>(p, n, val);
   return cudaGetLastError();

@@ -75,6 +75,7 @@ cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t 
                           int64_t ocap, cudaStream_t s);
 cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s);
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
+cudaError_t launch_block_hash(const int32_t *tok, int64_t nblocks, uint64_t *out, int num_sms, cudaStream_t s);
 int export_tile_tokens();
 cudaError_t launch_route(char *region, const RouteHead &head, cudaStream_t s);
 // pack the region's query tokens into its 18-bit planes (RouteDesc::lo_off / hi_off)

@@ -198,7 +198,7 @@ struct tm_store {
   int plan_roots = 0;           // planner also resolves root rows (TM_PLAN_ROOTS=1)
   tms::Sched *sched = nullptr;  // walk scheduler block (self-cleaning)
   bool profile = false;
-  static constexpr int kProfKinds = 8;
+  static constexpr int kProfKinds = 9;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kProfKinds];
   size_t ev_used[kProfKinds] = {};
 };
@@ -1814,6 +1814,16 @@ int tm_store_load(tm_store *s, const char *path) {
       throw;
     }
     fclose(f);
+  });
+}
+
+int tm_block_hashes(tm_store *s, const int32_t *tokens, int64_t n_words, uint64_t *out, void *stream) {
+  NvtxRange nvtx_("tm_block_hashes");
+  return guarded(s, [&] {
+    if (n_words < 0 || n_words % 128) fail(TM_EINVAL, "n_words must be a multiple of 128");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    ProfScope ps(s, 8, st);
+    ck(tms::launch_block_hash(tokens, n_words / 128, out, s->num_sms, st), "block hash");
   });
 }
 

@@ -162,7 +162,7 @@ class DeviceStore:
         return st
 
     KERNELS = {"walk": 0, "commit": 1, "export": 2, "plan": 3, "route": 4, "route_pack": 5, "route_wait": 6,
-               "record_copy": 7}
+               "record_copy": 7, "block_hash": 8}
 
     def profile_begin(self, reserve: int = 0):
         """Start recording CUDA events around every kernel launch of this store (with
@@ -295,6 +295,14 @@ class DeviceStore:
         check(self.lib.tm_match_batch(self.h, sids.numel(), TM_MEM_DEVICE, _tptr(sids), _tptr(tokens), _tptr(tok_off),
                                       _tptr(tok_len), _tptr(out_matched), _tptr(out_parent), _tptr(out_dup),
                                       self._stream_arg(stream)))
+
+    def block_hashes(self, tokens, out, stream=None):
+        """Per-128-word block hashes of a device token buffer (tm_block_hashes)."""
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(self.lib.tm_block_hashes(self.h, _tptr(tokens), tokens.numel(), _tptr(out), self._stream_arg(stream)))
 
     # -- export (trajectory assembly) ---------------------------------------------------
     def rows_total(self, rows) -> int:
