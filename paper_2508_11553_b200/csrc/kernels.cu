@@ -1159,6 +1159,20 @@ __device__ void record_copy_warp(const DevView &v, const Batch &b, RecShared &sh
   }
 }
 
+// K2b after the warp-specialised K2: every new row switches to its arena copy (virtual
+// base, runs; a prefix row has none), a parent's extension hint pointing at it follows.
+__device__ __forceinline__ void record_finish_entry(const DevView &v, const Batch &b, int64_t e) {
+  if (b.o_dup[e] >= 0) return;
+  const int64_t m = b.o_m[e], L = b.len[e], row = b.c_row[e];
+  const bool own = L > m;
+  const int64_t vb = own ? b.c_vb[e] : -m;
+  v.row_vb[row] = vb;
+  v.row_run0[row] = own ? b.c_run0[e] : 0;
+  v.row_nrun[row] = own ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
+  const int64_t par = b.o_parent[e];
+  if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
+}
+
 // K2, chain part.  NCW = 0: NT walk threads do everything on the chain's path and
 // k_record_copy moves the suffixes afterwards.  NCW = 1: a 32-thread copy warp beside the
 // NT walk threads (named barrier 1 keeps it out of theirs) moves each committed entry's
@@ -1176,8 +1190,10 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
     sh.q_head = sh.q_read = sh.q_closed = 0;
   }
   __syncthreads();
+  const bool fused = NCW && a.fuse_finish && gridDim.x == 1;  // one CTA: finish here, no second launch
   if (NCW && threadIdx.x >= NT) {
     record_copy_warp(v, b, sh);
+    if (fused) asm volatile("bar.sync 2, %0;" ::"n"(NT + 32) : "memory");
     return;
   }
   // the first wave takes chains by CTA index; later chains come from the work counter,
@@ -1264,24 +1280,21 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
     __threadfence_block();
     *(volatile int *)&sh.q_closed = 1;
   }
+  if (fused) {  // after the copy warp drained the queue: the rows' bases, the counters, the scheduler
+    asm volatile("bar.sync 2, %0;" ::"n"(NT + 32) : "memory");
+    __threadfence_block();
+    for (int64_t e = threadIdx.x; e < b.n; e += NT) record_finish_entry(v, b, e);
+    group_sync<NT, BAR>();
+    if (threadIdx.x == 0) a.sched->work = 0;
+    if (a.ctr_out && threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
+  }
 }
 
-// K2b after the warp-specialised K2: every new row switches to its arena copy (virtual
-// base, runs; a prefix row has none), a parent's extension hint pointing at it follows.
 __global__ void __launch_bounds__(256) k_record_finish(DevView v, RecordArgs a) {
   const Batch &b = a.b;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.sched->work = 0;  // k_record's work counter, for the next launch
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b.n; e += (int64_t)gridDim.x * blockDim.x) {
-    if (b.o_dup[e] >= 0) continue;
-    const int64_t m = b.o_m[e], L = b.len[e], row = b.c_row[e];
-    const bool own = L > m;
-    const int64_t vb = own ? b.c_vb[e] : -m;
-    v.row_vb[row] = vb;
-    v.row_run0[row] = own ? b.c_run0[e] : 0;
-    v.row_nrun[row] = own ? (int32_t)(b.run_off[e + 1] - b.run_off[e] - b.c_firstrun[e]) : 0;
-    const int64_t par = b.o_parent[e];
-    if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
-  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b.n; e += (int64_t)gridDim.x * blockDim.x)
+    record_finish_entry(v, b, e);
   if (a.ctr_out && gridDim.x == 1) {  // the only CTA, and k_record is done: counters beside the results
     __syncthreads();
     if (threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
@@ -2079,8 +2092,10 @@ static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int
     if (occ < 1) occ = 1;
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
-  k_record_tma<NT, NCW, S, CHV, MINB><<<(int)grid, NT + 32 * NCW, 0, s>>>(v, a);
-  *copy_warp = NCW;
+  RecordArgs ra = a;
+  ra.fuse_finish = NCW && grid == 1 ? 1 : 0;
+  k_record_tma<NT, NCW, S, CHV, MINB><<<(int)grid, NT + 32 * NCW, 0, s>>>(v, ra);
+  *copy_warp = ra.fuse_finish ? 2 : NCW;
   return cudaGetLastError();
 }
 

@@ -66,7 +66,8 @@ int64_t plan_items_ints(int64_t n);
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 struct RecordArgs;
 // K2: the chains.  *copy_warp = 1: the suffixes were copied by copy warps inside it - follow with
-// launch_record_finish; 0: follow with launch_record_copy (same stream, right after)
+// launch_record_finish; 2: the single CTA also finished the rows - nothing follows; 0: follow
+// with launch_record_copy (same stream, right after)
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s, int *copy_warp);
 cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_record_finish(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s);

@@ -1043,8 +1043,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       }
       tr.mark("launch1");
       ProfScope ps(s, 7, s->stream);
-      if (copy_warp) ck(tms::launch_record_finish(dv, ra, s->num_sms, s->stream), "record finish");
-      else ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
+      if (copy_warp == 1) ck(tms::launch_record_finish(dv, ra, s->num_sms, s->stream), "record finish");
+      else if (copy_warp == 0) ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
       tr.mark("launch2");
     }
     // ---- results back (chain order), into the host mirror in batch order
