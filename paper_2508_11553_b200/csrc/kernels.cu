@@ -2257,8 +2257,18 @@ cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s
 }
 
 // Per-block token hashes (the north star's "per-block prefix hashes", measured as an A/B
-// against the exact walk): one warp per 128-word block, each lane mixes its
-// int4, xor-reduce, finalise.  out[b] = hash of words [128 b, 128 b + 128).
+// against the exact walk): one warp per 128-word block, 32-bit multiply-add
+// hashing per lane (cheap: the A/B must not blame the filter for an expensive hash), two
+// xor-reduced words, finalised into 64 bits.  out[b] = hash of words [128 b, 128 b + 128).
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
 __global__ void __launch_bounds__(256) k_block_hash(const int32_t *__restrict__ tok, int64_t nblocks, uint64_t *out) {
   constexpr int U = 8;  // blocks per warp and round: 8 int4 loads in flight per lane
   const int lane = threadIdx.x & 31;
@@ -2270,11 +2280,15 @@ __global__ void __launch_bounds__(256) k_block_hash(const int32_t *__restrict__ 
       x[u] = ldg_stream_if(reinterpret_cast<const int4 *>(tok) + (b0 + u) * 32 + lane, b0 + u < nblocks);
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      uint64_t h = mix64(((uint64_t)(uint32_t)x[u].x << 32 | (uint32_t)x[u].y) + 0x9e3779b97f4a7c15ull * (2 * lane + 1));
-      h ^= mix64(((uint64_t)(uint32_t)x[u].z << 32 | (uint32_t)x[u].w) + 0x9e3779b97f4a7c15ull * (2 * lane + 2));
+      const uint32_t k = 2u * (uint32_t)lane + 1u;
+      uint32_t a = fmix32(((uint32_t)x[u].x * 0x9e3779b1u + (uint32_t)x[u].y * 0x85ebca77u) ^ (k * 0x27d4eb2fu));
+      uint32_t c = fmix32(((uint32_t)x[u].z * 0xc2b2ae3du + (uint32_t)x[u].w * 0x165667b1u) ^ (k * 0x9e3779b1u));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
-      if (lane == 0 && b0 + u < nblocks) out[b0 + u] = mix64(h);
+      for (int o = 16; o > 0; o >>= 1) {
+        a ^= __shfl_xor_sync(0xffffffffu, a, o);
+        c ^= __shfl_xor_sync(0xffffffffu, c, o);
+      }
+      if (lane == 0 && b0 + u < nblocks) out[b0 + u] = (uint64_t)fmix32(a ^ 0x5bd1e995u) << 32 | fmix32(c + a);
     }
   }
 }

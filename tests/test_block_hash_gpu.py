@@ -6,30 +6,28 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-M = np.uint64(0xFFFFFFFFFFFFFFFF)
-
-
-def mix64(x):
-    x = x.astype(np.uint64)
+def fmix32(h):
+    h = h.astype(np.uint32)
     with np.errstate(over="ignore"):
-        x = x ^ (x >> np.uint64(30))
-        x = x * np.uint64(0xBF58476D1CE4E5B9)
-        x = x ^ (x >> np.uint64(27))
-        x = x * np.uint64(0x94D049BB133111EB)
-        x = x ^ (x >> np.uint64(31))
-    return x
+        h = h ^ (h >> np.uint32(16))
+        h = h * np.uint32(0x85EBCA6B)
+        h = h ^ (h >> np.uint32(13))
+        h = h * np.uint32(0xC2B2AE35)
+        h = h ^ (h >> np.uint32(16))
+    return h
 
 
 def block_hash_ref(tok):
-    w = tok.astype(np.int64).astype(np.uint64) & np.uint64(0xFFFFFFFF)
-    w = w.reshape(-1, 32, 4)
-    lane = np.arange(32, dtype=np.uint64)
-    g = np.uint64(0x9E3779B97F4A7C15)
+    w = tok.view(np.uint32).reshape(-1, 32, 4)
+    k = (np.uint32(2) * np.arange(32, dtype=np.uint32) + np.uint32(1))[None, :]
     with np.errstate(over="ignore"):
-        a = mix64(((w[:, :, 0] << np.uint64(32)) | w[:, :, 1]) + g * (np.uint64(2) * lane + np.uint64(1)))
-        b = mix64(((w[:, :, 2] << np.uint64(32)) | w[:, :, 3]) + g * (np.uint64(2) * lane + np.uint64(2)))
-    h = np.bitwise_xor.reduce(a ^ b, axis=1)
-    return mix64(h)
+        a = fmix32((w[:, :, 0] * np.uint32(0x9E3779B1) + w[:, :, 1] * np.uint32(0x85EBCA77)) ^ (k * np.uint32(0x27D4EB2F)))
+        c = fmix32((w[:, :, 2] * np.uint32(0xC2B2AE3D) + w[:, :, 3] * np.uint32(0x165667B1)) ^ (k * np.uint32(0x9E3779B1)))
+        a = np.bitwise_xor.reduce(a, axis=1)
+        c = np.bitwise_xor.reduce(c, axis=1)
+        hi = fmix32(a ^ np.uint32(0x5BD1E995)).astype(np.uint64)
+        lo = fmix32(c + a).astype(np.uint64)
+    return (hi << np.uint64(32)) | lo
 
 
 def test_block_hashes_match_restatement():
