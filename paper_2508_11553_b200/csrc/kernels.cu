@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
 // A chain is serial, so its cost is the latency of each entry's dependent steps, not its
 // bytes: k_record keeps only the steps the NEXT entry of the chain depends on (the walk,
 // the row table, the branch index, the session counters) and leaves everything else to
-// k_record_copy, which runs after it over all entries at once: arena / run-table
+// the chain's end (or a copy warp beside the chain): arena / run-table
 // allocation, the novel suffix copy, the metadata runs.  Until then a committed row is
 // read where its tokens already are - in its entry's query (read-only for the launch).
 // Inside an entry, the session's counters and path-copy state live in shared memory for
@@ -854,7 +854,7 @@ struct RecShared {
   // copy warp moves into the arena while the walk warps go on with the chain
   int q_e[kRecQ], q_m[kRecQ], q_L[kRecQ];
   long long q_off[kRecQ];
-  int q_head, q_read, q_closed;
+  int q_head, q_read, q_closed, q_done;
   // entry prefetch
   long long pre_off[kRecPre];
   int pre_len[kRecPre], pre_q0[kRecPre];
@@ -970,7 +970,7 @@ __device__ __forceinline__ void record_walk(const DevView &v, const Batch &b, Re
 }
 
 // Commit the walked entry e (thread 0): row table, the parent's extension hint, the
-// branch index, the session counters (shared memory).  Arena / run slots: k_record_copy.
+// branch index, the session counters (shared memory).  Arena / run slots: the chain's copy.
 __device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, int64_t e, RecShared &sh) {
   const int64_t m = sh.m, L = sh.len, par = sh.parent;
   sh.pcw_len = 0;  // no path-copy write unless this entry's row takes the copy (below)
@@ -1090,7 +1090,7 @@ __device__ __forceinline__ void record_commit(const DevView &v, const Batch &b, 
 // order, allocates their arena lines and run slots (atomics off the chain's serial path),
 // moves the novel suffix [m, L) from the query into the arena (8 int4 loads in flight per
 // lane) and the runs (first clamped to m) into the run table.  The row keeps reading its
-// query until k_record_finish switches its virtual base.
+// query until the chain's end switches its virtual base.
 __device__ void record_copy_warp(const DevView &v, const Batch &b, RecShared &sh) {
   const int lane = threadIdx.x & 31;
   for (int i = 0;; i++) {
@@ -1155,12 +1155,14 @@ __device__ void record_copy_warp(const DevView &v, const Batch &b, RecShared &sh
       b.c_vb[e] = vb;
       b.c_run0[e] = run0;
       b.c_firstrun[e] = fr;
+      __threadfence_block();
+      *(volatile int *)&sh.q_done = i + 1;  // records complete in queue order (one copy warp)
     }
   }
 }
 
-// K2b after the warp-specialised K2: every new row switches to its arena copy (virtual
-// base, runs; a prefix row has none), a parent's extension hint pointing at it follows.
+// A committed row switches to its arena copy (virtual base, runs; a prefix row has none),
+// and a parent's extension hint pointing at it follows.
 __device__ __forceinline__ void record_finish_entry(const DevView &v, const Batch &b, int64_t e) {
   if (b.o_dup[e] >= 0) return;
   const int64_t m = b.o_m[e], L = b.len[e], row = b.c_row[e];
@@ -1173,257 +1175,207 @@ __device__ __forceinline__ void record_finish_entry(const DevView &v, const Batc
   if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
 }
 
-// K2, chain part.  NCW = 0: NT walk threads do everything on the chain's path and
-// k_record_copy moves the suffixes afterwards.  NCW = 1: a 32-thread copy warp beside the
-// NT walk threads (named barrier 1 keeps it out of theirs) moves each committed entry's
-// suffix while the chain goes on, and k_record_finish only switches the rows' bases.
+// Chain end without a copy warp: the walk group allocates the chain's arena lines and run
+// slots (one scan, one atomic per counter), moves every suffix and its runs, and switches
+// the rows.  Only this CTA ever reads the session's rows inside the launch, so switching
+// here is safe; chains that finish early overlap their copies with the walks of others.
+template <int NT, int BAR>
+__device__ void record_chain_copy(const DevView &v, const Batch &b, int64_t e0, int64_t e1, long long *s_scan) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = e0; base < e1; base += NT) {
+    const int64_t e = base + threadIdx.x;
+    long long words = 0, runs = 0;
+    int fr = 0;
+    int64_t m = 0;
+    if (e < e1 && b.o_dup[e] < 0) {
+      m = b.o_m[e];
+      const int64_t L = b.len[e];
+      if (L > m) {
+        words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
+        fr = first_run_at(b, e, m);
+        runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
+      }
+    }
+    long long iw = words, ir = runs;  // inclusive scans within the warp, then across warps
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long tw = __shfl_up_sync(0xffffffffu, iw, d), tr = __shfl_up_sync(0xffffffffu, ir, d);
+      if (lane >= d) { iw += tw; ir += tr; }
+    }
+    if (lane == 31) { s_scan[2 * warp] = iw; s_scan[2 * warp + 1] = ir; }
+    group_sync<NT, BAR>();
+    if (threadIdx.x == 0) {
+      long long tw = 0, tr = 0;
+      for (int w = 0; w < NT / 32; w++) {
+        const long long x = s_scan[2 * w], y = s_scan[2 * w + 1];
+        s_scan[2 * w] = tw;
+        s_scan[2 * w + 1] = tr;
+        tw += x;
+        tr += y;
+      }
+      s_scan[8] = tw ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)tw) : 0;
+      s_scan[9] = tr ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)tr) : 0;
+    }
+    group_sync<NT, BAR>();
+    if (words) {
+      const long long vb = s_scan[8] + s_scan[2 * warp] + iw - words - (m / kAlignWords) * kAlignWords;
+      const long long run0 = s_scan[9] + s_scan[2 * warp + 1] + ir - runs;
+      TM_DCHECK(v, vb + (m & ~31ll) >= 0 && vb + ((b.len[e] + 31) & ~31ll) <= v.arena_cap, kErrArena);
+      TM_DCHECK(v, run0 >= 0 && run0 + runs <= v.run_cap, kErrRun);
+      b.c_vb[e] = vb;
+      b.c_run0[e] = run0;
+      b.c_firstrun[e] = fr;
+    }
+    group_sync<NT, BAR>();
+  }
+  for (int64_t e = e0; e < e1; e++) {  // the whole group on each entry's suffix and runs
+    if (b.o_dup[e] >= 0) continue;
+    const int64_t m = b.o_m[e], L = b.len[e];
+    if (L <= m) continue;
+    block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + b.c_vb[e]), reinterpret_cast<const int4 *>(b.tok + b.off[e]),
+                            m >> 2, (L + 3) >> 2);
+    const int64_t r0 = b.run_off[e] + b.c_firstrun[e], nr = b.run_off[e + 1] - r0, d0 = b.c_run0[e];
+    for (int64_t k = threadIdx.x; k < nr; k += NT) {
+      const int32_t st = b.run_start[r0 + k];
+      v.run_start[d0 + k] = (int32_t)(st > m ? (int64_t)st : m);
+      v.run_origin[d0 + k] = b.run_origin[r0 + k];
+      v.run_version[d0 + k] = b.run_version[r0 + k];
+    }
+  }
+  group_sync<NT, BAR>();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += NT) record_finish_entry(v, b, e);
+}
+
+// K2: the chains.  NCW = 0: NT walk threads; at each chain's end they copy its suffixes
+// and switch its rows (record_chain_copy).  NCW = 1: a 32-thread copy warp beside the NT
+// walk threads (named barrier 1 keeps it out of theirs) moves each committed entry's
+// suffix while the chain goes on; at the chain's end the walk threads wait for its last
+// record and switch the rows.  Either way one launch records the whole batch; the last CTA
+// out snapshots the counters for the host.
 template <int NT, int NCW, int S, int CHV, int MINB>
 __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, RecordArgs a) {
   static_assert(NCW == 0 || NCW == 1, "one copy warp: the queue has one reader");
+  static_assert(NT <= 128, "scan scratch for <= 4 warps");
   constexpr int BAR = NCW ? 1 : 0;
   const Batch &b = a.b;
   __shared__ RecShared sh;
   __shared__ long long s_item;
+  __shared__ long long s_scan[10];
   __shared__ TmaRing<NT, S, CHV> rg;
   tma_ring_init(rg);  // every thread: __syncthreads inside
   if (NCW && threadIdx.x == 0) {
-    sh.q_head = sh.q_read = sh.q_closed = 0;
+    sh.q_head = sh.q_read = sh.q_closed = sh.q_done = 0;
   }
   __syncthreads();
-  const bool fused = NCW && a.fuse_finish && gridDim.x == 1;  // one CTA: finish here, no second launch
   if (NCW && threadIdx.x >= NT) {
     record_copy_warp(v, b, sh);
-    if (fused) asm volatile("bar.sync 2, %0;" ::"n"(NT + 32) : "memory");
-    return;
-  }
-  // the first wave takes chains by CTA index; later chains come from the work counter,
-  // which the next kernel on the stream leaves zeroed for the next launch
-  long long it = blockIdx.x;
-  for (;;) {
-    if (it >= a.nchains) break;
-    const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
-    if (threadIdx.x == 0) {  // the session, cached for the whole chain
-      const int32_t sid = (int32_t)a.chains[3 * it + 2];
-      sh.sid = sid;
-      sh.nrows = v.s_nrows[sid];
-      sh.stored = v.s_stored[sid];
-      sh.naive = v.s_naive[sid];
-      sh.pc_row = v.s_pc_row[sid];
-      sh.pc_vb = v.s_pc_vb[sid];
-      sh.pc_cap = v.s_pc_cap[sid];
-      if (sh.pc_row >= 0) {
-        sh.pc_rlen = v.row_len[sh.pc_row];
-        sh.pc_depth = v.row_depth[sh.pc_row];
+  } else {
+    // the first wave takes chains by CTA index; later chains come from the work counter
+    long long it = blockIdx.x;
+    for (;;) {
+      if (it >= a.nchains) break;
+      const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
+      if (threadIdx.x == 0) {  // the session, cached for the whole chain
+        const int32_t sid = (int32_t)a.chains[3 * it + 2];
+        sh.sid = sid;
+        sh.nrows = v.s_nrows[sid];
+        sh.stored = v.s_stored[sid];
+        sh.naive = v.s_naive[sid];
+        sh.pc_row = v.s_pc_row[sid];
+        sh.pc_vb = v.s_pc_vb[sid];
+        sh.pc_cap = v.s_pc_cap[sid];
+        if (sh.pc_row >= 0) {
+          sh.pc_rlen = v.row_len[sh.pc_row];
+          sh.pc_depth = v.row_depth[sh.pc_row];
+        }
+        for (int i = 0; i < kRecCache; i++) {
+          sh.rc_row[i] = -1;
+          sh.fc_row[i] = -1;
+        }
+        sh.rc_next = sh.fc_next = 0;
       }
-      for (int i = 0; i < kRecCache; i++) {
-        sh.rc_row[i] = -1;
-        sh.fc_row[i] = -1;
-      }
-      sh.rc_next = sh.fc_next = 0;
-    }
-    for (int64_t e = e0; e < e1; e++) {
-      const int k = (int)((e - e0) % kRecPre);
-      if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
+      for (int64_t e = e0; e < e1; e++) {
+        const int k = (int)((e - e0) % kRecPre);
+        if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
+          group_sync<NT, BAR>();
+          for (int t = threadIdx.x; t < kRecPre && e + t < e1; t += NT) {
+            const int64_t off = b.off[e + t];
+            sh.pre_off[t] = off;
+            sh.pre_len[t] = (int)b.len[e + t];
+            sh.pre_q0[t] = b.tok[off];
+          }
+        }
         group_sync<NT, BAR>();
-        for (int t = threadIdx.x; t < kRecPre && e + t < e1; t += NT) {
-          const int64_t off = b.off[e + t];
-          sh.pre_off[t] = off;
-          sh.pre_len[t] = (int)b.len[e + t];
-          sh.pre_q0[t] = b.tok[off];
+        if (threadIdx.x == 0) {
+          sh.off = sh.pre_off[k];
+          sh.len = sh.pre_len[k];
+          sh.q0 = sh.pre_q0[k];
+        }
+        group_sync<NT, BAR>();
+        record_walk<NT, BAR>(v, b, sh, rg);
+        if (threadIdx.x == 0) {
+          record_commit(v, b, e, sh);
+          if (NCW && sh.dup < 0 && sh.len > sh.m) {  // hand the suffix copy to the copy warp
+            const int head = sh.q_head;
+            while (head - *(volatile int *)&sh.q_read >= kRecQ) __nanosleep(100);
+            const int slot = head % kRecQ;
+            sh.q_e[slot] = (int)e;
+            sh.q_m[slot] = (int)sh.m;
+            sh.q_L[slot] = sh.len;
+            sh.q_off[slot] = sh.off;
+            __threadfence_block();
+            *(volatile int *)&sh.q_head = head + 1;
+          }
+        }
+        group_sync<NT, BAR>();
+        if (sh.pcw_len > 0) {  // path copy: [from, L) of the entry's query (congruent layout)
+          block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
+                                  reinterpret_cast<const int4 *>(b.tok + sh.off), sh.pcw_from >> 2, (sh.pcw_len + 3) >> 2);
+          // generic-proxy arena writes -> visible to the next entry's cp.async.bulk reads
+          asm volatile("fence.proxy.async.global;" ::: "memory");
         }
       }
-      group_sync<NT, BAR>();
-      if (threadIdx.x == 0) {
-        sh.off = sh.pre_off[k];
-        sh.len = sh.pre_len[k];
-        sh.q0 = sh.pre_q0[k];
-      }
-      group_sync<NT, BAR>();
-      record_walk<NT, BAR>(v, b, sh, rg);
-      if (threadIdx.x == 0) {
-        record_commit(v, b, e, sh);
-        if (NCW && sh.dup < 0 && sh.len > sh.m) {  // hand the suffix copy to the copy warp
-          const int head = sh.q_head;
-          while (head - *(volatile int *)&sh.q_read >= kRecQ) __nanosleep(100);
-          const int slot = head % kRecQ;
-          sh.q_e[slot] = (int)e;
-          sh.q_m[slot] = (int)sh.m;
-          sh.q_L[slot] = sh.len;
-          sh.q_off[slot] = sh.off;
+      if (threadIdx.x == 0) {  // write the session back
+        const int32_t sid = sh.sid;
+        v.s_nrows[sid] = sh.nrows;
+        v.s_stored[sid] = sh.stored;
+        v.s_naive[sid] = sh.naive;
+        v.s_pc_row[sid] = sh.pc_row;
+        v.s_pc_vb[sid] = sh.pc_vb;
+        v.s_pc_cap[sid] = sh.pc_cap;
+        if (NCW) {  // the copy warp has finished every record of this chain
+          const int target = sh.q_head;
+          while (*(volatile int *)&sh.q_done < target) __nanosleep(64);
           __threadfence_block();
-          *(volatile int *)&sh.q_head = head + 1;
         }
       }
       group_sync<NT, BAR>();
-      if (sh.pcw_len > 0) {  // path copy: [from, L) of the entry's query (congruent layout)
-        block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + sh.pcw_vb),
-                                reinterpret_cast<const int4 *>(b.tok + sh.off), sh.pcw_from >> 2, (sh.pcw_len + 3) >> 2);
-        // generic-proxy arena writes -> visible to the next entry's cp.async.bulk reads
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (NCW) {
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += NT) record_finish_entry(v, b, e);
+      } else {
+        record_chain_copy<NT, BAR>(v, b, e0, e1, s_scan);
       }
+      if (threadIdx.x == 0) s_item = (long long)gridDim.x + (long long)atomicAdd(&a.work[0], 1ull);
+      group_sync<NT, BAR>();
+      it = s_item;
+      group_sync<NT, BAR>();
     }
-    if (threadIdx.x == 0) {  // write the session back
-      const int32_t sid = sh.sid;
-      v.s_nrows[sid] = sh.nrows;
-      v.s_stored[sid] = sh.stored;
-      v.s_naive[sid] = sh.naive;
-      v.s_pc_row[sid] = sh.pc_row;
-      v.s_pc_vb[sid] = sh.pc_vb;
-      v.s_pc_cap[sid] = sh.pc_cap;
-      s_item = (long long)gridDim.x + (long long)atomicAdd(&a.sched->work, 1ull);
+    if (NCW && threadIdx.x == 0) {
+      __threadfence_block();
+      *(volatile int *)&sh.q_closed = 1;
     }
-    group_sync<NT, BAR>();
-    it = s_item;
-    group_sync<NT, BAR>();
   }
-  if (NCW && threadIdx.x == 0) {
-    __threadfence_block();
-    *(volatile int *)&sh.q_closed = 1;
-  }
-  if (fused) {  // after the copy warp drained the queue: the rows' bases, the counters, the scheduler
-    asm volatile("bar.sync 2, %0;" ::"n"(NT + 32) : "memory");
-    __threadfence_block();
-    for (int64_t e = threadIdx.x; e < b.n; e += NT) record_finish_entry(v, b, e);
-    group_sync<NT, BAR>();
-    if (threadIdx.x == 0) a.sched->work = 0;
-    if (a.ctr_out && threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
-  }
-}
-
-__global__ void __launch_bounds__(256) k_record_finish(DevView v, RecordArgs a) {
-  const Batch &b = a.b;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.sched->work = 0;  // k_record's work counter, for the next launch
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < b.n; e += (int64_t)gridDim.x * blockDim.x)
-    record_finish_entry(v, b, e);
-  if (a.ctr_out && gridDim.x == 1) {  // the only CTA, and k_record is done: counters beside the results
+  if (a.ctr_out) {  // the last CTA out: every counter update of the launch is done
     __syncthreads();
-    if (threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
-  }
-}
-
-// K2b (after k_record, all entries at once): allocate arena lines and run slots for every
-// new row (a block scan per CTA, one atomic per CTA and counter), move its novel suffix
-// [m, L) from the query into the arena (congruent mod 32 words; edge words land in the
-// row's own padding) and its metadata runs into the run table (first run clamped to m),
-// then switch the row's virtual base - and a parent's extension hint pointing at it - to
-// the arena.  CTA b owns entries [b*chunk, (b+1)*chunk), chunk <= NT: one thread per entry
-// for the allocation (one round trip of loads, then the scan and the atomics; an entry with
-// at most 4 runs reserves slots for all of them, so the search for the run holding m is
-// not on the way to the token copy), then one warp per entry for the copy, 8 int4 loads in
-// flight per lane.
-template <int NT>
-__global__ void __launch_bounds__(NT) k_record_copy(DevView v, RecordArgs a, int64_t chunk) {
-  const Batch &b = a.b;
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.sched->work = 0;  // k_record's work counter, for the next launch
-  __shared__ long long s_words[NT / 32], s_runs[NT / 32];
-  __shared__ long long s_base_w, s_base_r;
-  __shared__ long long s_vb[NT], s_src[NT], s_run0[NT], s_r0[NT], s_row[NT], s_par[NT];
-  __shared__ int s_m[NT], s_L[NT], s_nr[NT];
-  const int64_t e0 = blockIdx.x * chunk;
-  const int64_t e = e0 + threadIdx.x;
-  long long words = 0, runs = 0;
-  bool isnew = false;
-  int64_t m = 0, L = 0, off = 0, r0 = 0, row = 0, par = 0;
-  if (threadIdx.x < chunk && e < b.n) {  // one round trip: every load is independent
-    const int64_t dup = b.o_dup[e];
-    m = b.o_m[e];
-    L = b.len[e];
-    off = b.off[e];
-    r0 = b.run_off[e];
-    const int64_t r1 = b.run_off[e + 1];
-    row = b.c_row[e];
-    par = b.o_parent[e];
-    isnew = dup < 0;
-    if (isnew && L > m) {
-      words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
-      if (r1 - r0 > 4) r0 += first_run_at(b, e, m);  // many runs (deep chains): skip those before m now
-      runs = r1 - r0;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_item = atomicAdd(&a.work[1], 1ull) == gridDim.x - 1;
     }
-  }
-  // block-wide exclusive scans of words and runs
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  long long iw = words, ir = runs;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const long long tw = __shfl_up_sync(0xffffffffu, iw, d), tr = __shfl_up_sync(0xffffffffu, ir, d);
-    if (lane >= d) { iw += tw; ir += tr; }
-  }
-  if (lane == 31) { s_words[warp] = iw; s_runs[warp] = ir; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long tw = 0, tr = 0;
-    for (int w = 0; w < NT / 32; w++) {
-      const long long x = s_words[w], y = s_runs[w];
-      s_words[w] = tw;
-      s_runs[w] = tr;
-      tw += x;
-      tr += y;
-    }
-    s_base_w = tw ? (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)tw) : 0;
-    s_base_r = tr ? (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)tr) : 0;
-  }
-  __syncthreads();
-  s_L[threadIdx.x] = 0;  // L <= m: nothing to copy for this slot
-  s_m[threadIdx.x] = 0;
-  s_nr[threadIdx.x] = -1;  // -1: no row to finish
-  if (isnew) {
-    const long long vb = words ? s_base_w + s_words[warp] + iw - words - (m / kAlignWords) * kAlignWords : -m;
-    const long long run0 = runs ? s_base_r + s_runs[warp] + ir - runs : 0;
-    TM_DCHECK(v, !words || (vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap), kErrArena);
-    TM_DCHECK(v, run0 >= 0 && run0 + runs <= v.run_cap, kErrRun);
-    s_vb[threadIdx.x] = vb;
-    s_src[threadIdx.x] = off;
-    s_run0[threadIdx.x] = run0;
-    s_r0[threadIdx.x] = r0;
-    s_nr[threadIdx.x] = (int)runs;
-    s_m[threadIdx.x] = (int)m;
-    s_L[threadIdx.x] = (int)L;
-    s_row[threadIdx.x] = row;
-    s_par[threadIdx.x] = par;
-  }
-  __syncthreads();
-  for (int x = warp; x < (int)chunk; x += NT / 32) {
-    if (s_nr[x] < 0) continue;
-    const int64_t mx = s_m[x], Lx = s_L[x];
-    int fr = 0;
-    if (Lx > mx) {
-      const int4 *src = reinterpret_cast<const int4 *>(b.tok + s_src[x]);
-      int4 *dst = reinterpret_cast<int4 *>(v.arena + s_vb[x]);
-      const int64_t i1 = (Lx + 3) >> 2;
-      for (int64_t base = (mx >> 2) + lane; base < i1; base += 32 * 8) {
-        int4 t[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) t[k] = ldg_stream_if(src + base + 32 * k, base + 32 * k < i1);
-#pragma unroll
-        for (int k = 0; k < 8; k++) stg_if(dst + base + 32 * k, t[k], base + 32 * k < i1);
-      }
-      // runs overlapping [m, L) (the first clamped to m) keep their slot offsets inside the
-      // entry's reservation: the row's runs are [run0 + fr, run0 + nr)
-      const int64_t rb = s_r0[x], d0 = s_run0[x];
-      int64_t lo = 0, hi = s_nr[x];  // last run with start <= m
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (b.run_start[rb + mid] <= mx) lo = mid; else hi = mid;
-      }
-      fr = (int)lo;
-      for (int k = fr + lane; k < s_nr[x]; k += 32) {
-        const int32_t st = b.run_start[rb + k];
-        v.run_start[d0 + k] = (int32_t)(st > mx ? (int64_t)st : mx);
-        v.run_origin[d0 + k] = b.run_origin[rb + k];
-        v.run_version[d0 + k] = b.run_version[rb + k];
-      }
-    }
-    if (lane == 0) {
-      const int64_t row = s_row[x], par = s_par[x], vb = s_vb[x];
-      v.row_vb[row] = vb;
-      v.row_run0[row] = s_run0[x] + fr;
-      v.row_nrun[row] = Lx > mx ? (int32_t)(s_nr[x] - fr) : 0;
-      if (par >= 0 && v.row_ext[par] == row) v.row_ext_vb[par] = vb;
-    }
-  }
-  if (a.ctr_out && gridDim.x == 1) {  // the only CTA: every counter update is done (one D2H for the host)
     __syncthreads();
-    if (threadIdx.x < 4) a.ctr_out[threadIdx.x] = v.ctr[threadIdx.x];
+    if (s_item && threadIdx.x < 4) {
+      __threadfence();
+      a.ctr_out[threadIdx.x] = *(volatile long long *)&v.ctr[threadIdx.x];
+    }
   }
 }
 
@@ -2058,31 +2010,6 @@ cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStrea
   return walk_tma_variant<kTmaStages, kTmaChunk>(v, b, num_sms, s);
 }
 
-constexpr int kRecordCopyNT = 256;
-
-cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
-  if (a.b.n < 1) return cudaSuccess;
-  // chunk <= NT entries per CTA (the allocation scan is one entry per thread), a multiple
-  // of the CTA's warps (one warp per entry in the copy)
-  constexpr int kWarps = kRecordCopyNT / 32;
-  // a.ctr_out (small host batches): one CTA, which also snapshots the counters
-  const int64_t grid = a.ctr_out && a.b.n <= kRecordCopyNT
-                           ? 1
-                           : std::max<int64_t>((a.b.n + kRecordCopyNT - 1) / kRecordCopyNT,
-                                               std::min<int64_t>(a.b.n, (int64_t)num_sms * 8));
-  int64_t chunk = (a.b.n + grid - 1) / grid;
-  chunk = std::min<int64_t>(kRecordCopyNT, (chunk + kWarps - 1) / kWarps * kWarps);
-  k_record_copy<kRecordCopyNT><<<(int)((a.b.n + chunk - 1) / chunk), kRecordCopyNT, 0, s>>>(v, a, chunk);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_record_finish(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s) {
-  if (a.b.n < 1) return cudaSuccess;
-  const int64_t grid = a.ctr_out && a.b.n <= 256 ? 1 : std::min<int64_t>((a.b.n + 255) / 256, (int64_t)num_sms * 4);
-  k_record_finish<<<(int)grid, 256, 0, s>>>(v, a);
-  return cudaGetLastError();
-}
-
 template <int S, int CHV, int MINB, int NT = 64, int NCW = 0>
 static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s,
                                       int *copy_warp) {
@@ -2092,25 +2019,19 @@ static cudaError_t record_tma_variant(const DevView &v, const RecordArgs &a, int
     if (occ < 1) occ = 1;
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * occ, a.nchains));
-  RecordArgs ra = a;
-  ra.fuse_finish = NCW && grid == 1 ? 1 : 0;
-  k_record_tma<NT, NCW, S, CHV, MINB><<<(int)grid, NT + 32 * NCW, 0, s>>>(v, ra);
-  *copy_warp = ra.fuse_finish ? 2 : NCW;
+  k_record_tma<NT, NCW, S, CHV, MINB><<<(int)grid, NT + 32 * NCW, 0, s>>>(v, a);
+  *copy_warp = NCW;
   return cudaGetLastError();
 }
 
-// K2 = k_record_tma (chains: walk + commit, serial per session) + either k_record_copy
-// (arena allocation, suffixes and runs, all entries in parallel, after the chains) or -
-// with a copy warp in every chain CTA moving each entry's suffix while the chain goes on -
-// k_record_finish (the rows' bases only).  A chain's compare is TMA-staged (the stages
+// K2 = k_record_tma, one launch per batch.  A chain's compare is TMA-staged (the stages
 // live in shared memory, not registers).
 //   <= 8 chains per SM (c2, 1,000 chains): 64 walk threads + 1 copy warp, 3 x 4 KB stages
 //     per stream, every chain resident; the copies ride under the chains' latency-bound
-//     walks: c2 0.859 of peak (0.764 with the copies after the chains, 128 walk threads)
+//     walks
 //   more chains (c3, 4,000 chains of 2 entries): one-warp CTAs, 32 per SM, 2 x 1 KB stages,
-//     so up to 4,736 chains are resident at once; registers leave no room for copy warps
-//     (16 CTAs per SM with them: two waves), so k_record_copy follows: c3 0.524 (0.500 with
-//     copy warps)
+//     so up to 4,736 chains are resident at once (registers leave no room for copy warps);
+//     each chain copies its own suffixes at its end, overlapping the walks of the others
 // Tuning builds (-DTM_TUNING) select other shapes with TM_RECORD_VARIANT.
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s, int *copy_warp) {
   *copy_warp = 0;

@@ -209,10 +209,9 @@ struct Batch {
 struct RecordArgs {
   Batch b;                    // entries grouped by session chain, batch order inside a chain
   const int64_t *chains;      // per chain in processing order (longest first): first entry, end, session
-  int64_t *ctr_out;           // non-null: k_record_copy runs as ONE CTA and copies the 4 counters here
-  int32_t fuse_finish;        // set by launch_record: one warp-specialised CTA finishes the rows itself
+  int64_t *ctr_out;           // non-null: the last CTA out copies the 4 counters here (one D2H for the host)
   int64_t nchains;
-  Sched *sched;               // work counter (self-cleaning)
+  unsigned long long *work;   // [0] chain counter, [1] CTAs done: zeroed by the call's staging copy
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

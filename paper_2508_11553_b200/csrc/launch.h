@@ -65,12 +65,9 @@ cudaError_t launch_plan(const DevView &v, Batch &b, int64_t *root, int *items, c
 int64_t plan_items_ints(int64_t n);
 cudaError_t launch_walk(const DevView &v, const Batch &b, int num_sms, cudaStream_t s);
 struct RecordArgs;
-// K2: the chains.  *copy_warp = 1: the suffixes were copied by copy warps inside it - follow with
-// launch_record_finish; 2: the single CTA also finished the rows - nothing follows; 0: follow
-// with launch_record_copy (same stream, right after)
+// K2: records the whole batch in one launch (chains walked and committed, suffixes copied
+// into the arena, rows switched to it); *copy_warp = 1 when the chain CTAs carried a copy warp
 cudaError_t launch_record(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s, int *copy_warp);
-cudaError_t launch_record_copy(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s);
-cudaError_t launch_record_finish(const DevView &v, const RecordArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_export(const DevView &v, const ExportArgsHost &e, int num_sms, cudaStream_t s);
 cudaError_t launch_rehash(const DevView &v, const uint64_t *ok0, const uint64_t *ok1, const int64_t *oval,
                           int64_t ocap, cudaStream_t s);

@@ -949,7 +949,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     size_t o_sid = lay.add(4 * n), o_off = lay.add(8 * n), o_len = lay.add(8 * n), o_roff = lay.add(8 * (n + 1)),
            o_rs = lay.add(4 * total_runs), o_ro = lay.add(total_runs), o_rv = lay.add(4 * total_runs),
            o_tok = lay.add(4 * (size_t)(small_words + tms::kAlignWords)),
-           o_crow = lay.add(8 * n), o_chains = lay.add(24 * nchains);
+           o_crow = lay.add(8 * n), o_chains = lay.add(24 * nchains), o_work = lay.add(16);
     size_t in_bytes = lay.bytes;
     size_t o_m = lay.add(8 * n), o_par = lay.add(8 * n), o_dup = lay.add(8 * n), o_tn = lay.add(4 * n),
            o_sp = lay.add(4 * n), o_cloc = lay.add(4 * n), o_ctr = lay.add(8 * 4);
@@ -993,6 +993,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       rr += r1 - r0;
     }
     h_roff[n] = rr;
+    memset(h + o_work, 0, 16);  // the launch's chain counter and CTAs-done counter start at zero
     {  // chains in processing order: first entry, end, session
       int64_t *hc = (int64_t *)(h + o_chains);
       for (int64_t it = 0; it < nchains; it++) {
@@ -1028,33 +1029,26 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       b.c_firstrun = (int32_t *)(d + o_cfr);
       b.c_local = (int32_t *)(d + o_cloc);
       ra.chains = (const int64_t *)(d + o_chains);
-      ra.ctr_out = small ? (int64_t *)(d + o_ctr) : nullptr;  // single-CTA copy: counters beside the results
+      ra.ctr_out = (int64_t *)(d + o_ctr);  // the last CTA out snapshots the counters beside the results
       ra.nchains = nchains;
-      ra.sched = s->sched;
+      ra.work = (unsigned long long *)(d + o_work);
       tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
       int64_t qend = 0;
       for (int64_t k = 0; k < n; k++) qend = std::max<int64_t>(qend, doff[k] + round_up(h_len[k], 4));
       dv.qv_lo = (int64_t)(tok_base - s->v.arena);
       dv.qv_hi = dv.qv_lo + qend;
       int copy_warp = 0;
-      {
-        ProfScope ps(s, 1, s->stream);
-        ck(tms::launch_record(dv, ra, s->num_sms, s->stream, &copy_warp), "record");
-      }
-      tr.mark("launch1");
-      ProfScope ps(s, 7, s->stream);
-      if (copy_warp == 1) ck(tms::launch_record_finish(dv, ra, s->num_sms, s->stream), "record finish");
-      else if (copy_warp == 0) ck(tms::launch_record_copy(dv, ra, s->num_sms, s->stream), "record copy");
-      tr.mark("launch2");
+      ProfScope ps(s, 1, s->stream);
+      ck(tms::launch_record(dv, ra, s->num_sms, s->stream, &copy_warp), "record");
+      tr.mark("launch");
     }
     // ---- results back (chain order), into the host mirror in batch order
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
-    if (!small) enqueue_ctr_readback(s, s->stream);
     mark_done(s, s->stream);
     tr.mark("d2h+event");
     ck(cudaStreamSynchronize(s->stream), "record sync");
     tr.mark("sync");
-    const int64_t *ctr = small ? (const int64_t *)(h + o_ctr) : s->pin_ctr;
+    const int64_t *ctr = (const int64_t *)(h + o_ctr);
     if (ctr[3]) raise_device_error(ctr[3]);
     const int64_t *r_m = (const int64_t *)(h + o_m), *r_par = (const int64_t *)(h + o_par),
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
