@@ -164,7 +164,7 @@ def c5_config(args, world):
                         "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
                         "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
                 args.routing] if world > 1 else "one rank: every query is local",
-            "pipelined": bool(args.pipeline and world > 1 and args.routing == "fused"),
+            "pipelined": bool(args.pipeline and args.routing == "fused"),
             "l2": "inputs larger than L2 (~%.0f GB arena per rank)" % (107.0 / world)}
 
 
@@ -727,7 +727,7 @@ def measure_c5(args, steps, warmup):
     router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
     wl.fill_queries(router)
     routers = [router]
-    if args.pipeline and world > 1 and args.routing == "fused":
+    if args.pipeline and args.routing == "fused":
         # a second region: the next batch is bucketed + packed while this one is matched
         routers.append(Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()),
                               g2l=wl.g2l))

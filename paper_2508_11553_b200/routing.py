@@ -259,12 +259,24 @@ def match_pipelined(routers, n: int, batches: int, side_stream=None):
         routers[b].prepare(n, stream=side)
         prepared[b].record(side)
 
+    # one rank (no cross-rank barriers): consecutive walks also alternate between two
+    # streams, so batch i+1's walk fills the SMs batch i's tail leaves idle
+    walks = [main]
+    if routers[0].nranks == 1 and k > 1:
+        if not hasattr(routers[0], "_walk_stream"):
+            routers[0]._walk_stream = torch.cuda.Stream(routers[0].store.device)
+        walks = [main, routers[0]._walk_stream]
+        walks[1].wait_stream(main)
     prep(0)
     for i in range(batches):
         b = i % k
-        main.wait_event(prepared[b])
-        routers[b].match_prepared("device")
+        ws = walks[i % len(walks)]
+        ws.wait_event(prepared[b])
+        with torch.cuda.stream(ws):
+            routers[b].match_prepared("device")
         done[b] = torch.cuda.Event()
-        done[b].record(main)
+        done[b].record(ws)
         if i + 1 < batches:
             prep(i + 1)
+    for ws in walks[1:]:
+        main.wait_stream(ws)
