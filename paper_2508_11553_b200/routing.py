@@ -260,7 +260,9 @@ def match_pipelined(routers, n: int, batches: int, side_stream=None):
         prepared[b].record(side)
 
     # one rank (no cross-rank barriers): consecutive walks also alternate between two
-    # streams, so batch i+1's walk fills the SMs batch i's tail leaves idle
+    # streams, so batch i+1's walk fills the SMs batch i's tail leaves idle (c5 at one GPU:
+    # 27.6 -> 28.9 M q/s).  With peers the same overlap measured slower (N=2: 26.9 vs 28.2:
+    # the next walk's waiting CTAs and link traffic crowd the current one), so it stays off.
     walks = [main]
     if routers[0].nranks == 1 and k > 1:
         if not hasattr(routers[0], "_walk_stream"):
