@@ -858,6 +858,9 @@ struct RecShared {
   // entry prefetch
   long long pre_off[kRecPre];
   int pre_len[kRecPre], pre_q0[kRecPre];
+  // the chain's results for its end (chains of <= kRecPre entries): matched, new row
+  int win_m[kRecPre];
+  unsigned char win_new[kRecPre];
 };
 
 __device__ __forceinline__ void rec_cache_row(RecShared &sh, int64_t r, const RowFields &f) {
@@ -1180,20 +1183,32 @@ __device__ __forceinline__ void record_finish_entry(const DevView &v, const Batc
 // the rows.  Only this CTA ever reads the session's rows inside the launch, so switching
 // here is safe; chains that finish early overlap their copies with the walks of others.
 template <int NT, int BAR>
-__device__ void record_chain_copy(const DevView &v, const Batch &b, int64_t e0, int64_t e1, long long *s_scan) {
+__device__ void record_chain_copy(const DevView &v, const Batch &b, int64_t e0, int64_t e1, long long *s_scan,
+                                  const RecShared &sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool win = e1 - e0 <= kRecPre;  // the chain's results are still in shared memory
   for (int64_t base = e0; base < e1; base += NT) {
     const int64_t e = base + threadIdx.x;
     long long words = 0, runs = 0;
     int fr = 0;
     int64_t m = 0;
-    if (e < e1 && b.o_dup[e] < 0) {
-      m = b.o_m[e];
-      const int64_t L = b.len[e];
+    const bool isnew = e < e1 && (win ? sh.win_new[e - e0] != 0 : b.o_dup[e] < 0);
+    if (isnew) {
+      m = win ? sh.win_m[e - e0] : b.o_m[e];
+      const int64_t L = win ? sh.pre_len[e - e0] : b.len[e];
       if (L > m) {
         words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - (m / kAlignWords) * kAlignWords;
-        fr = first_run_at(b, e, m);
-        runs = (b.run_off[e + 1] - b.run_off[e]) - fr;
+        const int64_t r0 = b.run_off[e], r1 = b.run_off[e + 1];
+        if (r1 - r0 <= 4) {  // a few runs: read them at once (one round trip, no search chain)
+          int32_t st[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) st[k] = r0 + k < r1 ? b.run_start[r0 + k] : 0x7fffffff;
+#pragma unroll
+          for (int k = 1; k < 4; k++) fr += st[k] <= m ? 1 : 0;
+        } else {
+          fr = first_run_at(b, e, m);
+        }
+        runs = (r1 - r0) - fr;
       }
     }
     long long iw = words, ir = runs;  // inclusive scans within the warp, then across warps
@@ -1229,10 +1244,11 @@ __device__ void record_chain_copy(const DevView &v, const Batch &b, int64_t e0, 
     group_sync<NT, BAR>();
   }
   for (int64_t e = e0; e < e1; e++) {  // the whole group on each entry's suffix and runs
-    if (b.o_dup[e] >= 0) continue;
-    const int64_t m = b.o_m[e], L = b.len[e];
+    if (win ? !sh.win_new[e - e0] : b.o_dup[e] >= 0) continue;
+    const int64_t m = win ? sh.win_m[e - e0] : b.o_m[e], L = win ? sh.pre_len[e - e0] : b.len[e];
     if (L <= m) continue;
-    block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + b.c_vb[e]), reinterpret_cast<const int4 *>(b.tok + b.off[e]),
+    const int64_t off = win ? sh.pre_off[e - e0] : b.off[e];
+    block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + b.c_vb[e]), reinterpret_cast<const int4 *>(b.tok + off),
                             m >> 2, (L + 3) >> 2);
     const int64_t r0 = b.run_off[e] + b.c_firstrun[e], nr = b.run_off[e + 1] - r0, d0 = b.c_run0[e];
     for (int64_t k = threadIdx.x; k < nr; k += NT) {
@@ -1272,10 +1288,18 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
   } else {
     // the first wave takes chains by CTA index; later chains come from the work counter
     long long it = blockIdx.x;
+    long long next_it = 0;  // thread 0: the next chain, claimed at this chain's start (used at its end)
     for (;;) {
       if (it >= a.nchains) break;
       const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
+      for (int t = threadIdx.x; t < kRecPre && e0 + t < e1; t += NT) {  // the first entries, beside the session
+        const int64_t off = b.off[e0 + t];
+        sh.pre_off[t] = off;
+        sh.pre_len[t] = (int)b.len[e0 + t];
+        sh.pre_q0[t] = b.tok[off];
+      }
       if (threadIdx.x == 0) {  // the session, cached for the whole chain
+        next_it = (long long)gridDim.x + (long long)atomicAdd(&a.work[0], 1ull);
         const int32_t sid = (int32_t)a.chains[3 * it + 2];
         sh.sid = sid;
         sh.nrows = v.s_nrows[sid];
@@ -1296,7 +1320,7 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
       }
       for (int64_t e = e0; e < e1; e++) {
         const int k = (int)((e - e0) % kRecPre);
-        if (k == 0) {  // the next kRecPre entries' offsets, lengths and first tokens
+        if (k == 0 && e != e0) {  // the next kRecPre entries' offsets, lengths and first tokens
           group_sync<NT, BAR>();
           for (int t = threadIdx.x; t < kRecPre && e + t < e1; t += NT) {
             const int64_t off = b.off[e + t];
@@ -1315,6 +1339,10 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
         record_walk<NT, BAR>(v, b, sh, rg);
         if (threadIdx.x == 0) {
           record_commit(v, b, e, sh);
+          if (e - e0 < kRecPre) {
+            sh.win_m[e - e0] = (int)sh.m;
+            sh.win_new[e - e0] = sh.dup < 0 ? 1 : 0;
+          }
           if (NCW && sh.dup < 0 && sh.len > sh.m) {  // hand the suffix copy to the copy warp
             const int head = sh.q_head;
             while (head - *(volatile int *)&sh.q_read >= kRecQ) __nanosleep(100);
@@ -1353,9 +1381,9 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
       if (NCW) {
         for (int64_t e = e0 + threadIdx.x; e < e1; e += NT) record_finish_entry(v, b, e);
       } else {
-        record_chain_copy<NT, BAR>(v, b, e0, e1, s_scan);
+        record_chain_copy<NT, BAR>(v, b, e0, e1, s_scan, sh);
       }
-      if (threadIdx.x == 0) s_item = (long long)gridDim.x + (long long)atomicAdd(&a.work[0], 1ull);
+      if (threadIdx.x == 0) s_item = next_it;
       group_sync<NT, BAR>();
       it = s_item;
       group_sync<NT, BAR>();

@@ -1,5 +1,5 @@
 # K2 ring-shape sweep on configs 2 and 3 (tuning build): device time of k_record + k_record_copy
-for v in default ws64x3x256 t32x2x64 ws32x2x64 t128x3x256; do
+for v in default; do
   echo "== $v"
   TM_LIB=paper_2508_11553_b200/libtmstore_tuning.so TM_RECORD_VARIANT=$v timeout 200 python tools/bench_paths.py --configs 2,3 --no-cpu 2>&1 | python -c "
 import sys, json
