@@ -1554,6 +1554,7 @@ __global__ void k_export_plan(DevView v, ExportArgs e) {
     const int64_t t0 = e.tile_off[i], t1 = e.tile_off[i + 1];
     const int64_t row = e.rows[i];
     const int64_t len = v.row_len[row], o = e.out_off[i];
+    if (lane == 0 && e.resp) e.resp[i] = 0;  // the export kernel atomicMax-es into it (stream order)
     for (int64_t t = t0 + lane; t < t1; t += 32) plan_tile(v, e, t, i, row, len, o, (t - t0) * kExportTile);
   }
 }

@@ -130,6 +130,22 @@ struct Layout {
   }
 };
 
+// A session's rows in insertion order.  Most sessions hold one or two rows: those stay
+// inline (no heap allocation per new session - it dominated the host side of large
+// record calls of fresh sessions).
+struct RowList {
+  int64_t n = 0;
+  int64_t inl[2] = {0, 0};
+  std::vector<int64_t> more;
+  int64_t size() const { return n; }
+  int64_t operator[](int64_t k) const { return k < 2 ? inl[k] : more[k - 2]; }
+  void push_back(int64_t r) {
+    if (n < 2) inl[n] = r;
+    else more.push_back(r);
+    n++;
+  }
+};
+
 struct RowHost {
   int32_t sid, local;
   int64_t parent;
@@ -160,7 +176,7 @@ struct tm_store {
   std::vector<int32_t> chain_slot;
   uint64_t batch_stamp = 0;
   std::vector<RowHost> rows;
-  std::vector<std::vector<int64_t>> sess_rows;
+  std::vector<RowList> sess_rows;
   std::vector<int64_t> sess_stored, sess_naive;
   std::vector<int32_t> sess_maxdepth;  // deepest row per session (-1: none); sizes path-copy reservations
   int64_t max_depth = 0;
@@ -894,6 +910,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       if (s->sess_maxdepth[sid] + chain_len[c] >= tms::kPathCopyDepth) words_upper += round_up(2 * L, tms::kAlignWords);
     }
     const int64_t nchains = (int64_t)chain_tokens.size();
+    tr.mark("validate+chains");
     std::vector<int64_t> chain_beg(nchains + 1, 0);
     for (int64_t c = 0; c < nchains; c++) chain_beg[c + 1] = chain_beg[c] + chain_len[c];
     std::vector<int64_t> perm(n);  // position in chain order -> batch index
@@ -903,7 +920,10 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     }
     std::vector<int64_t> order(nchains);
     for (int64_t c = 0; c < nchains; c++) order[c] = c;
-    std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return chain_tokens[x] > chain_tokens[y]; });
+    bool ordered = true;  // already longest-first (e.g. equal chains): no sort
+    for (int64_t c = 1; c < nchains && ordered; c++) ordered = chain_tokens[c - 1] >= chain_tokens[c];
+    if (!ordered)
+      std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return chain_tokens[x] > chain_tokens[y]; });
     // ---- capacity (upper bounds); every entry reserves a row id (batch order): holes left by
     // earlier re-recorded sequences first, then fresh ids
     const int64_t row_base = (int64_t)s->rows.size();
@@ -978,21 +998,30 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     int64_t *h_crow = (int64_t *)(h + o_crow);
     int32_t *h_rs = (int32_t *)(h + o_rs), *h_rv = (int32_t *)(h + o_rv);
     uint8_t *h_ro = (uint8_t *)(h + o_ro);
-    int64_t rr = 0;
-    for (int64_t k = 0; k < n; k++) {
-      int64_t e = perm[k];
-      h_sid[k] = sids[e];
-      h_off[k] = doff[k];
-      h_len[k] = tok_len[e];
-      h_roff[k] = rr;
-      h_crow[k] = reserved[e];  // reserved id (batch order)
-      int64_t r0 = run_off[e], r1 = run_off[e + 1];
-      memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
-      memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
-      memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
-      rr += r1 - r0;
+    // per-entry staging in chain order; the run offsets first (a prefix sum), then the
+    // entries - spread over the host pool for large batches
+    h_roff[0] = 0;
+    for (int64_t k = 0; k < n; k++) h_roff[k + 1] = h_roff[k] + (run_off[perm[k] + 1] - run_off[perm[k]]);
+    auto stage_range = [&](int64_t k0, int64_t k1) {
+      for (int64_t k = k0; k < k1; k++) {
+        const int64_t e = perm[k], rr = h_roff[k];
+        h_sid[k] = sids[e];
+        h_off[k] = doff[k];
+        h_len[k] = tok_len[e];
+        h_crow[k] = reserved[e];  // reserved id (batch order)
+        const int64_t r0 = run_off[e], r1 = run_off[e + 1];
+        memcpy(h_rs + rr, run_start + r0, 4 * (r1 - r0));
+        memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
+        memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
+      }
+    };
+    constexpr int64_t kStageChunk = 2048;
+    if (n >= 4 * kStageChunk) {
+      tms::parallel_for((n + kStageChunk - 1) / kStageChunk,
+                        [&](int64_t c) { stage_range(c * kStageChunk, std::min(n, (c + 1) * kStageChunk)); });
+    } else {
+      stage_range(0, n);
     }
-    h_roff[n] = rr;
     memset(h + o_work, 0, 16);  // the launch's chain counter and CTAs-done counter start at zero
     {  // chains in processing order: first entry, end, session
       int64_t *hc = (int64_t *)(h + o_chains);
@@ -1054,35 +1083,53 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
     const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
                   *r_loc = (const int32_t *)(h + o_cloc);
-    std::vector<int64_t> pos(n);  // batch index -> chain position
-    for (int64_t k = 0; k < n; k++) pos[perm[k]] = k;
     s->rows.resize(row_base + n_fresh, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
-    for (int64_t e = 0; e < n; e++) {  // batch order: local ordinals are assigned in it
-      const int64_t k = pos[e];
-      const int32_t sid = sids[e];
-      const int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
-      if (r_dup[k] < 0) {
-        if (row != reserved[e]) fail(TM_ECUDA, "row numbering out of sync");
-        RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
-        rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
-        s->max_depth = std::max<int64_t>(s->max_depth, rh.depth);
-        s->sess_maxdepth[sid] = std::max(s->sess_maxdepth[sid], rh.depth);
-        s->rows[row] = rh;
-        if (r_loc[k] != (int32_t)s->sess_rows[sid].size()) fail(TM_ECUDA, "session ordinal out of sync");
-        s->sess_rows[sid].push_back(row);
-        s->sess_stored[sid] += L - m;
-        s->n_real_rows++;
-      } else {
-        s->free_rows.push_back(reserved[e]);  // the reserved slot stayed empty: reuse it
+    // The host mirror, chain by chain (a chain is one session's entries in batch order).
+    struct MirrorAcc {
+      int64_t real = 0, maxd = 0;
+      std::vector<int64_t> holes;
+      bool bad_row = false, bad_ord = false;
+    };
+    auto mirror_chain = [&](int64_t c, MirrorAcc &acc) {
+      for (int64_t k = chain_beg[c]; k < chain_beg[c + 1]; k++) {
+        const int64_t e = perm[k];
+        const int32_t sid = sids[e];
+        const int64_t L = tok_len[e], m = r_m[k], row = r_row[k], par = r_par[k];
+        if (r_dup[k] < 0) {
+          if (row != reserved[e]) acc.bad_row = true;
+          RowHost rh{sid, r_loc[k], par, (int32_t)m, (int32_t)L, 0, r_tn[k], r_sp[k]};
+          rh.depth = par >= 0 ? s->rows[par].depth + 1 : 0;
+          acc.maxd = std::max<int64_t>(acc.maxd, rh.depth);
+          s->sess_maxdepth[sid] = std::max(s->sess_maxdepth[sid], rh.depth);
+          s->rows[row] = rh;
+          if (r_loc[k] != (int32_t)s->sess_rows[sid].size()) acc.bad_ord = true;
+          s->sess_rows[sid].push_back(row);
+          s->sess_stored[sid] += L - m;
+          acc.real++;
+        } else {
+          acc.holes.push_back(reserved[e]);  // the reserved slot stayed empty: reuse it
+        }
+        s->sess_naive[sid] += L;
+        if (out_matched) out_matched[e] = m;
+        if (out_row) out_row[e] = row;
+        if (out_local) out_local[e] = r_loc[k];
+        if (out_parent) out_parent[e] = par;
+        if (out_parent_local) out_parent_local[e] = par >= 0 ? s->rows[par].local : -1;
+        if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
       }
-      s->sess_naive[sid] += L;
-      if (out_matched) out_matched[e] = m;
-      if (out_row) out_row[e] = row;
-      if (out_local) out_local[e] = r_loc[k];
-      if (out_parent) out_parent[e] = par;
-      if (out_parent_local) out_parent_local[e] = par >= 0 ? s->rows[par].local : -1;
-      if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
+    };
+    // (a parallel version over host threads measured slower: the per-entry work is a few
+    // cache lines of session state, less than a pool dispatch)
+    std::vector<MirrorAcc> accs(1);
+    for (int64_t c = 0; c < nchains; c++) mirror_chain(c, accs[0]);
+    for (const MirrorAcc &acc : accs) {
+      if (acc.bad_row) fail(TM_ECUDA, "row numbering out of sync");
+      if (acc.bad_ord) fail(TM_ECUDA, "session ordinal out of sync");
+      s->n_real_rows += acc.real;
+      s->max_depth = std::max<int64_t>(s->max_depth, acc.maxd);
+      s->free_rows.insert(s->free_rows.end(), acc.holes.begin(), acc.holes.end());
     }
+    tr.mark("mirror");
     s->arena_used = ctr[0];
     s->n_runs = ctr[2];
     s->c_record_calls++;
@@ -1264,7 +1311,7 @@ int tm_export_rows(tm_store *s, int64_t n, const int64_t *rows, int32_t mem_out,
       e.versions = out_versions;
       e.resp = out_resp_start;
     }
-    if (e.resp) ck(cudaMemsetAsync(e.resp, 0, 8 * n, st), "memset resp");
+    // e.resp is zeroed by the export planner (no memset call)
     {
       ProfScope ps(s, 2, st);
       ck(tms::launch_export(s->v, e, s->num_sms, st), "export");
@@ -1713,7 +1760,7 @@ int tm_store_save(tm_store *s, const char *path) {
       for (int64_t i = 0; i < s->n_sess; i++) {
         const int64_t k = (int64_t)s->sess_rows[i].size();
         w.val(s->sess_stored[i]); w.val(s->sess_naive[i]); w.val(k);
-        w.put(s->sess_rows[i].data(), 8 * k);
+        for (int64_t j = 0; j < k; j++) w.val(s->sess_rows[i][j]);
       }
       save_dev(s, w, s->v.arena, s->arena_used);
       save_dev(s, w, s->v.row_vb, nrows); save_dev(s, w, s->v.row_m, nrows); save_dev(s, w, s->v.row_len, nrows);
@@ -1772,8 +1819,7 @@ int tm_store_load(tm_store *s, const char *path) {
         s->sess_stored[i] = r.val<int64_t>();
         s->sess_naive[i] = r.val<int64_t>();
         const int64_t k = r.val<int64_t>();
-        s->sess_rows[i].resize(k);
-        r.get(s->sess_rows[i].data(), 8 * k);
+        for (int64_t j = 0; j < k; j++) s->sess_rows[i].push_back(r.val<int64_t>());
       }
       load_dev(s, r, s->v.arena, aused);
       load_dev(s, r, s->v.row_vb, nrows); load_dev(s, r, s->v.row_m, nrows); load_dev(s, r, s->v.row_len, nrows);
