@@ -67,8 +67,9 @@ def parse():
     ap.add_argument("--pipeline", action=argparse.BooleanOptionalAction, default=True,
                     help="c5, N>1, fused routing: two routing regions, batch k+1 bucketed + packed while batch k "
                          "is matched (--no-pipeline: one region, batches back to back)")
-    ap.add_argument("--routing", default="fused", choices=["fused", "fused-nccl-barrier", "nccl"],
-                    help="c5 exchange: fused P2P K1 (product) or NCCL all-to-all + local match (baseline)")
+    ap.add_argument("--routing", default="fused", choices=["fused", "push", "fused-nccl-barrier", "nccl"],
+                    help="c5 exchange: fused P2P K1 (owners pull the planes), push (requesters write the planes "
+                         "into the owners' inboxes) or NCCL all-to-all + local match (baseline)")
     ap.add_argument("--mixed", default=None,
                     help="lo,hi: log-uniform history lengths (config-5 shard) instead of fixed --hist")
     a = ap.parse_args()
@@ -161,10 +162,13 @@ def c5_config(args, world):
             "batch_queries_per_rank": args.queries, "owner": "splitmix64(gsid) mod N", "n_ranks": world,
             "routing": {"fused": "fused P2P K1: owners read requester HBM over NVLink, write results back; "
                                  "device-side epoch-flag barriers (no collective call per batch)",
+                        "push": "push P2P: requesters pack remote queries' 18-bit planes straight into the owners' "
+                                "inboxes (P2P stores, beside the previous batch's walk); owners walk from local HBM "
+                                "and write results back; device-side epoch-flag barriers",
                         "fused-nccl-barrier": "fused P2P K1 bracketed by two one-element NCCL all-reduces",
                         "nccl": "BASELINE: NCCL all-to-all of query tokens, local K1, all-to-all of results"}[
                 args.routing] if world > 1 else "one rank: every query is local",
-            "pipelined": bool(args.pipeline and args.routing == "fused"),
+            "pipelined": bool(args.pipeline and args.routing in ("fused", "push")),
             "l2": "inputs larger than L2 (~%.0f GB arena per rank)" % (107.0 / world)}
 
 
@@ -706,7 +710,7 @@ def measure_c5(args, steps, warmup):
     own_pg = False
     if not dist.is_initialized():
         own_pg = True
-        if world == 1:
+        if world == 1 and "MASTER_ADDR" not in os.environ:  # plain `python bench.py` (under torchrun: env://)
             dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1, device_id=dev)
         else:
             dist.init_process_group("nccl", device_id=dev)
@@ -724,13 +728,15 @@ def measure_c5(args, steps, warmup):
     log(f"rank {rank}: c5 shard ({len(wl.owned)} sessions, {owned_tokens * 4 / 1e9:.1f} GB) built in {build_s:.1f} s")
     tok_need = torch.tensor([int(wl.q_off[-1])], device=dev)
     dist.all_reduce(tok_need, op=dist.ReduceOp.MAX)
-    router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l)
+    push = args.routing == "push"
+    router = Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()), g2l=wl.g2l,
+                    push=push)
     wl.fill_queries(router)
     routers = [router]
-    if args.pipeline and args.routing == "fused":
+    if args.pipeline and args.routing in ("fused", "push"):
         # a second region: the next batch is bucketed + packed while this one is matched
         routers.append(Router(store, dist.group.WORLD, n_max=args.queries, tokens_max=int(tok_need.item()),
-                              g2l=wl.g2l))
+                              g2l=wl.g2l, push=push))
         wl.fill_queries(routers[1])
     torch.cuda.synchronize()
     if len(routers) > 1:
@@ -739,7 +745,8 @@ def measure_c5(args, steps, warmup):
         side = torch.cuda.Stream(dev)
         run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side)  # noqa: E731
     else:
-        route = {"fused": router.match, "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
+        route = {"fused": router.match, "push": router.match,
+                 "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),
                  "nccl": router.match_nccl}[args.routing]
 
         def run_batches(k):
@@ -790,10 +797,13 @@ def measure_c5(args, steps, warmup):
     L = wl.lens[wl.q_g]
     cq = np.minimum(np.minimum(wl.q_depth + 1, wl.q_len), L)
     remote = wl.owner[wl.q_g] != rank
-    stats = torch.tensor([float(cq.sum()), float(cq[remote].sum()), float(remote.mean())], device=dev,
+    pushed = float(((wl.q_len[remote] + 31) // 32 * 32).sum())  # push: whole queries cross, not compared prefixes
+    stats = torch.tensor([float(cq.sum()), float(cq[remote].sum()), float(remote.mean()), pushed], device=dev,
                          dtype=torch.float64)
     dist.all_reduce(stats)
     toks, remote_toks, xfrac = float(stats[0]), float(stats[1]), float(stats[2]) / world
+    if push and world > 1:
+        remote_toks = float(stats[3])
     value = world * wl.n_queries * steps / elapsed
     wire_b = 2.25 if (world > 1 and args.routing != "nccl" and os.environ.get("TM_ROUTE_PACK", "1") != "0") else 4.0
     peak, peak_kind = peaks()
@@ -827,7 +837,7 @@ def measure_c5(args, steps, warmup):
                              "peer reads 780 GB/s one direction, 670 GB/s per GPU both directions at once)"},
         # ours per batch: k_route + k_walk_routed (+ k_route_pack with peers, + k_route_arrive +
         # k_route_wait_done with device barriers)
-        "gpu_launches": steps * ((4 if args.routing == "fused" else 2) + (1 if world > 1 and
+        "gpu_launches": steps * ((4 if args.routing in ("fused", "push") else 2) + (1 if world > 1 and
                                                                         args.routing != "nccl" else 0)),
         "clocks": clk.summary(),
         "timing": "CUDA events on the launching stream around K routed batches; max over ranks",

@@ -225,6 +225,20 @@ int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *
 int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
                          const int32_t *g2l, int64_t g2l_len, int64_t epoch, void *stream);
 
+/* Push routing: the same exchange with the plane traffic turned around.  Each region
+ * also holds an inbox of nranks slices at `inbox_stride` bytes apart (slice p = the
+ * lo / hi / rec arrays of source rank p at offsets[8], [9], [11] + p * inbox_stride);
+ * tm_route_prepare_push packs every remote query's planes and record straight into its
+ * owner's inbox slice for this rank (P2P stores over NVLink, overlapping the previous
+ * batch's walk when pipelined), and tm_match_routed_push (device barriers as in
+ * tm_match_routed_sync) has each owner read them from its own HBM.  A region's inbox
+ * may be rewritten once every owner has finished the batch that last used it (the
+ * done wait of that batch).  Same results as tm_match_routed_sync. */
+int tm_route_prepare_push(tm_store *store, void *region, int64_t n, const int64_t *offsets, int32_t nranks,
+                          int32_t rank, void *const *peer_regions, int64_t inbox_stride, void *stream);
+int tm_match_routed_push(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
+                         const int32_t *g2l, int64_t g2l_len, int64_t epoch, int64_t inbox_stride, void *stream);
+
 /* Snapshot / restore (the reference store is in-memory only, trajectory.py:128): write
  * the arena, row table, metadata runs, session counters and the host row mirror to a
  * file; load them into an EMPTY store (any GPU), rebuilding the branch index. */

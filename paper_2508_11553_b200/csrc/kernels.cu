@@ -337,7 +337,7 @@ constexpr int kPackBlock = 4096;  // positions per k_route_pack work item
 // every pass issues all of a thread's loads of a chunk before using any of them: the
 // whole kernel is a handful of dependent global round trips for a 4096-query batch.
 constexpr int kRouteU = 4;  // queries per thread per chunk
-__global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head) {
+__global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head, PushArgs pa) {
   RouteDesc *d = reinterpret_cast<RouteDesc *>(region);
   if (threadIdx.x == 0) *reinterpret_cast<RouteHead *>(region) = head;
   const int nranks = head.nranks;
@@ -411,9 +411,15 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head
   const bool pk = head.lo_off != 0;
   int32_t *pkf = reinterpret_cast<int32_t *>(region + head.pkf_off);
   const int own0 = s_own0, nown = s_nown;
+  const int64_t *qoff = reinterpret_cast<const int64_t *>(region + head.qoff_off);
   for (int64_t c0 = 0; c0 < n; c0 += CH) {
     int key[kRouteU];
-    int64_t L[kRouteU], g[kRouteU];
+    int64_t L[kRouteU], g[kRouteU], qo[kRouteU];
+#pragma unroll
+    for (int u = 0; u < kRouteU; u++) {  // in flight with the keys
+      const int64_t i = c0 + u * kRouteNT + threadIdx.x;
+      qo[u] = (head.rec_off && i < n) ? qoff[i] : 0;
+    }
     load_keys(c0, key, L, g);
 #pragma unroll
     for (int u = 0; u < kRouteU; u++) {
@@ -421,10 +427,16 @@ __global__ void __launch_bounds__(kRouteNT) k_route(char *region, RouteHead head
       if (i >= n) continue;
       const int pos = atomicAdd(&cnt[key[u]], 1);
       idx[pos] = (int32_t)i;
+      if (head.rec_off && key[u] / kPlanNB == head.rank) {  // own query: its record for the walk
+        char *rb = pa.stride ? region + pa.stride * head.rank : region;
+        reinterpret_cast<RouteRec *>(rb + head.rec_off)[pos] = RouteRec{g[u], qo[u], (int32_t)L[u], (int32_t)i, 0, 0};
+      }
       if (pk && key[u] / kPlanNB != head.rank) {
         pkf[pos < own0 ? pos : pos - nown] = (int)((L[u] + kPackBlock - 1) / kPackBlock);
-        if (L[u] == 0 && head.rec_off)  // no block to pack: its record is written here
-          reinterpret_cast<RouteRec *>(region + head.rec_off)[pos] = RouteRec{g[u], 0, 0, (int32_t)i, 0, 0};
+        if (L[u] == 0 && head.rec_off) {  // no block to pack: its record is written here
+          char *rb = pa.stride ? pa.peer[key[u] / kPlanNB] + pa.stride * head.rank : region;
+          reinterpret_cast<RouteRec *>(rb + head.rec_off)[pos] = RouteRec{g[u], 0, 0, (int32_t)i, 0, 0};
+        }
       }
     }
   }
@@ -531,10 +543,8 @@ __global__ void k_route_wait_done(DevView v, RoutedArgs a) {
 constexpr int kPackNT = 256;
 struct PackView {
   const int64_t *qoff, *qlen, *gsid;
-  RouteRec *rec;  // or nullptr
   const int32_t *tok, *idx, *pkf;
-  uint16_t *plo;
-  uint8_t *phi;
+  int64_t lo_off, hi_off, rec_off;  // planes / records at these offsets of the destination region
   int own0, nown;
   int64_t nrem, nblk;
 };
@@ -546,25 +556,30 @@ __device__ __forceinline__ PackView pack_view(char *region) {
   w.tok = reinterpret_cast<const int32_t *>(region + d->tok_off);
   w.idx = reinterpret_cast<const int32_t *>(region + d->idx_off);
   w.gsid = reinterpret_cast<const int64_t *>(region + d->sid_off);
-  w.rec = d->rec_off ? reinterpret_cast<RouteRec *>(region + d->rec_off) : nullptr;
   w.pkf = reinterpret_cast<const int32_t *>(region + d->pkf_off);
-  w.plo = reinterpret_cast<uint16_t *>(region + d->lo_off);
-  w.phi = reinterpret_cast<uint8_t *>(region + d->hi_off);
+  w.lo_off = d->lo_off;
+  w.hi_off = d->hi_off;
+  w.rec_off = d->rec_off;
   w.own0 = d->start[d->rank];
   w.nown = d->count[d->rank];
   w.nrem = d->n - w.nown;
   w.nblk = w.pkf[w.nrem];
   return w;
 }
-// block blk of remote query j (pkf[j] <= blk < pkf[j + 1]); bj = pkf[j]
+// block blk of remote query j (pkf[j] <= blk < pkf[j + 1]); bj = pkf[j].  The planes and
+// the record go to the region at db: this rank's own (owners pull), or with push routing
+// the owner's inbox slice for this rank (P2P stores over NVLink).
 template <int NT>
-__device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int64_t bj, int64_t blk) {
+__device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int64_t bj, int64_t blk, char *db) {
   constexpr int SL = kPackBlock / (8 * NT);  // 8-position slots per thread
   const int64_t pos = j < w.own0 ? j : j + w.nown;
   const int64_t q = w.idx[pos];
+  uint16_t *plo = reinterpret_cast<uint16_t *>(db + w.lo_off);
+  uint8_t *phi = reinterpret_cast<uint8_t *>(db + w.hi_off);
+  RouteRec *rec = w.rec_off ? reinterpret_cast<RouteRec *>(db + w.rec_off) : nullptr;
   const int64_t off = w.qoff[q], len = w.qlen[q];
   const int64_t r0 = (blk - bj) * kPackBlock;
-  const int64_t g = (w.rec && blk == bj && threadIdx.x == 0) ? w.gsid[q] : 0;  // in flight with the tokens
+  const int64_t g = (rec && blk == bj && threadIdx.x == 0) ? w.gsid[q] : 0;  // in flight with the tokens
   const int k = threadIdx.x & 3;  // this thread's 8 positions within the 32-position group
   int4 a[SL], b[SL];
 #pragma unroll
@@ -581,8 +596,8 @@ __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int
       b[u] = make_int4(t[4], t[5], t[6], t[7]);
     }
   }
-  if (w.rec && blk == bj && threadIdx.x == 0)  // the query's first block: its record
-    w.rec[pos] = RouteRec{g, off, (int32_t)len, (int32_t)q, a[0].x, 0};
+  if (rec && blk == bj && threadIdx.x == 0)  // the query's first block: its record
+    rec[pos] = RouteRec{g, off, (int32_t)len, (int32_t)q, a[0].x, 1};
   unsigned bad = 0;
 #pragma unroll
   for (int u = 0; u < SL; u++) {
@@ -594,7 +609,7 @@ __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int
     lo4.y = ((uint32_t)t[2] & 0xFFFFu) | ((uint32_t)t[3] << 16);
     lo4.z = ((uint32_t)t[4] & 0xFFFFu) | ((uint32_t)t[5] << 16);
     lo4.w = ((uint32_t)t[6] & 0xFFFFu) | ((uint32_t)t[7] << 16);
-    *reinterpret_cast<uint4 *>(w.plo + p) = lo4;
+    *reinterpret_cast<uint4 *>(plo + p) = lo4;
     unsigned long long h = 0;
 #pragma unroll
     for (int e = 0; e < 8; e++) {
@@ -604,14 +619,14 @@ __device__ __forceinline__ unsigned pack_block(const PackView &w, int64_t j, int
     const unsigned quad = __activemask();  // whole 32-position groups are active together
     h |= __shfl_xor_sync(quad, h, 1);
     h |= __shfl_xor_sync(quad, h, 2);
-    if (k == 0) *reinterpret_cast<unsigned long long *>(w.phi + (p >> 5) * 8) = h;
+    if (k == 0) *reinterpret_cast<unsigned long long *>(phi + (p >> 5) * 8) = h;
   }
   return bad;
 }
 
 // tm_route_prepare with peers: every CTA packs one contiguous range of blocks (one
 // binary search for its first query, then it steps through the queries in order)
-__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
+__global__ void __launch_bounds__(kPackNT) k_route_pack(char *region, PushArgs pa) {
   const PackView w = pack_view(region);
   const int64_t per = (w.nblk + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = min(w.nblk, b0 + per);
@@ -621,13 +636,27 @@ __global__ void __launch_bounds__(kPackNT) k_route_pack(char *region) {
     const int64_t mid = (lo + hi) >> 1;
     if (w.pkf[mid] <= b0) lo = mid; else hi = mid;
   }
+  const RouteDesc *d = reinterpret_cast<const RouteDesc *>(region);
+  // destination of query j: its owner's inbox slice (push) or this region
+  auto dest = [&](int64_t j) -> char * {
+    if (!pa.stride) return region;
+    const int64_t pos = j < w.own0 ? j : j + w.nown;
+    int o = 0;
+    while (o + 1 < d->nranks && pos >= d->start[o + 1]) o++;
+    return pa.peer[o] + pa.stride * d->rank;
+  };
   int64_t j = lo, bj = w.pkf[j], bn = w.pkf[j + 1];
+  char *db = dest(j);
   unsigned bad = 0;
   for (int64_t blk = b0; blk < b1; blk++) {
-    while (blk >= bn) { j++; bj = bn; bn = w.pkf[j + 1]; }
-    bad |= pack_block<kPackNT>(w, j, bj, blk);
+    if (blk >= bn) {
+      while (blk >= bn) { j++; bj = bn; bn = w.pkf[j + 1]; }
+      db = dest(j);
+    }
+    bad |= pack_block<kPackNT>(w, j, bj, blk, db);
   }
   if (bad) atomicOr(&reinterpret_cast<RouteDesc *>(region)->pk_bad, 1);
+  if (pa.stride) __threadfence_system();  // P2P stores ordered before the arrive flag
 }
 
 // Owner side.  Two work queues, each longest first: this rank's own queries (HBM only)
@@ -650,6 +679,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
   __shared__ int s_nloc;  // cells in the local queue
   __shared__ RouteRec s_rec;
   __shared__ bool s_has_rec;
+  __shared__ long long s_trace;
   const int np = a.nranks;
   const int ncell = kPlanNB * np;
   // TMA-staged compare for remote queries: bulk copies pull the query's 18-bit planes
@@ -686,46 +716,151 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
   }
   __syncthreads();
   const long long tot[2] = {s_pre[ncell], s_pre[ncell + 1]};
-  int q = (np > 1 && blockIdx.x % np != 0) ? 1 : 0;  // queue this CTA prefers
+  // per-source views (read once per launch, after the arrive barrier: the requesters'
+  // headers and pack flags are final for this batch)
+  struct PeerInfo {
+    const int32_t *tok;
+    int64_t *m, *par, *dup;
+    const uint16_t *plo;
+    const uint8_t *phi;
+    const int4 *rec;  // RouteRec per idx position (nullptr: none)
+    const int32_t *idx;
+    const int64_t *gsid, *qoff, *qlen;
+    int packed;  // remote queries of this source compare through the 18-bit planes
+  };
+  __shared__ PeerInfo s_pi[kMaxRanks];
+  __shared__ int32_t s_sid;
+  if (threadIdx.x < np) {
+    const int p = threadIdx.x;
+    char *reg = const_cast<char *>(a.peer[p]);
+    const RouteDesc *d = reinterpret_cast<const RouteDesc *>(reg);
+    // push routing: planes and records of source p sit in this rank's inbox slice p
+    const char *ib = a.push_stride ? reinterpret_cast<const char *>(own) + a.push_stride * p : reg;
+    const RouteDesc *id = a.push_stride ? own : d;
+    PeerInfo pi;
+    pi.tok = reinterpret_cast<const int32_t *>(reg + d->tok_off);
+    pi.m = reinterpret_cast<int64_t *>(reg + d->m_off);
+    pi.par = reinterpret_cast<int64_t *>(reg + d->par_off);
+    pi.dup = reinterpret_cast<int64_t *>(reg + d->dup_off);
+    pi.plo = reinterpret_cast<const uint16_t *>(ib + id->lo_off);
+    pi.phi = reinterpret_cast<const uint8_t *>(ib + id->hi_off);
+    pi.rec = id->rec_off ? reinterpret_cast<const int4 *>(ib + id->rec_off) : nullptr;
+    pi.idx = reinterpret_cast<const int32_t *>(reg + d->idx_off);
+    pi.gsid = reinterpret_cast<const int64_t *>(reg + d->sid_off);
+    pi.qoff = reinterpret_cast<const int64_t *>(reg + d->qoff_off);
+    pi.qlen = reinterpret_cast<const int64_t *>(reg + d->len_off);
+    pi.packed = PACKED && p != a.rank && d->lo_off && !*reinterpret_cast<const volatile int32_t *>(&d->pk_bad);
+    s_pi[p] = pi;
+  }
+  __syncthreads();
+  // tail CTAs take the shortest remaining items (and prefer the remote queue): each queue
+  // counter holds head claims in its low and tail claims in its high 32 bits, so one
+  // atomic hands out every item exactly once from either end
+  const bool tail = a.tail_every > 0 && blockIdx.x % a.tail_every == (unsigned)a.tail_every - 1;
+  int q = (np > 1 && (tail || blockIdx.x % np != 0)) ? 1 : 0;  // queue this CTA prefers
   bool dry[2] = {false, false};
+  // thread 0: claim the next item; `left` = items still unclaimed in its queue after it
+  auto claim = [&](long long &it, int &cell, long long &left) {
+    it = -1;
+    cell = -1;
+    left = 0;
+    while (it < 0 && !(dry[0] && dry[1])) {
+      const int qq = dry[q] ? 1 - q : q;
+      const unsigned long long old = atomicAdd(qq ? &a.sched->work2 : &a.sched->work, tail ? (1ull << 32) : 1ull);
+      const long long h = (long long)(old & 0xffffffffull), t = (long long)(old >> 32);
+      if (h + t >= tot[qq]) { dry[qq] = true; continue; }
+      const long long x = tail ? tot[qq] - 1 - t : h;
+      int lo = qq ? kPlanNB : 0, hi = qq ? ncell : kPlanNB;  // last cell with prefix <= x
+      while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= x) lo = mid; else hi = mid;
+      }
+      it = x;
+      cell = lo;
+      left = tot[qq] - 1 - h - t;
+    }
+  };
+  // The item's record (one load, over NVLink for a pulled remote query) is requested one
+  // item ahead while the queue still holds more than one item per CTA, so its latency
+  // hides under the current walk (near the end items are claimed only when a CTA is free).
+  // Thread 0's look-ahead state lives in shared memory and the record is copied by
+  // cp.async straight into it: nothing stays live in registers across the walk.
+  __shared__ long long s_nit;
+  __shared__ int s_ncell, s_nready;
+  __shared__ __align__(16) int4 s_nrec[2];
+  auto request = [&]() {  // thread 0, s_nit >= 0
+    const int4 *rp = s_pi[s_peer[s_ncell]].rec;
+    s_nready = rp != nullptr;
+    if (rp) {
+      rp += 2 * (s_bs[s_ncell] + (s_nit - s_pre[s_ncell]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&s_nrec[0])), "l"(rp) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&s_nrec[1])), "l"(rp + 1) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  constexpr long long kClaimLater = -2;
+  constexpr int kLookaheadLen = 8192;
+  if (threadIdx.x == 0) s_nit = kClaimLater;
   for (;;) {
     if (threadIdx.x == 0) {
-      long long it = -1;
-      int cell = -1;
-      while (it < 0 && !(dry[0] && dry[1])) {
-        const int qq = dry[q] ? 1 - q : q;
-        const long long x = (long long)atomicAdd(qq ? &a.sched->work2 : &a.sched->work, 1ull);
-        if (x >= tot[qq]) { dry[qq] = true; continue; }
-        int lo = qq ? kPlanNB : 0, hi = qq ? ncell : kPlanNB;  // last cell with prefix <= x
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if (s_pre[mid] <= x) lo = mid; else hi = mid;
-        }
-        it = x;
-        cell = lo;
+      if (s_nit == kClaimLater) {
+        long long nit, left;
+        int ncell;
+        claim(nit, ncell, left);
+        s_nit = nit;
+        s_ncell = ncell;
+        s_nready = 0;
       }
+      const long long it = s_nit;
+      const int cell = s_ncell;
       s_item = it;
       s_cell = cell;
-      s_has_rec = false;
-      if (it >= 0 && s_peer[cell] != a.rank) {  // a remote query's record: one load over NVLink
-        const RouteDesc *dd = reinterpret_cast<const RouteDesc *>(a.peer[s_peer[cell]]);
-        if (dd->rec_off) {
-          const int4 *rp = reinterpret_cast<const int4 *>(reinterpret_cast<const char *>(dd) + dd->rec_off) +
-                           2 * (s_bs[cell] + (it - s_pre[cell]));
-          const int4 r0 = rp[0], r1 = rp[1];
-          s_rec.gsid = (int64_t)(uint32_t)r0.x | ((int64_t)r0.y << 32);
-          s_rec.off = (int64_t)(uint32_t)r0.z | ((int64_t)r0.w << 32);
-          s_rec.len = r1.x;
-          s_rec.qi = r1.y;
-          s_rec.q0 = r1.z;
-          s_has_rec = true;
+      if (it >= 0) {
+        if (!s_nready) request();
+        const PeerInfo &pi = s_pi[s_peer[cell]];
+        if (pi.rec) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          const int4 n0 = s_nrec[0], n1 = s_nrec[1];
+          s_rec.gsid = (int64_t)(uint32_t)n0.x | ((int64_t)n0.y << 32);
+          s_rec.off = (int64_t)(uint32_t)n0.z | ((int64_t)n0.w << 32);
+          s_rec.len = n1.x;
+          s_rec.qi = n1.y;
+          s_rec.q0 = n1.z;
+          s_rec.has_q0 = n1.w;
+        } else {  // no records (routing without planes): the batch arrays
+          const int32_t qi = pi.idx[s_bs[cell] + (it - s_pre[cell])];
+          s_rec.qi = qi;
+          s_rec.gsid = pi.gsid[qi];
+          s_rec.off = pi.qoff[qi];
+          s_rec.len = (int32_t)pi.qlen[qi];
+          s_rec.q0 = 0;
+          s_rec.has_q0 = 0;
+        }
+        const int64_t g = s_rec.gsid;
+        s_sid = (g >= 0 && g < a.g2l_len) ? a.g2l[g] : -1;
+        // the next item is claimed (and its record requested) now only for a short current
+        // item while the queue is far from empty: claiming ahead of a long item would pair
+        // long items on one CTA and break the longest-first balance
+        s_nit = kClaimLater;
+        if (s_rec.len <= kLookaheadLen) {
+          long long nit, left;
+          int ncell;
+          claim(nit, ncell, left);
+          s_nit = nit;
+          s_ncell = ncell;
+          s_nready = 0;
+          if (nit >= 0 && left > (long long)gridDim.x) request();
         }
       }
     }
     __syncthreads();
     const long long it = s_item;
     const int cell = s_cell;
-    __syncthreads();
+    if (a.trace && threadIdx.x == 0 && it >= 0) {  // diagnostics: item start
+      const long long k = atomicAdd(reinterpret_cast<unsigned long long *>(a.trace), 1ull);
+      s_trace = k < a.trace_cap ? k : -1;
+      if (s_trace >= 0) a.trace[4 + 4 * s_trace] = (long long)globaltimer_ns();
+    }
     if (it < 0) {
       if (sched_exit(a.sched) && a.epoch > 0) {  // last CTA out: results are written, tell every requester
         __threadfence_system();
@@ -735,36 +870,33 @@ __global__ void __launch_bounds__(NT, NT == 64 ? MINB : 1) k_walk_routed(DevView
       return;
     }
     const int p = s_peer[cell];
-    const char *reg = a.peer[p];
-    const RouteDesc *d = reinterpret_cast<const RouteDesc *>(reg);
-    const bool has_rec = s_has_rec;
-    const int32_t qi = has_rec ? s_rec.qi : reinterpret_cast<const int32_t *>(reg + d->idx_off)[s_bs[cell] + (it - s_pre[cell])];
-    const int64_t g = has_rec ? s_rec.gsid : reinterpret_cast<const int64_t *>(reg + d->sid_off)[qi];
-    const int64_t off = has_rec ? s_rec.off : reinterpret_cast<const int64_t *>(reg + d->qoff_off)[qi];
-    const int L = has_rec ? s_rec.len : (int)reinterpret_cast<const int64_t *>(reg + d->len_off)[qi];
-    const int32_t *q0 = has_rec ? &s_rec.q0 : nullptr;
-    char *wreg = const_cast<char *>(reg);
-    WalkOut o{reinterpret_cast<int64_t *>(wreg + d->m_off) + qi, reinterpret_cast<int64_t *>(wreg + d->par_off) + qi,
-              reinterpret_cast<int64_t *>(wreg + d->dup_off) + qi, nullptr, nullptr};
-    const int32_t sid = (g >= 0 && g < a.g2l_len) ? a.g2l[g] : -1;
+    const PeerInfo &pi = s_pi[p];
+    const int32_t qi = s_rec.qi;
+    const int64_t off = s_rec.off;
+    const int L = s_rec.len;
+    const int32_t sid = s_sid;
+    const int32_t *q0p = s_rec.has_q0 ? &s_rec.q0 : nullptr;  // read by thread 0 before s_rec changes
+    WalkOut o{pi.m + qi, pi.par + qi, pi.dup + qi, nullptr, nullptr};
+    __syncthreads();  // s_rec / s_sid are read: thread 0 may overwrite them for the next item
     if (sid < 0) {  // unknown id, or routed to the wrong owner: flag it, never guess
       if (threadIdx.x == 0) { *o.m = -1; *o.parent = -1; *o.dup = -1; }
-      __syncthreads();
       continue;
     }
-    const int32_t *q = reinterpret_cast<const int32_t *>(reg + d->tok_off) + off;
-    bool packed_q = false;
-    if constexpr (PACKED) {
-      if (p != a.rank && d->lo_off && !*reinterpret_cast<const volatile int32_t *>(&d->pk_bad)) {
-        // remote query: packed planes, TMA bulk copies over NVLink
-        const PackedQuery pk{reinterpret_cast<const uint16_t *>(reg + d->lo_off),
-                             reinterpret_cast<const uint8_t *>(reg + d->hi_off), off};
-        walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk, q0);
-        packed_q = true;
-      }
+    const int32_t *q = pi.tok + off;
+    if (PACKED && pi.packed) {
+      // remote query: packed planes, TMA bulk copies over NVLink (or out of this rank's
+      // inbox when the requester pushed them)
+      const PackedQuery pk{pi.plo, pi.phi, off};
+      if constexpr (PACKED) walk_query<NT, U>(v, q, L, sid, nullptr, o, sh, rg, &pk, q0p);
+    } else {  // local (or ids beyond 18 bits): int32, registers
+      walk_query<NT, U, NoRing>(v, q, L, sid, nullptr, o, sh, nullptr, nullptr, q0p);
     }
-    if (!packed_q)  // local (or ids beyond 18 bits): int32, registers
-      walk_query<NT, U, NoRing>(v, q, L, sid, nullptr, o, sh, nullptr, nullptr, q0);
+    if (a.trace && threadIdx.x == 0 && s_trace >= 0) {
+      long long *t = a.trace + 4 + 4 * s_trace;
+      t[1] = (long long)globaltimer_ns();
+      t[2] = (long long)L | ((long long)(p != a.rank) << 40) | ((long long)max(0, (int)*o.m) << 41);
+      t[3] = blockIdx.x;
+    }
   }
 }
 
@@ -2257,14 +2389,22 @@ cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s
 
 int export_tile_tokens() { return kExportTile; }
 
-cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s) {
+static int env_knob(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+cudaError_t launch_route_pack(char *region, int64_t n, const PushArgs &pa, cudaStream_t s) {
   if (n < 1) return cudaSuccess;
-  k_route_pack<<<148 * 8, kPackNT, 0, s>>>(region);
+  // push routing measured best with 2 CTAs per SM (its P2P stores queue behind the walk's
+  // traffic; N=2: 25.6 vs 24.6 M q/s at 8 per SM)
+  static const int grid_pull = env_knob("TM_PACK_GRID", 148 * 8), grid_push = env_knob("TM_PACK_GRID", 148 * 2);
+  k_route_pack<<<pa.stride ? grid_push : grid_pull, kPackNT, 0, s>>>(region, pa);
   return cudaGetLastError();
 }
 
-cudaError_t launch_route(char *region, const RouteHead &head, cudaStream_t s) {
-  k_route<<<1, kRouteNT, 0, s>>>(region, head);
+cudaError_t launch_route(char *region, const RouteHead &head, const PushArgs &pa, cudaStream_t s) {
+  k_route<<<1, kRouteNT, 0, s>>>(region, head, pa);
   return cudaGetLastError();
 }
 
@@ -2295,7 +2435,8 @@ static cudaError_t walk_routed_variant(const DevView &v, const RoutedArgs &a, in
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.nranks], kern, kWalkNT, smem);
     if (occ[a.nranks] < 1) occ[a.nranks] = 1;
-    if (PACKED) occ[a.nranks] = std::min(occ[a.nranks], kRoutedCtasPerSm);
+    static const int cap = env_knob(a.push_stride ? "TM_PUSH_WALK_OCC" : "TM_WALK_OCC", kRoutedCtasPerSm);
+    if (PACKED) occ[a.nranks] = std::min(occ[a.nranks], cap);
   }
   kern<<<num_sms * occ[a.nranks], kWalkNT, smem, s>>>(v, a);
   return cudaGetLastError();

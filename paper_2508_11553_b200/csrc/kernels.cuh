@@ -161,10 +161,19 @@ struct RouteRec {
   int64_t off;
   int32_t len;
   int32_t qi;
-  int32_t q0;  // first token (0 if len == 0)
-  int32_t pad_;
+  int32_t q0;      // first token (0 if len == 0)
+  int32_t has_q0;  // 0: q0 not filled in (the owner reads the query's first token itself)
 };
 static_assert(sizeof(RouteRec) == 32, "two 16-byte loads");
+
+// Push routing (tm_route_prepare_push): the requester writes each remote query's planes and
+// record straight into its owner's region (P2P stores), slice `rank` of the owner's inbox
+// at + rank * stride from the layout's lo / hi / rec offsets, so the owner's walk reads
+// them from its own HBM.  stride 0: the planes stay in the requester's region.
+struct PushArgs {
+  char *peer[kMaxRanks];  // every rank's region as mapped on this GPU (own included)
+  int64_t stride;
+};
 
 struct RoutedArgs {
   int nranks, rank;
@@ -172,8 +181,15 @@ struct RoutedArgs {
   const int32_t *g2l;           // global session id -> local session id (-1: not owned)
   int64_t g2l_len;              // entries of g2l; ids outside it are not owned here
   Sched *sched;
+  int64_t push_stride;          // > 0: requesters pushed their remote queries' planes and records
+                                // into this rank's region, source p's slice at + p * push_stride
   int64_t epoch;                // > 0: device-side barriers (wait for arrive, signal done)
   uint64_t timeout_ns;          // a peer silent this long is a device error, not a hang
+  int tail_every;               // > 0: every tail_every-th CTA takes items from the SHORT end of its
+                                // queue (latency-bound short queries overlap the long ones instead of
+                                // forming a tail after them)
+  long long *trace;             // diagnostics (TM_ROUTED_TRACE): per item {t0, t1, len | remote << 40, cta}
+  long long trace_cap;
 };
 
 // one batch of sequences resident on the device

@@ -75,9 +75,9 @@ cudaError_t launch_rebuild_index(const DevView &v, int64_t nrows, cudaStream_t s
 cudaError_t launch_fill_u64(uint64_t *p, int64_t n, uint64_t val, cudaStream_t s);
 cudaError_t launch_block_hash(const int32_t *tok, int64_t nblocks, uint64_t *out, int num_sms, cudaStream_t s);
 int export_tile_tokens();
-cudaError_t launch_route(char *region, const RouteHead &head, cudaStream_t s);
+cudaError_t launch_route(char *region, const RouteHead &head, const PushArgs &pa, cudaStream_t s);
 // pack the region's query tokens into its 18-bit planes (RouteDesc::lo_off / hi_off)
-cudaError_t launch_route_pack(char *region, int64_t n, cudaStream_t s);
+cudaError_t launch_route_pack(char *region, int64_t n, const PushArgs &pa, cudaStream_t s);
 // device-side barriers of the routed match (RoutedArgs::epoch > 0)
 cudaError_t launch_route_arrive(const RoutedArgs &a, cudaStream_t s);
 cudaError_t launch_route_wait_done(const DevView &v, const RoutedArgs &a, cudaStream_t s);

@@ -169,6 +169,7 @@ struct tm_store {
   // row ids an entry reserved but did not use (it re-recorded an existing sequence): handed
   // out again before fresh ids, so the row table grows with distinct sequences, not calls
   std::vector<int64_t> free_rows;
+  void *trace_buf = nullptr;  // TM_ROUTED_TRACE diagnostics
   // observability counters (tm_store_counters)
   int64_t c_record_calls = 0, c_records = 0, c_record_tokens = 0, c_match_calls = 0, c_queries = 0,
           c_export_calls = 0, c_export_rows = 0, c_export_tokens = 0;
@@ -817,7 +818,8 @@ int tm_store_destroy(tm_store *s) {
                   s->v.row_local, s->v.row_depth, s->v.row_run0, s->v.row_nrun, s->v.row_ext,
                   s->v.row_ext_tok, s->v.row_ext_len, s->v.row_ext_vb, s->v.row_jump, s->v.run_start,
                   s->v.run_version, s->v.run_origin, s->v.hk0, s->v.hk1, s->v.hval, s->v.s_nrows,
-                  s->v.s_stored, s->v.s_naive, s->v.s_pc_row, s->v.s_pc_vb, s->v.s_pc_cap, s->v.ctr, s->sched};
+                  s->v.s_stored, s->v.s_naive, s->v.s_pc_row, s->v.s_pc_vb, s->v.s_pc_cap, s->v.ctr, s->sched,
+                  s->trace_buf};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (auto &sl : s->slots) {
@@ -1639,9 +1641,9 @@ int tm_route_desc_bytes(int64_t *out_bytes) {
   return TM_OK;
 }
 
-int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, int32_t rank,
-                     void *stream) {
-  NvtxRange nvtx_("tm_route_prepare");
+namespace {
+int route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, int32_t rank,
+                  const tms::PushArgs &pa, void *stream) {
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
@@ -1668,16 +1670,41 @@ int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offset
     d.hi_off = packed ? offsets[9] : 0;
     d.pkf_off = packed ? offsets[10] : 0;
     d.pk_bad = 0;
-    d.rec_off = packed ? offsets[11] : 0;  // per-query records, written with the pack
+    // per-query records (gsid, offset, length, index, first token) at idx positions: own
+    // queries' written by k_route, remote ones' with the pack; the walk starts an item
+    // with one load
+    d.rec_off = offsets[11] > 0 ? offsets[11] : 0;
+    if (pa.stride && !packed) fail(TM_EINVAL, "push routing needs the plane and record offsets");
     {
       ProfScope ps(s, 4, st);
-      ck(tms::launch_route((char *)region, d, st), "route");
+      ck(tms::launch_route((char *)region, d, pa, st), "route");
     }
     if (packed) {
       ProfScope ps(s, 5, st);
-      ck(tms::launch_route_pack((char *)region, n, st), "route pack");
+      ck(tms::launch_route_pack((char *)region, n, pa, st), "route pack");
     }
   });
+}
+}  // namespace
+
+int tm_route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks, int32_t rank,
+                     void *stream) {
+  NvtxRange nvtx_("tm_route_prepare");
+  tms::PushArgs pa{};
+  return route_prepare(s, region, n, offsets, nranks, rank, pa, stream);
+}
+
+int tm_route_prepare_push(tm_store *s, void *region, int64_t n, const int64_t *offsets, int32_t nranks,
+                          int32_t rank, void *const *peer_regions, int64_t inbox_stride, void *stream) {
+  NvtxRange nvtx_("tm_route_prepare_push");
+  if (nranks < 1 || nranks > tms::kMaxRanks || inbox_stride <= 0 || !peer_regions) {
+    g_err = "push routing: bad rank count, inbox stride or peer table";
+    return TM_EINVAL;
+  }
+  tms::PushArgs pa{};
+  for (int p = 0; p < nranks; p++) pa.peer[p] = (char *)peer_regions[p];
+  pa.stride = inbox_stride;
+  return route_prepare(s, region, n, offsets, nranks, rank, pa, stream);
 }
 
 int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *stream) {
@@ -1691,7 +1718,7 @@ int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *
 
 namespace {
 int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                 int64_t g2l_len, int64_t epoch, void *stream) {
+                 int64_t g2l_len, int64_t epoch, int64_t push_stride, void *stream) {
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     if (g2l_len < 0 || (g2l_len > 0 && !g2l)) fail(TM_EINVAL, "bad g2l table");
@@ -1706,12 +1733,29 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
     a.g2l = g2l;
     a.g2l_len = g2l_len;
     a.sched = slot->sched;
+    a.push_stride = push_stride;
     a.epoch = epoch;
     static const uint64_t timeout_ms = [] {  // TM_PEER_TIMEOUT_MS (default 20 s)
       const char *e = getenv("TM_PEER_TIMEOUT_MS");
       return e ? (uint64_t)std::max(1ll, atoll(e)) : 20000ull;
     }();
     a.timeout_ns = timeout_ms * 1000000ull;
+    static const int tail_every = [] {  // TM_ROUTED_TAIL: 1 in N CTAs works from the short end (0: off)
+      const char *e = getenv("TM_ROUTED_TAIL");
+      return e ? std::max(0, atoi(e)) : 8;
+    }();
+    a.tail_every = tail_every;
+    // diagnostics: TM_ROUTED_TRACE=<path> appends every routed call's per-item timeline
+    // ({start ns, end ns, length | remote << 40 | matched << 41, CTA} per query) to
+    // <path>.<rank> (synchronous; not for timing runs)
+    static const char *trace_path = getenv("TM_ROUTED_TRACE");
+    constexpr long long kTraceCap = 1 << 20;
+    if (trace_path) {
+      if (!s->trace_buf) ck(cudaMalloc(&s->trace_buf, 8 * (4 + 4 * kTraceCap)), "cudaMalloc(trace)");
+      ck(cudaMemsetAsync(s->trace_buf, 0, 8 * (4 + 4 * kTraceCap), st), "memset(trace)");
+      a.trace = (long long *)s->trace_buf;
+      a.trace_cap = kTraceCap;
+    }
     if (epoch > 0) ck(tms::launch_route_arrive(a, st), "route arrive");
     {
       ProfScope ps(s, 0, st);
@@ -1720,6 +1764,21 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
     if (epoch > 0) {
       ProfScope ps(s, 6, st);
       ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
+    }
+    if (trace_path) {
+      long long cnt = 0;
+      ck(cudaStreamSynchronize(st), "trace sync");
+      ck(cudaMemcpy(&cnt, s->trace_buf, 8, cudaMemcpyDeviceToHost), "trace count");
+      cnt = std::min(cnt, kTraceCap);
+      std::vector<long long> buf(4 * (size_t)cnt);
+      ck(cudaMemcpy(buf.data(), (char *)s->trace_buf + 32, 32 * (size_t)cnt, cudaMemcpyDeviceToHost), "trace D2H");
+      const std::string fn = std::string(trace_path) + "." + std::to_string(rank);
+      if (FILE *f = fopen(fn.c_str(), "ab")) {
+        const long long hdr[2] = {cnt, (long long)epoch};
+        fwrite(hdr, 8, 2, f);
+        fwrite(buf.data(), 8, buf.size(), f);
+        fclose(f);
+      }
     }
     ck(cudaEventRecord(slot->done, st), "cudaEventRecord");
     slot->used = true;
@@ -1730,7 +1789,7 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
 int tm_match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
                     int64_t g2l_len, void *stream) {
   NvtxRange nvtx_("tm_match_routed");
-  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, 0, stream);
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, 0, 0, stream);
 }
 
 int tm_match_routed_sync(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
@@ -1740,7 +1799,17 @@ int tm_match_routed_sync(tm_store *s, int32_t nranks, int32_t rank, void *const 
     g_err = "epoch must be positive and increase by one per routed call";
     return TM_EINVAL;
   }
-  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, stream);
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, 0, stream);
+}
+
+int tm_match_routed_push(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                         int64_t g2l_len, int64_t epoch, int64_t inbox_stride, void *stream) {
+  NvtxRange nvtx_("tm_match_routed_push");
+  if (epoch <= 0 || inbox_stride <= 0) {
+    g_err = "push routing: epoch and inbox stride must be positive";
+    return TM_EINVAL;
+  }
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, inbox_stride, stream);
 }
 
 

@@ -65,38 +65,60 @@ class _CudaArray:
                                          "version": 3, "strides": None}
 
 
-def route_layout(n_max: int, tokens_max: int, header: int | None = None) -> tuple[list[int], int]:
+def route_layout(n_max: int, tokens_max: int, header: int | None = None,
+                 inbox: int = 0) -> tuple[list[int], int] | tuple[list[int], int, int]:
     """Byte offsets (sid, qoff, len, tok, idx, m, par, dup, low plane, high plane, pack
     blocks, query records) and total bytes of a region.  The 18-bit planes
     (include/tmstore.h) carry 128 positions of slack: owners copy them in 64-position
-    granules."""
+    granules.  ``inbox`` > 0 (push routing): the planes and records form ``inbox`` slices,
+    one per source rank, and the slice stride is returned as a third value."""
     if header is None:
         from . import _lib
 
         hb = C.c_int64()
         check(_lib.load().tm_route_desc_bytes(C.byref(hb)))
         header = hb.value
-    off, cur = [], (header + 255) // 256 * 256  # RouteDesc header
+    a = lambda nbytes: (nbytes + 255) // 256 * 256  # noqa: E731
+    off, cur = [], a(header)  # RouteDesc header
     planes = (tokens_max + 63) // 64 * 64 + 128
-    for nbytes in (8 * n_max, 8 * n_max, 8 * n_max, 4 * tokens_max, 4 * n_max, 8 * n_max, 8 * n_max, 8 * n_max,
-                   2 * planes, planes // 4, 4 * (n_max + 1), 32 * n_max):
+    sizes = (8 * n_max, 8 * n_max, 8 * n_max, 4 * tokens_max, 4 * n_max, 8 * n_max, 8 * n_max, 8 * n_max,
+             2 * planes, planes // 4, 4 * (n_max + 1), 32 * n_max)
+    if not inbox:
+        for nbytes in sizes:
+            off.append(cur)
+            cur += a(nbytes)
+        return off, cur
+    for nbytes in sizes[:8]:
         off.append(cur)
-        cur += (nbytes + 255) // 256 * 256
-    return off, cur
+        cur += a(nbytes)
+    pk = cur
+    cur += a(sizes[10])
+    lo, hi = cur, cur + a(sizes[8])
+    rec = hi + a(sizes[9])
+    stride = rec + a(sizes[11]) - lo
+    off += [lo, hi, pk, rec]
+    return off, lo + inbox * stride, stride
 
 
 class Router:
     """One rank's side of cross-GPU routing (collective construction: every rank of
     ``group`` must build its Router in the same order)."""
 
-    def __init__(self, store: DeviceStore, group, n_max: int, tokens_max: int, g2l):
+    def __init__(self, store: DeviceStore, group, n_max: int, tokens_max: int, g2l, push: bool = False):
         import torch
         import torch.distributed as dist
 
         self.store, self.group = store, group
         self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
         self.n_max, self.tokens_max = n_max, tokens_max
-        self.offsets, self.bytes = route_layout(n_max, tokens_max)
+        # push routing (peers only): requesters write remote queries' planes into the
+        # owners' inboxes, owners read them from their own HBM (tm_route_prepare_push)
+        self.push = bool(push) and self.nranks > 1
+        self.stride = 0
+        if self.push:
+            self.offsets, self.bytes, self.stride = route_layout(n_max, tokens_max, inbox=self.nranks)
+        else:
+            self.offsets, self.bytes = route_layout(n_max, tokens_max)
         ptr = C.c_void_p()
         check(store.lib.tm_shared_alloc(store.h, self.bytes, C.byref(ptr)))
         self.base = ptr.value
@@ -153,6 +175,10 @@ class Router:
             raise ValueError("batch larger than the routing region")
         st = (stream or torch.cuda.current_stream(self.store.device)).cuda_stream
         st = C.c_void_p(1 if st == 0 else st)
+        if self.push:
+            check(self.store.lib.tm_route_prepare_push(self.store.h, C.c_void_p(self.base), n, self._off_arr,
+                                                       self.nranks, self.rank, self._peer_arr, self.stride, st))
+            return
         check(self.store.lib.tm_route_prepare(self.store.h, C.c_void_p(self.base), n, self._off_arr, self.nranks,
                                               self.rank, st))
 
@@ -164,6 +190,13 @@ class Router:
         st = C.c_void_p(1 if st == 0 else st)
         lib, h = self.store.lib, self.store.h
         g2l = C.c_void_p(self.g2l.data_ptr())
+        if self.push:
+            if sync != "device":
+                raise ValueError("push routing uses the device-side barriers")
+            self._epoch += 1
+            check(lib.tm_match_routed_push(h, self.nranks, self.rank, self._peer_arr, g2l, self.g2l.numel(),
+                                           self._epoch, self.stride, st))
+            return
         if sync == "device" and self.nranks > 1:
             self._epoch += 1
             check(lib.tm_match_routed_sync(h, self.nranks, self.rank, self._peer_arr, g2l, self.g2l.numel(),

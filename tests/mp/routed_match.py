@@ -84,6 +84,43 @@ for r in (router, router2):
     ok = ok and np.array_equal(r.out_matched[: wl.n_queries].cpu().numpy(), m)
     ok = ok and np.array_equal(r.out_parent[: wl.n_queries].cpu().numpy(), par)
 router2.close()
+# push routing: requesters write the remote queries' planes into the owners' inboxes
+# (one batch, the big-id fallback, ragged lengths, and pipelined over two regions)
+if world > 1:
+    pr = [Router(store, dist.group.WORLD, n_max=wl.n_queries, tokens_max=int(need.item()), g2l=wl.g2l, push=True)
+          for _ in range(2)]
+    for r in pr:
+        wl.fill_queries(r)
+        r.out_matched.fill_(-7)
+    pr[0].match(wl.n_queries)
+    torch.cuda.synchronize()
+    ok = ok and np.array_equal(pr[0].out_matched[: wl.n_queries].cpu().numpy(), m)
+    ok = ok and np.array_equal(pr[0].out_parent[: wl.n_queries].cpu().numpy(), par)
+    ok = ok and np.array_equal(pr[0].out_dup[: wl.n_queries].cpu().numpy(), router.out_dup[: wl.n_queries].cpu().numpy())
+    pr[0].tokens[pos] = 1 << 20
+    pr[0].out_matched.fill_(-7)
+    pr[0].match(wl.n_queries)
+    torch.cuda.synchronize()
+    ok = ok and np.array_equal(pr[0].out_matched[: wl.n_queries].cpu().numpy(), m)
+    pr[0].tokens[pos] = saved
+    pr[0].qlen[: wl.n_queries].copy_(torch.as_tensor(short, device=dev))
+    pr[0].out_matched.fill_(-7)
+    pr[0].match(wl.n_queries)
+    torch.cuda.synchronize()
+    ok = ok and np.array_equal(pr[0].out_matched[: wl.n_queries].cpu().numpy(), np.minimum(short, wl.q_depth))
+    pr[0].qlen[: wl.n_queries].copy_(torch.as_tensor(wl.q_len, device=dev))
+    for r in pr:
+        r.out_matched.fill_(-7)
+    torch.cuda.synchronize()
+    match_pipelined(pr, wl.n_queries, 5)
+    torch.cuda.synchronize()
+    store.synchronize()
+    for r in pr:
+        ok = ok and np.array_equal(r.out_matched[: wl.n_queries].cpu().numpy(), m)
+        ok = ok and np.array_equal(r.out_parent[: wl.n_queries].cpu().numpy(), par)
+    print(f"rank {rank} push ok={ok}", flush=True)
+    for r in pr:
+        r.close()
 remote = float(np.mean(wl.owner[wl.q_g] != rank))
 flag = torch.tensor([1 if ok else 0], device=dev)
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)

@@ -42,6 +42,21 @@ def test_route_layout_disjoint_and_aligned():
         assert a % 256 == 0 and a + s <= b
 
 
+def test_route_layout_push_inbox_slices():
+    """Push routing: nranks slices of (low plane, high plane, records) at one stride, past
+    every other array, so slice p of one rank's region is written only by rank p."""
+    n, t, r = 4096, 1_000_000, 4
+    off, total, stride = route_layout(n, t, header=16_000, inbox=r)
+    planes = (t + 63) // 64 * 64 + 128
+    lo, hi, pk, rec = off[8:]
+    assert lo % 256 == 0 and hi % 256 == 0 and rec % 256 == 0 and stride % 256 == 0
+    assert lo + 2 * planes <= hi and hi + planes // 4 <= rec and rec + 32 * n <= lo + stride
+    assert pk + 4 * (n + 1) <= lo and max(off[:8]) < pk
+    assert total == lo + r * stride
+    flat, _ = route_layout(n, t, header=16_000)
+    assert off[:8] == flat[:8]
+
+
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
