@@ -743,7 +743,8 @@ def measure_c5(args, steps, warmup):
         from paper_2508_11553_b200.routing import match_pipelined
 
         side = torch.cuda.Stream(dev)
-        run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side)  # noqa: E731
+        defer = os.environ.get("BENCH_DEFER_DONE", "0") == "1"  # A/B knob: done waits on their own stream (measured neutral)
+        run_batches = lambda k: match_pipelined(routers, wl.n_queries, k, side, defer_done=defer)  # noqa: E731
     else:
         route = {"fused": router.match, "push": router.match,
                  "fused-nccl-barrier": lambda n: router.match(n, sync="nccl"),

@@ -225,6 +225,15 @@ int tm_match_routed(tm_store *store, int32_t nranks, int32_t rank, void *const *
 int tm_match_routed_sync(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
                          const int32_t *g2l, int64_t g2l_len, int64_t epoch, void *stream);
 
+/* tm_match_routed_sync (inbox_stride 0) or tm_match_routed_push without its last step: the
+ * wait for every owner's `done` flag is left to tm_route_wait_done, which the caller
+ * enqueues on another stream (ordered after this call), so the next batch's walk does not
+ * queue behind the peers' tails.  Results are visible to work ordered after that wait. */
+int tm_match_routed_nowait(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions,
+                           const int32_t *g2l, int64_t g2l_len, int64_t epoch, int64_t inbox_stride, void *stream);
+int tm_route_wait_done(tm_store *store, int32_t nranks, int32_t rank, void *const *peer_regions, int64_t epoch,
+                       void *stream);
+
 /* Push routing: the same exchange with the plane traffic turned around.  Each region
  * also holds an inbox of nranks slices at `inbox_stride` bytes apart (slice p = the
  * lo / hi / rec arrays of source rank p at offsets[8], [9], [11] + p * inbox_stride);

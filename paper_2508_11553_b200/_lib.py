@@ -62,6 +62,8 @@ SIGNATURES = {
     "tm_match_routed": (C.c_int, [_P, _I32, _I32, _P, _P, _I64, _P]),
     "tm_match_routed_sync": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _I64, C.c_int64, _P]),
     "tm_route_prepare_push": (C.c_int, [_P, _P, _I64, _P, _I32, _I32, _P, _I64, _P]),
+    "tm_match_routed_nowait": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _I64, C.c_int64, _I64, _P]),
+    "tm_route_wait_done": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int64, _P]),
     "tm_match_routed_push": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _I64, C.c_int64, _I64, _P]),
     "tm_route_counts": (C.c_int, [_P, _P, _P, _P]),
     "tm_profile_end": (C.c_int, [_P, _I32, _P, _P]),

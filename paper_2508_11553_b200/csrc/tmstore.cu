@@ -191,7 +191,7 @@ struct tm_store {
   bool pack_pending = false;
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
   bool pack_auto = true;                // TM_H2D_PACK_MIN unset: pack only as the node's sole GPU client
-  double pack_frac = 1.0;               // share of a packed call's tokens that is packed (TM_H2D_PACK_FRAC)
+  double pack_frac = 0.9;               // share of a packed call's tokens that is packed (TM_H2D_PACK_FRAC)
   int local_world = 1;                  // LOCAL_WORLD_SIZE (torchrun) at creation
   int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0,
           c_h2d_bytes = 0;  // token bytes actually copied host->device
@@ -1717,8 +1717,16 @@ int tm_route_counts(tm_store *s, const void *region, int32_t *out_counts, void *
 }
 
 namespace {
+uint64_t peer_timeout_ns() {  // TM_PEER_TIMEOUT_MS (default 20 s)
+  static const uint64_t ms = [] {
+    const char *e = getenv("TM_PEER_TIMEOUT_MS");
+    return e ? (uint64_t)std::max(1ll, atoll(e)) : 20000ull;
+  }();
+  return ms * 1000000ull;
+}
+
 int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
-                 int64_t g2l_len, int64_t epoch, int64_t push_stride, void *stream) {
+                 int64_t g2l_len, int64_t epoch, int64_t push_stride, void *stream, bool wait_done = true) {
   return guarded(s, [&] {
     if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks) fail(TM_EINVAL, "bad rank");
     if (g2l_len < 0 || (g2l_len > 0 && !g2l)) fail(TM_EINVAL, "bad g2l table");
@@ -1735,11 +1743,7 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
     a.sched = slot->sched;
     a.push_stride = push_stride;
     a.epoch = epoch;
-    static const uint64_t timeout_ms = [] {  // TM_PEER_TIMEOUT_MS (default 20 s)
-      const char *e = getenv("TM_PEER_TIMEOUT_MS");
-      return e ? (uint64_t)std::max(1ll, atoll(e)) : 20000ull;
-    }();
-    a.timeout_ns = timeout_ms * 1000000ull;
+    a.timeout_ns = peer_timeout_ns();
     static const int tail_every = [] {  // TM_ROUTED_TAIL: 1 in N CTAs works from the short end (0: off)
       const char *e = getenv("TM_ROUTED_TAIL");
       return e ? std::max(0, atoi(e)) : 8;
@@ -1761,7 +1765,7 @@ int match_routed(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_re
       ProfScope ps(s, 0, st);
       ck(tms::launch_walk_routed(s->v, a, s->num_sms, st), "walk_routed");
     }
-    if (epoch > 0) {
+    if (epoch > 0 && wait_done) {
       ProfScope ps(s, 6, st);
       ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
     }
@@ -1800,6 +1804,34 @@ int tm_match_routed_sync(tm_store *s, int32_t nranks, int32_t rank, void *const 
     return TM_EINVAL;
   }
   return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, 0, stream);
+}
+
+int tm_match_routed_nowait(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
+                           int64_t g2l_len, int64_t epoch, int64_t inbox_stride, void *stream) {
+  NvtxRange nvtx_("tm_match_routed_nowait");
+  if (epoch <= 0 || inbox_stride < 0) {
+    g_err = "epoch must be positive, inbox stride non-negative";
+    return TM_EINVAL;
+  }
+  return match_routed(s, nranks, rank, peer_regions, g2l, g2l_len, epoch, inbox_stride, stream, false);
+}
+
+int tm_route_wait_done(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, int64_t epoch,
+                       void *stream) {
+  NvtxRange nvtx_("tm_route_wait_done");
+  return guarded(s, [&] {
+    if (nranks < 1 || nranks > tms::kMaxRanks || rank < 0 || rank >= nranks || epoch <= 0)
+      fail(TM_EINVAL, "bad rank or epoch");
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    tms::RoutedArgs a{};
+    a.nranks = nranks;
+    a.rank = rank;
+    for (int p = 0; p < nranks; p++) a.peer[p] = (const char *)peer_regions[p];
+    a.epoch = epoch;
+    a.timeout_ns = peer_timeout_ns();
+    ProfScope ps(s, 6, st);
+    ck(tms::launch_route_wait_done(s->v, a, st), "route wait");
+  });
 }
 
 int tm_match_routed_push(tm_store *s, int32_t nranks, int32_t rank, void *const *peer_regions, const int32_t *g2l,
