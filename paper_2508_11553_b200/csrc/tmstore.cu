@@ -591,7 +591,12 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
       // of the tokens).  Packing alone leaves PCIe idle while the host packs; raw alone is
       // PCIe-bound - the split keeps both busy.
       size_t k = pieces.size();
-      if (s->pack_frac < 1.0 && !pieces.empty()) {
+      // (only from page-locked caller memory: a pageable source would be staged by the
+      // driver on this thread before the packing starts)
+      cudaPointerAttributes pa{};
+      const bool pinned_src = cudaPointerGetAttributes(&pa, tokens) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();  // (a pageable pointer may leave an error on older drivers)
+      if (s->pack_frac < 1.0 && !pieces.empty() && pinned_src) {
         int64_t tot = 0, acc = 0;
         for (const auto &pc : pieces) tot += pc.len;
         for (k = 0; k < pieces.size() && acc < (int64_t)(s->pack_frac * (double)tot); k++) acc += pieces[k].len;
