@@ -1380,7 +1380,7 @@ __device__ void record_chain_copy(const DevView &v, const Batch &b, int64_t e0, 
     const int64_t m = win ? sh.win_m[e - e0] : b.o_m[e], L = win ? sh.pre_len[e - e0] : b.len[e];
     if (L <= m) continue;
     const int64_t off = win ? sh.pre_off[e - e0] : b.off[e];
-    block_copy4<NT, kCopyU>(reinterpret_cast<int4 *>(v.arena + b.c_vb[e]), reinterpret_cast<const int4 *>(b.tok + off),
+    block_copy4<NT, (NT <= 32 ? 2 * kCopyU : kCopyU)>(reinterpret_cast<int4 *>(v.arena + b.c_vb[e]), reinterpret_cast<const int4 *>(b.tok + off),
                             m >> 2, (L + 3) >> 2);
     const int64_t r0 = b.run_off[e] + b.c_firstrun[e], nr = b.run_off[e + 1] - r0, d0 = b.c_run0[e];
     for (int64_t k = threadIdx.x; k < nr; k += NT) {
