@@ -192,6 +192,7 @@ struct tm_store {
   int64_t pack_min = int64_t(8) << 20;  // tokens per call below which the raw copy is used (TM_H2D_PACK_MIN; <0: off)
   bool pack_auto = true;                // TM_H2D_PACK_MIN unset: pack only as the node's sole GPU client
   double pack_frac = 0.9;               // share of a packed call's tokens that is packed (TM_H2D_PACK_FRAC)
+  bool pack_frac_set = false;           // TM_H2D_PACK_FRAC given: split pageable sources too
   int local_world = 1;                  // LOCAL_WORLD_SIZE (torchrun) at creation
   int64_t c_pack_calls = 0, c_pack_tokens = 0, c_raw_calls = 0, c_raw_tokens = 0, c_pack_fallbacks = 0,
           c_h2d_bytes = 0;  // token bytes actually copied host->device
@@ -596,7 +597,7 @@ void stage_tokens(tm_store *s, int64_t n, const int32_t *tokens, const int64_t *
       cudaPointerAttributes pa{};
       const bool pinned_src = cudaPointerGetAttributes(&pa, tokens) == cudaSuccess && pa.type == cudaMemoryTypeHost;
       cudaGetLastError();  // (a pageable pointer may leave an error on older drivers)
-      if (s->pack_frac < 1.0 && !pieces.empty() && pinned_src) {
+      if (s->pack_frac < 1.0 && !pieces.empty() && (pinned_src || s->pack_frac_set)) {
         int64_t tot = 0, acc = 0;
         for (const auto &pc : pieces) tot += pc.len;
         for (k = 0; k < pieces.size() && acc < (int64_t)(s->pack_frac * (double)tot); k++) acc += pieces[k].len;
@@ -776,7 +777,10 @@ int tm_store_create(const tm_config *cfg, tm_store **out) {
     s->pack_min = atoll(e);
     s->pack_auto = false;
   }
-  if (const char *e = getenv("TM_H2D_PACK_FRAC")) s->pack_frac = std::min(1.0, std::max(0.0, atof(e)));
+  if (const char *e = getenv("TM_H2D_PACK_FRAC")) {
+    s->pack_frac = std::min(1.0, std::max(0.0, atof(e)));
+    s->pack_frac_set = true;
+  }
   if (const char *e = getenv("LOCAL_WORLD_SIZE")) s->local_world = std::max(1, atoi(e));
   int rc = guarded(s, [&] {
     ck(cudaSetDevice(c.device), "cudaSetDevice");
