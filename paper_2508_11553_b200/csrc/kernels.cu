@@ -1680,6 +1680,7 @@ __device__ __forceinline__ void plan_tile(const DevView &v, const ExportArgs &e,
 }
 
 __global__ void k_export_plan(DevView v, ExportArgs e) {
+  asm volatile("griddepcontrol.launch_dependents;");  // k_export_tma may start its prologue
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < e.n; i += nwarps) {
@@ -1840,6 +1841,9 @@ __global__ void __launch_bounds__(kExportTmaNT) k_export_tma(DevView v, ExportAr
     mbar_init(&sm.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // launched as a programmatic dependent of k_export_plan: the prologue above overlaps the
+  // planner; everything it writes (plans, zeroed response starts) is read after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   fetch_plan(&sm.plan[0], &e.plan[t]);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
@@ -2253,8 +2257,17 @@ cudaError_t launch_export(const DevView &v, const ExportArgsHost &h, int num_sms
   }
   if (variant == 1) {
     const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * tma_ctas);
-    k_export_tma<<<(int)grid, kExportTmaNT, sizeof(ExportTmaSmem), s>>>(v, e);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kExportTmaNT);
+    cfg.dynamicSmemBytes = sizeof(ExportTmaSmem);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlaps the planner's tail
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_export_tma, v, e);
   }
   const int64_t grid = std::min<int64_t>(h.ntiles, (int64_t)num_sms * kExportCtas);
   k_export<<<(int)grid, kExportNT, 0, s>>>(v, e);
