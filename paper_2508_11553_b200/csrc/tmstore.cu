@@ -256,6 +256,10 @@ void ensure_rows(tm_store *s, int64_t need) {
   dev_grow(s->v.row_jump, n, nc, s->stream);
   s->row_cap = nc;
   s->v.row_cap = nc;
+  // the host mirror grows in place (no copy inside a record call), its new pages faulted in
+  // here, once per doubling, instead of by every call that appends rows
+  s->rows.reserve((size_t)nc);
+  memset((void *)(s->rows.data() + s->rows.size()), 0, (s->rows.capacity() - s->rows.size()) * sizeof(RowHost));
 }
 
 void ensure_runs(tm_store *s, int64_t need) {
@@ -896,13 +900,8 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       int64_t L = tok_len[k];
       if (L <= 0) fail(TM_EINVAL, "cannot insert an empty sequence");
       if (L >= (int64_t)INT32_MAX - 64) fail(TM_EINVAL, "sequence too long");
-      int64_t r0 = run_off[k], r1 = run_off[k + 1];
-      if (r1 <= r0 || run_start[r0] != 0) fail(TM_EINVAL, "tokens, origins, versions must be parallel");
-      for (int64_t r = r0 + 1; r < r1; r++)
-        if (run_start[r] <= run_start[r - 1] || run_start[r] >= L)
-          fail(TM_EINVAL, "tokens, origins, versions must be parallel");
-      for (int64_t r = r0; r < r1; r++)
-        if (run_origin[r] > 1) fail(TM_EINVAL, "bad origin");
+      const int64_t r0 = run_off[k], r1 = run_off[k + 1];
+      if (r1 <= r0) fail(TM_EINVAL, "tokens, origins, versions must be parallel");
       if (mem == TM_MEM_DEVICE && tok_off[k] % tms::kAlignWords)
         fail(TM_EINVAL, "device token offsets must be multiples of 32");
       int32_t c = s->chain_stamp[sid] == stamp ? s->chain_slot[sid] : -1;
@@ -919,6 +918,33 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       words_upper += round_up(L, tms::kAlignWords) + tms::kAlignWords;
       // the entry's row may reach path-copy depth: room for a fresh copy with 2x headroom
       if (s->sess_maxdepth[sid] + chain_len[c] >= tms::kPathCopyDepth) words_upper += round_up(2 * L, tms::kAlignWords);
+    }
+    {  // the metadata runs of every entry (trie.py:128-131), over the host pool for large batches
+      auto check_runs = [&](int64_t k0, int64_t k1) -> int {
+        for (int64_t k = k0; k < k1; k++) {
+          const int64_t L = tok_len[k], r0 = run_off[k], r1 = run_off[k + 1];
+          if (run_start[r0] != 0) return 1;
+          for (int64_t r = r0 + 1; r < r1; r++)
+            if (run_start[r] <= run_start[r - 1] || run_start[r] >= L) return 1;
+          for (int64_t r = r0; r < r1; r++)
+            if (run_origin[r] > 1) return 2;
+        }
+        return 0;
+      };
+      int bad = 0;
+      constexpr int64_t kCheckChunk = 4096;  // (a pool dispatch costs more than 16k entries' checks)
+      if (n >= 16 * kCheckChunk) {
+        std::atomic<int> worst{0};
+        tms::parallel_for((n + kCheckChunk - 1) / kCheckChunk, [&](int64_t c) {
+          const int r = check_runs(c * kCheckChunk, std::min(n, (c + 1) * kCheckChunk));
+          if (r) worst.store(r);
+        });
+        bad = worst.load();
+      } else {
+        bad = check_runs(0, n);
+      }
+      if (bad == 1) fail(TM_EINVAL, "tokens, origins, versions must be parallel");
+      if (bad == 2) fail(TM_EINVAL, "bad origin");
     }
     const int64_t nchains = (int64_t)chain_tokens.size();
     tr.mark("validate+chains");
@@ -1013,9 +1039,12 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     // entries - spread over the host pool for large batches
     h_roff[0] = 0;
     for (int64_t k = 0; k < n; k++) h_roff[k + 1] = h_roff[k] + (run_off[perm[k] + 1] - run_off[perm[k]]);
+    std::atomic<int64_t> qend_a{0};  // end of the query words (debug bounds of in-flight rows)
     auto stage_range = [&](int64_t k0, int64_t k1) {
+      int64_t lq = 0;
       for (int64_t k = k0; k < k1; k++) {
         const int64_t e = perm[k], rr = h_roff[k];
+        lq = std::max<int64_t>(lq, doff[k] + round_up(tok_len[e], 4));
         h_sid[k] = sids[e];
         h_off[k] = doff[k];
         h_len[k] = tok_len[e];
@@ -1025,8 +1054,11 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         memcpy(h_ro + rr, run_origin + r0, (r1 - r0));
         memcpy(h_rv + rr, run_version + r0, 4 * (r1 - r0));
       }
+      int64_t cur = qend_a.load(std::memory_order_relaxed);
+      while (lq > cur && !qend_a.compare_exchange_weak(cur, lq)) {
+      }
     };
-    constexpr int64_t kStageChunk = 2048;
+    constexpr int64_t kStageChunk = 1024;
     if (n >= 4 * kStageChunk) {
       tms::parallel_for((n + kStageChunk - 1) / kStageChunk,
                         [&](int64_t c) { stage_range(c * kStageChunk, std::min(n, (c + 1) * kStageChunk)); });
@@ -1073,8 +1105,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       ra.nchains = nchains;
       ra.work = (unsigned long long *)(d + o_work);
       tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
-      int64_t qend = 0;
-      for (int64_t k = 0; k < n; k++) qend = std::max<int64_t>(qend, doff[k] + round_up(h_len[k], 4));
+      const int64_t qend = qend_a.load();
       dv.qv_lo = (int64_t)(tok_base - s->v.arena);
       dv.qv_hi = dv.qv_lo + qend;
       int copy_warp = 0;
@@ -1086,6 +1117,9 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
     mark_done(s, s->stream);
     tr.mark("d2h+event");
+    // the mirror's new slots are laid out while the GPU records
+    s->rows.resize(row_base + n_fresh, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
+    tr.mark("mirror-slots");
     ck(cudaStreamSynchronize(s->stream), "record sync");
     tr.mark("sync");
     const int64_t *ctr = (const int64_t *)(h + o_ctr);
@@ -1094,7 +1128,6 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
                   *r_dup = (const int64_t *)(h + o_dup), *r_row = (const int64_t *)(h + o_crow);
     const int32_t *r_tn = (const int32_t *)(h + o_tn), *r_sp = (const int32_t *)(h + o_sp),
                   *r_loc = (const int32_t *)(h + o_cloc);
-    s->rows.resize(row_base + n_fresh, RowHost{-1, -1, -1, 0, 0, 0, -1, -1});
     // The host mirror, chain by chain (a chain is one session's entries in batch order).
     struct MirrorAcc {
       int64_t real = 0, maxd = 0;
@@ -1129,10 +1162,22 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
         if (out_added) out_added[e] = r_dup[k] < 0 ? L - m : 0;
       }
     };
-    // (a parallel version over host threads measured slower: the per-entry work is a few
-    // cache lines of session state, less than a pool dispatch)
+    // chains touch disjoint sessions, rows and outputs: large batches spread over the host
+    // pool (the row slots were faulted in ahead, see ensure_rows)
+    constexpr int64_t kMirrorEntries = 1024;  // entries per pool work item (whole chains)
     std::vector<MirrorAcc> accs(1);
-    for (int64_t c = 0; c < nchains; c++) mirror_chain(c, accs[0]);
+    if (n >= 4 * kMirrorEntries && nchains > 1) {
+      std::vector<int64_t> cut{0};
+      for (int64_t c = 0; c < nchains; c++)
+        if (chain_beg[c + 1] - chain_beg[cut.back()] >= kMirrorEntries || c + 1 == nchains) cut.push_back(c + 1);
+      const int64_t nck = (int64_t)cut.size() - 1;
+      accs.resize((size_t)nck);
+      tms::parallel_for(nck, [&](int64_t k) {
+        for (int64_t c = cut[k]; c < cut[k + 1]; c++) mirror_chain(c, accs[k]);
+      });
+    } else {
+      for (int64_t c = 0; c < nchains; c++) mirror_chain(c, accs[0]);
+    }
     for (const MirrorAcc &acc : accs) {
       if (acc.bad_row) fail(TM_ECUDA, "row numbering out of sync");
       if (acc.bad_ord) fail(TM_ECUDA, "session ordinal out of sync");
