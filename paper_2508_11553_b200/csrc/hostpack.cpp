@@ -23,13 +23,17 @@ class Pool {
   ~Pool() {
     {
       std::lock_guard<std::mutex> l(mu_);
-      stop_ = true;
+      stop_.store(true);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto &t : th_) t.join();
   }
   int size() const { return (int)th_.size() + 1; }
 
+  // A job is fanned out to every worker; workers that finish keep polling for the next job
+  // for a short while before they sleep, so the several parallel steps of one call (e.g. a
+  // record batch's checks, staging and mirror) do not each pay a futex wake-up per thread.
   void run(int64_t n, const std::function<void(int64_t)> &fn) {
     std::lock_guard<std::mutex> one_job(call_mu_);
     if (th_.empty() || n <= 1) {
@@ -41,32 +45,46 @@ class Pool {
       job_ = &fn;
       n_ = n;
       next_.store(0);
-      active_ = (int)th_.size();
-      gen_++;
+      active_.store((int)th_.size(), std::memory_order_relaxed);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     drain();  // the calling thread works too
-    std::unique_lock<std::mutex> l(mu_);
-    done_cv_.wait(l, [&] { return active_ == 0; });
+    for (int spin = 0; active_.load(std::memory_order_acquire) != 0; spin++) {
+      if (spin < kSpin) {
+        _mm_pause();
+        continue;
+      }
+      std::unique_lock<std::mutex> l(mu_);
+      done_cv_.wait(l, [&] { return active_.load(std::memory_order_acquire) == 0; });
+    }
     job_ = nullptr;
   }
 
  private:
+  static constexpr int kSpin = 1 << 14;  // ~50 us of polling before sleeping
   void drain() {
     for (int64_t i; (i = next_.fetch_add(1)) < n_;) (*job_)(i);
   }
   void worker() {
     uint64_t seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> l(mu_);
-        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
+      int spin = 0;
+      while (gen_.load(std::memory_order_acquire) == seen && spin < kSpin) {
+        _mm_pause();
+        spin++;
       }
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+      }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
       drain();
-      std::lock_guard<std::mutex> l(mu_);
-      if (--active_ == 0) done_cv_.notify_all();
+      if (active_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+        std::lock_guard<std::mutex> l(mu_);
+        done_cv_.notify_all();
+      }
     }
   }
 
@@ -76,9 +94,9 @@ class Pool {
   const std::function<void(int64_t)> *job_ = nullptr;
   std::atomic<int64_t> next_{0};
   int64_t n_ = 0;
-  int active_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<int> active_{0};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<bool> stop_{false};
 };
 
 Pool &pool() {
