@@ -187,7 +187,9 @@ bool pack18_supported() {
 int host_threads() {
   static const int n = [] {
     const char *e = getenv("TM_HOST_THREADS");
-    int v = e ? atoi(e) : (int)std::thread::hardware_concurrency();
+    // default: all cores up to 16 - packing is host-memory-bound, and more threads only
+    // crowd the copy engine's reads (24-core box, c4 e2e: 0.57 M q/s at 24 threads, 0.60-0.61 at 16)
+    int v = e ? atoi(e) : std::min(16, (int)std::thread::hardware_concurrency());
     return std::max(1, std::min(v, 64));
   }();
   return n;

@@ -28,7 +28,8 @@ bool pack_piece(const PackPiece &p, uint16_t *lo, uint8_t *hi);
 // memcpy with non-temporal stores (no read-for-ownership of the destination): for large
 // pinned -> pageable copies of results; falls back to memcpy without AVX2.
 void copy_stream(void *dst, const void *src, size_t n);
-// Host thread pool shared by all stores of the process (TM_HOST_THREADS, default: all cores).
+// Host thread pool shared by all stores of the process (TM_HOST_THREADS, default: all cores
+// up to 16).
 int host_threads();
 void parallel_for(int64_t n, const std::function<void(int64_t)> &fn);
 
