@@ -498,7 +498,11 @@ bool stage_packed(tm_store *s, const std::vector<tms::PackPiece> &pieces, int64_
   s->pack_pending = false;
   int64_t total = 0;
   for (const auto &p : pieces) total += p.len;
-  const int64_t chunk = std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(1) << 19, total / 24));
+  static const int64_t nsplit = [] {  // TM_H2D_CHUNKS (tuning): copies per call
+    const char *e = getenv("TM_H2D_CHUNKS");
+    return e ? std::max<int64_t>(1, atoll(e)) : 12;  // 24-core box: 12 -> 0.62-0.64, 24 -> 0.62, 48 -> 0.55 M q/s
+  }();
+  const int64_t chunk = std::max<int64_t>(int64_t(1) << 19, total / nsplit);
   std::vector<size_t> cbeg{0};  // chunk c = pieces [cbeg[c], cbeg[c+1])
   std::vector<int32_t> chunk_of(pieces.size());
   for (size_t i = 0, tok = 0; i < pieces.size(); i++) {
