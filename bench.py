@@ -697,6 +697,65 @@ def measure_config(cfg, reps=3, with_cpu=True):
 
 # ------------------------------------------------------------------------------------- c5
 
+def measure_config_shards(cfg, rank, world, local, dev, reps=3):
+    """N > 1: configs 2 / 3 as weak-scaling shards - every rank records and exports its own
+    copy of the config's sessions (sessions are independent) into its own
+    store; device time of K2 and K3 (CUDA events), max over ranks; aggregate rates."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_11553_b200 import DeviceStore
+    from workloads import SEED0, RecordWorkload
+
+    peak, _ = peaks()
+    wl = RecordWorkload(cfg, seed=SEED0 + 100 * cfg + rank)
+    sids, tok, off, roff, rs, ro, rv = wl.packed()
+    lens = np.diff(off)
+    pad = (lens + 31) // 32 * 32
+    aoff = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(pad, out=aoff[1:])
+    atok = np.zeros(int(aoff[-1]), np.int32)
+    for k in range(len(lens)):
+        atok[aoff[k]: aoff[k] + lens[k]] = tok[off[k]: off[k + 1]]
+    dtok = torch.from_numpy(atok).to(dev)
+    n_rec = len(lens)
+    store = DeviceStore(local, arena_words=(reps + 2) * int(aoff[-1]) + (1 << 22), row_capacity=(reps + 2) * n_rec + 64,
+                        run_capacity=(reps + 2) * len(rs) + 64, session_capacity=(reps + 2) * wl.n_sessions + 16)
+    store.profile_begin(reserve=64)
+    best_k2 = best_ex = float("inf")
+    r = rows = None
+    n_out = 0
+    for _ in range(reps + 1):
+        smap = [store.new_session() for _ in range(wl.n_sessions)]
+        g = np.asarray([smap[x] for x in sids], np.int32)
+        torch.cuda.synchronize()
+        store.profile_begin()
+        r = store.record_device(g, dtok, aoff[:-1], lens, roff, rs, ro, rv)
+        k2, _ = store.profile_end("commit")
+        rows = np.asarray(r.row, np.int64)
+        n_out = int(store.rows_total(rows))
+        torch.cuda.synchronize()
+        store.profile_begin()
+        store.export_device(rows)
+        torch.cuda.synchronize()
+        ex, _ = store.profile_end("export")
+        best_k2, best_ex = min(best_k2, k2), min(best_ex, ex)
+    m = r.matched.astype(np.int64)
+    cq = np.where(r.parent_local >= 0, np.minimum(m + 1, lens), 0)  # (upper bound on |parent|: the own length)
+    rec_bytes = float((8 * cq + 8 * (lens - m)).sum())
+    exp_bytes = 13.0 * n_out + 8.0 * len(rows)
+    t = torch.tensor([best_k2, best_ex], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    k2_max, ex_max = float(t[0]), float(t[1])
+    store.close()
+    return {"workload": f"c{cfg} x {world} shards (every rank its own {wl.n_sessions} sessions)",
+            "records_per_s": world * n_rec / k2_max * 1e3, "record_ms_max_over_ranks": k2_max,
+            "record_frac_per_rank": rec_bytes / k2_max / 1e6 / peak,
+            "export_tokens_per_s": world * n_out / ex_max * 1e3, "export_ms_max_over_ranks": ex_max,
+            "export_frac_per_rank": exp_bytes / ex_max / 1e6 / peak, "peak_GBps": peak,
+            "timing": "CUDA events around K2 / K3 on each rank (best of reps), max over ranks"}
+
+
 def measure_c5(args, steps, warmup):
     """Config 5: 1M sessions (log-uniform 1k-128k tokens) sharded by session hash; every
     rank originates 4096 queries for sessions owned anywhere; Router.match routes them
@@ -871,6 +930,8 @@ def main():
         if world > 1:  # the host-routed weak-scaling shards beside it (every rank its own c4 shard)
             line["c4_shards"] = {k: v for k, v in measure_c4(args, rank, world, local, dev).items()
                                  if k in ("value", "ms_per_step", "config", "roofline", "e2e", "tokens_compared_per_s")}
+            if not args.no_configs:  # record / export of configs 2 and 3 as shards
+                line["config_shards"] = {f"c{c}": measure_config_shards(c, rank, world, local, dev) for c in (2, 3)}
     else:
         line = measure_c4(args, rank, world, local, dev)
         if world == 1 and not args.no_configs:
