@@ -23,6 +23,8 @@ One JSON line (rank 0).  Headline workload by GPU count (BASELINE.json configs):
                 include_partials export, device and call rates with their rooflines, next to
                 the C port and the unmodified reference
   c5_routed     (N = 1) config 5 at one GPU (1M sessions in one 107 GB store, routed path)
+  c4_shards,    (N > 1) weak-scaling shards beside the routed headline: every rank its own
+  config_shards c4 match shard, and its own copy of configs 2 / 3 recorded and exported
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
