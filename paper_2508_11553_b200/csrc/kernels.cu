@@ -1254,37 +1254,65 @@ __device__ void record_copy_warp(const DevView &v, const Batch &b, RecShared &sh
     m = __shfl_sync(0xffffffffu, m, 0);
     L = __shfl_sync(0xffffffffu, L, 0);
     off = __shfl_sync(0xffffffffu, off, 0);
+    // the arena atomic, the run table's offsets, the suffix's first round and up to 32 run
+    // starts are all in flight together; only the stores wait for the allocations
     long long vb = 0, run0 = 0;
-    int fr = 0, nr = 0;
     if (lane == 0) {
       const long long words = ((L + kAlignWords - 1) / kAlignWords) * kAlignWords - ((long long)m / kAlignWords) * kAlignWords;
       vb = (long long)atomicAdd((unsigned long long *)&v.ctr[0], (unsigned long long)words) - (m / kAlignWords) * kAlignWords;
-      fr = first_run_at(b, e, m);
-      nr = (int)(b.run_off[e + 1] - b.run_off[e]) - fr;
-      run0 = (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)nr);
-      TM_DCHECK(v, vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap, kErrArena);
-      TM_DCHECK(v, run0 >= 0 && run0 + nr <= v.run_cap, kErrRun);
     }
+    const int64_t ra = b.run_off[e], rb = b.run_off[e + 1];
+    const int4 *src = reinterpret_cast<const int4 *>(b.tok + off);
+    const int64_t i1 = (L + 3) >> 2;
+    const int64_t base0 = (m >> 2) + lane;
+    int4 t[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) t[k] = ldg_stream_if(src + base0 + 32 * k, base0 + 32 * k < i1);
+    int fr;
+    int32_t rst = 0, rver = 0;
+    uint8_t rorg = 0;
+    const bool few = rb - ra <= 32;
+    if (few) {  // the run containing m: one round of loads and a ballot
+      const bool have = lane < rb - ra;
+      if (have) {
+        rst = b.run_start[ra + lane];
+        rorg = b.run_origin[ra + lane];
+        rver = b.run_version[ra + lane];
+      }
+      fr = __popc(__ballot_sync(0xffffffffu, have && lane > 0 && rst <= m));
+    } else {
+      fr = lane == 0 ? first_run_at(b, e, m) : 0;
+      fr = __shfl_sync(0xffffffffu, fr, 0);
+    }
+    const int nr = (int)(rb - ra) - fr;
+    if (lane == 0) run0 = (long long)atomicAdd((unsigned long long *)&v.ctr[2], (unsigned long long)nr);
     vb = __shfl_sync(0xffffffffu, vb, 0);
     run0 = __shfl_sync(0xffffffffu, run0, 0);
-    fr = __shfl_sync(0xffffffffu, fr, 0);
-    nr = __shfl_sync(0xffffffffu, nr, 0);
-    const int4 *src = reinterpret_cast<const int4 *>(b.tok + off);
+    TM_DCHECK(v, vb + (m & ~31ll) >= 0 && vb + ((L + 31) & ~31ll) <= v.arena_cap, kErrArena);
+    TM_DCHECK(v, run0 >= 0 && run0 + nr <= v.run_cap, kErrRun);
     int4 *dst = reinterpret_cast<int4 *>(v.arena + vb);
-    const int64_t i1 = (L + 3) >> 2;
-    for (int64_t base = (m >> 2) + lane; base < i1; base += 32 * 8) {
-      int4 t[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) stg_if(dst + base0 + 32 * k, t[k], base0 + 32 * k < i1);
+    for (int64_t base = base0 + 32 * 8; base < i1; base += 32 * 8) {
 #pragma unroll
       for (int k = 0; k < 8; k++) t[k] = ldg_stream_if(src + base + 32 * k, base + 32 * k < i1);
 #pragma unroll
       for (int k = 0; k < 8; k++) stg_if(dst + base + 32 * k, t[k], base + 32 * k < i1);
     }
-    const int64_t r0 = b.run_off[e] + fr;
-    for (int k = lane; k < nr; k += 32) {
-      const int32_t st = b.run_start[r0 + k];
-      v.run_start[run0 + k] = st > m ? st : m;
-      v.run_origin[run0 + k] = b.run_origin[r0 + k];
-      v.run_version[run0 + k] = b.run_version[r0 + k];
+    if (few) {
+      if (lane >= fr && lane < rb - ra) {
+        v.run_start[run0 + lane - fr] = rst > m ? rst : m;
+        v.run_origin[run0 + lane - fr] = rorg;
+        v.run_version[run0 + lane - fr] = rver;
+      }
+    } else {
+      const int64_t r0 = ra + fr;
+      for (int k = lane; k < nr; k += 32) {
+        const int32_t st = b.run_start[r0 + k];
+        v.run_start[run0 + k] = st > m ? st : m;
+        v.run_origin[run0 + k] = b.run_origin[r0 + k];
+        v.run_version[run0 + k] = b.run_version[r0 + k];
+      }
     }
     if (lane == 0) {
       b.c_vb[e] = vb;
@@ -1423,16 +1451,24 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
     long long next_it = 0;  // thread 0: the next chain, claimed at this chain's start (used at its end)
     for (;;) {
       if (it >= a.nchains) break;
-      const int64_t e0 = a.chains[3 * it], e1 = a.chains[3 * it + 1];
+      const bool given = it == 0 && a.c0_e1 >= 0;  // chain 0 in the parameters
+      const int64_t e0 = given ? 0 : a.chains[3 * it], e1 = given ? a.c0_e1 : a.chains[3 * it + 1];
       for (int t = threadIdx.x; t < kRecPre && e0 + t < e1; t += NT) {  // the first entries, beside the session
+        if (given && t == 0) {
+          sh.pre_off[0] = a.c0_off;
+          sh.pre_len[0] = a.c0_len;
+          sh.pre_q0[0] = a.c0_q0;
+          continue;
+        }
         const int64_t off = b.off[e0 + t];
         sh.pre_off[t] = off;
         sh.pre_len[t] = (int)b.len[e0 + t];
         sh.pre_q0[t] = b.tok[off];
       }
       if (threadIdx.x == 0) {  // the session, cached for the whole chain
-        next_it = (long long)gridDim.x + (long long)atomicAdd(&a.work[0], 1ull);
-        const int32_t sid = (int32_t)a.chains[3 * it + 2];
+        if (a.nchains > (int64_t)gridDim.x) next_it = (long long)gridDim.x + (long long)atomicAdd(&a.work[0], 1ull);
+        else next_it = a.nchains;  // every chain has its own CTA: nothing to claim
+        const int32_t sid = given ? a.c0_sid : (int32_t)a.chains[3 * it + 2];
         sh.sid = sid;
         sh.nrows = v.s_nrows[sid];
         sh.stored = v.s_stored[sid];
@@ -1527,7 +1563,9 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
   }
   if (a.ctr_out) {  // the last CTA out: every counter update of the launch is done
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (gridDim.x == 1) {  // the only CTA: its own updates are ordered by the barrier
+      s_item = 1;
+    } else if (threadIdx.x == 0) {
       __threadfence();
       s_item = atomicAdd(&a.work[1], 1ull) == gridDim.x - 1;
     }
@@ -1535,6 +1573,13 @@ __global__ void __launch_bounds__(NT + 32 * NCW, MINB) k_record_tma(DevView v, R
     if (s_item && threadIdx.x < 4) {
       __threadfence();
       a.ctr_out[threadIdx.x] = *(volatile long long *)&v.ctr[threadIdx.x];
+    }
+    if (a.out_dst) {  // results (ctr snapshot included) into the caller's pinned buffer
+      __syncthreads();
+      if (s_item) {
+        for (int64_t i = threadIdx.x; i < a.out_len; i += blockDim.x) a.out_dst[i] = ldg_coh(a.out_src + i);
+        __threadfence_system();
+      }
     }
   }
 }

@@ -228,6 +228,15 @@ struct RecordArgs {
   int64_t *ctr_out;           // non-null: the last CTA out copies the 4 counters here (one D2H for the host)
   int64_t nchains;
   unsigned long long *work;   // [0] chain counter, [1] CTAs done: zeroed by the call's staging copy
+  // chain 0 handed over in the launch parameters (host batches: no dependent loads for the
+  // first chain's table entry, its session id and its first entry): c0_e1 < 0 = not given
+  int64_t c0_e1, c0_off;
+  int32_t c0_sid, c0_len, c0_q0;
+  // small host calls: the last CTA copies the results region [out_src, out_src + out_len)
+  // straight into page-locked host memory (no device-to-host copy call); out_dst null: none
+  const int4 *out_src;
+  int4 *out_dst;
+  int64_t out_len;  // int4 units
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

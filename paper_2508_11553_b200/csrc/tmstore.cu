@@ -1082,6 +1082,7 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
     tr.mark("stage");
     ck(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, s->stream), "H2D batch");
     tr.mark("h2d");
+    bool direct_out = false;
     {
       tms::RecordArgs ra{};
       Batch &b = ra.b;
@@ -1108,17 +1109,39 @@ int tm_record_batch(tm_store *s, int64_t n, int32_t mem, const int32_t *sids, co
       ra.ctr_out = (int64_t *)(d + o_ctr);  // the last CTA out snapshots the counters beside the results
       ra.nchains = nchains;
       ra.work = (unsigned long long *)(d + o_work);
+      ra.c0_e1 = -1;
+      ra.out_dst = nullptr;
+      if (small) {  // results come back through the kernel's own stores into the pinned staging
+        void *hd = nullptr;
+        if (cudaHostGetDevicePointer(&hd, h + o_crow, 0) == cudaSuccess && hd && (o_crow % 16) == 0 &&
+            (out_end - o_crow) % 16 == 0) {
+          ra.out_src = (const int4 *)(d + o_crow);
+          ra.out_dst = (int4 *)hd;
+          ra.out_len = (int64_t)(out_end - o_crow) / 16;
+        }
+        cudaGetLastError();
+      }
+      if (nchains == 1 && mem == TM_MEM_HOST) {  // one session (e.g. lpm_insert): chain 0 as parameters
+        const int64_t e = perm[0];
+        ra.c0_e1 = n;
+        ra.c0_sid = sids[e];
+        ra.c0_off = doff[0];
+        ra.c0_len = (int32_t)tok_len[e];
+        ra.c0_q0 = tokens[tok_off[e]];
+      }
       tms::DevView dv = s->v;  // rows committed in the launch live in the query buffer until the copy
       const int64_t qend = qend_a.load();
       dv.qv_lo = (int64_t)(tok_base - s->v.arena);
       dv.qv_hi = dv.qv_lo + qend;
+      direct_out = ra.out_dst != nullptr;
       int copy_warp = 0;
       ProfScope ps(s, 1, s->stream);
       ck(tms::launch_record(dv, ra, s->num_sms, s->stream, &copy_warp), "record");
       tr.mark("launch");
     }
     // ---- results back (chain order), into the host mirror in batch order
-    ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
+    if (!direct_out)
+      ck(cudaMemcpyAsync(h + o_crow, d + o_crow, out_end - o_crow, cudaMemcpyDeviceToHost, s->stream), "D2H results");
     mark_done(s, s->stream);
     tr.mark("d2h+event");
     // the mirror's new slots are laid out while the GPU records
