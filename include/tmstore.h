@@ -266,7 +266,8 @@ int tm_block_hashes(tm_store *store, const int32_t *tokens, int64_t n_words, uin
  * summed device time and launch count of one kernel kind (TM_KERNEL_*), then stops. */
 enum {
   TM_KERNEL_WALK = 0, TM_KERNEL_COMMIT = 1, TM_KERNEL_EXPORT = 2, TM_KERNEL_PLAN = 3,
-  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6, TM_KERNEL_RECORD_COPY = 7,
+  TM_KERNEL_ROUTE = 4, TM_KERNEL_ROUTE_PACK = 5, TM_KERNEL_ROUTE_WAIT = 6,
+  TM_KERNEL_RECORD_COPY = 7, /* (no longer launched: K2 copies inside its one launch; always 0) */
   TM_KERNEL_BLOCK_HASH = 8
 };
 int tm_profile_begin(tm_store *store);

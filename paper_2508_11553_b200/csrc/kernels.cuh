@@ -58,7 +58,7 @@ struct DevView {
   int64_t arena_cap, row_cap, run_cap;
   int64_t n_sess;  // sessions created: device-buffer matches treat any other id as unknown (matched 0)
   // record launches: rows committed in the launch are read from their entry's query until
-  // k_record_copy moves them into the arena; their virtual bases fall in [qv_lo, qv_hi)
+  // the chain's copy moves them into the arena; their virtual bases fall in [qv_lo, qv_hi)
   // (debug bounds checks only)
   int64_t qv_lo, qv_hi;
 };
