@@ -206,34 +206,69 @@ static PyObject *meta_runs(PyObject *self, PyObject *args) {
     goto done;
   }
   PyObject **oi = PySequence_Fast_ITEMS(fo), **vi = PySequence_Fast_ITEMS(fv);
-  /* one pass into worst-case buffers, then shrunk to the run count */
-  bs = PyByteArray_FromStringAndSize(NULL, 4 * (n > 0 ? n : 1));
-  bo = PyByteArray_FromStringAndSize(NULL, n > 0 ? n : 1);
-  bv = PyByteArray_FromStringAndSize(NULL, 4 * (n > 0 ? n : 1));
-  if (!bs || !bo || !bv) goto done;
-  int32_t *s = (int32_t *)PyByteArray_AS_STRING(bs), *vv = (int32_t *)PyByteArray_AS_STRING(bv);
-  uint8_t *oo = (uint8_t *)PyByteArray_AS_STRING(bo);
-  Py_ssize_t nr = 0;
-  int po = -1;
-  int32_t pv = 0;
-  for (Py_ssize_t i = 0; i < n; i++) {
-    const int o = origin_code(oi[i], model_output, agent_input);
-    int64_t v;
-    int32_t v32;
-    if (compact_value(vi[i], &v)) v32 = (int32_t)v;
-    else if (to_i32(vi[i], &v32) < 0) goto done;
-    if (i == 0 || o != po || v32 != pv) {
-      s[nr] = (int32_t)i;
-      oo[nr] = (uint8_t)o;
-      vv[nr] = v32;
-      nr++;
+  /* one pass: runs collected in a small growable buffer (a handful for real sequences),
+   * items compared by identity first (a list of enum members or of one small int repeats
+   * the same objects, so a run's interior is a pointer scan); then exact-size bytearrays */
+  Py_ssize_t nr = 0, cap = 64;
+  int32_t st_buf[64], vr_buf[64];
+  uint8_t or_buf[64];
+  int32_t *rs = st_buf, *rv = vr_buf;
+  uint8_t *ro = or_buf;
+  int heap = 0, failed = 0;
+  {
+    PyObject *a = NULL, *b = NULL;
+    int po = -1;
+    int32_t pv = 0;
+    Py_ssize_t i = 0;
+    while (i < n) {
+      if (oi[i] == a && vi[i] == b) {  /* scan the rest of the run */
+        while (i + 4 <= n && oi[i] == a && oi[i + 1] == a && oi[i + 2] == a && oi[i + 3] == a && vi[i] == b &&
+               vi[i + 1] == b && vi[i + 2] == b && vi[i + 3] == b)
+          i += 4;
+        while (i < n && oi[i] == a && vi[i] == b) i++;
+        continue;
+      }
+      const int o = origin_code(oi[i], model_output, agent_input);
+      int64_t v;
+      int32_t v32;
+      if (compact_value(vi[i], &v)) v32 = (int32_t)v;
+      else if (to_i32(vi[i], &v32) < 0) { failed = 1; break; }
+      if (i == 0 || o != po || v32 != pv) {
+        if (nr == cap) {  /* grow (rare): move to the heap */
+          const Py_ssize_t nc = 2 * cap;
+          int32_t *ns = (int32_t *)PyMem_Malloc(4 * nc), *nv = (int32_t *)PyMem_Malloc(4 * nc);
+          uint8_t *no = (uint8_t *)PyMem_Malloc(nc);
+          if (!ns || !nv || !no) {
+            PyMem_Free(ns); PyMem_Free(nv); PyMem_Free(no);
+            PyErr_NoMemory();
+            failed = 1;
+            break;
+          }
+          memcpy(ns, rs, 4 * nr); memcpy(nv, rv, 4 * nr); memcpy(no, ro, nr);
+          if (heap) { PyMem_Free(rs); PyMem_Free(rv); PyMem_Free(ro); }
+          rs = ns; rv = nv; ro = no;
+          cap = nc;
+          heap = 1;
+        }
+        rs[nr] = (int32_t)i;
+        ro[nr] = (uint8_t)o;
+        rv[nr] = v32;
+        nr++;
+      }
+      po = o;
+      pv = v32;
+      a = oi[i];
+      b = vi[i];
+      i++;
     }
-    po = o;
-    pv = v32;
   }
-  if (nr > 0 && (PyByteArray_Resize(bs, 4 * nr) < 0 || PyByteArray_Resize(bo, nr) < 0 ||
-                 PyByteArray_Resize(bv, 4 * nr) < 0))
-    goto done;
+  if (!failed) {
+    bs = PyByteArray_FromStringAndSize((const char *)rs, 4 * nr);
+    bo = PyByteArray_FromStringAndSize((const char *)ro, nr);
+    bv = PyByteArray_FromStringAndSize((const char *)rv, 4 * nr);
+  }
+  if (heap) { PyMem_Free(rs); PyMem_Free(rv); PyMem_Free(ro); }
+  if (failed || !bs || !bo || !bv) goto done;
   res = Py_BuildValue("(OOOn)", bs, bo, bv, nr);
 done:
   Py_XDECREF(bs);
