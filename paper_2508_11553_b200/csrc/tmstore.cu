@@ -1754,7 +1754,8 @@ int route_prepare(tm_store *s, void *region, int64_t n, const int64_t *offsets, 
     // per-query records (gsid, offset, length, index, first token) at idx positions: own
     // queries' written by k_route, remote ones' with the pack; the walk starts an item
     // with one load
-    d.rec_off = offsets[11] > 0 ? offsets[11] : 0;
+    // (with peers only when the pack runs: it writes the remote queries' records)
+    d.rec_off = (offsets[11] > 0 && (packed || nranks == 1)) ? offsets[11] : 0;
     if (pa.stride && !packed) fail(TM_EINVAL, "push routing needs the plane and record offsets");
     {
       ProfScope ps(s, 4, st);
