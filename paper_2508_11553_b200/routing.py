@@ -21,7 +21,10 @@ in the region headers written and polled by the kernels themselves over NVLink โ
 collective library call per batch.  ``sync="nccl"`` (``tm_match_routed``) brackets the
 kernel with one-element NCCL all-reduces instead.  ``match_pipelined`` runs a stream of
 batches over two regions: batch k+1 is bucketed and packed on a side stream while batch k
-is exchanged and matched.  PyTorch provides the process group
+is exchanged and matched.  Measured alternatives kept behind flags (DESIGN.md ยง6):
+``Router(push=True)`` has requesters write the planes into the owners' inboxes instead of
+owners pulling them, and ``match_pipelined(defer_done=True)`` waits for the owners' done
+flags on a stream of its own.  PyTorch provides the process group
 (setup plumbing: the IPC handle exchange); routing and matching run in the CUDA kernels
 behind include/tmstore.h.
 """
