@@ -60,3 +60,24 @@ def test_store_create_fails_loudly_without_gpu(lib):
     assert rc != 0
     lib.tm_last_error.restype = ctypes.c_char_p
     assert lib.tm_last_error()
+
+
+def declared_arities():
+    """tm_* name -> parameter count, from the prototypes in include/tmstore.h."""
+    src = re.sub(r"/\*.*?\*/", " ", open(HEADER).read(), flags=re.S)
+    out = {}
+    for m in re.finditer(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tm_\w+)\s*\(([^;{]*?)\)\s*;", src, re.M):
+        params = " ".join(m.group(2).split())
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_python_binding_arities_match_header():
+    """Every ctypes signature in _lib.SIGNATURES passes as many arguments as the C
+    prototype takes (a mismatch would only show up as a crash on the GPU box)."""
+    from paper_2508_11553_b200._lib import SIGNATURES
+
+    ar = declared_arities()
+    assert sorted(ar) == declared_symbols()
+    bad = {k: (len(SIGNATURES[k][1]), ar[k]) for k in ar if len(SIGNATURES[k][1]) != ar[k]}
+    assert bad == {}
