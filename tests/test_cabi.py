@@ -81,3 +81,34 @@ def test_python_binding_arities_match_header():
     assert sorted(ar) == declared_symbols()
     bad = {k: (len(SIGNATURES[k][1]), ar[k]) for k in ar if len(SIGNATURES[k][1]) != ar[k]}
     assert bad == {}
+
+
+def _ctype_of(param: str):
+    p = " ".join(param.split())
+    if "*" in p:
+        return "ptr"
+    for c_name, kind in (("uint64_t", "u64"), ("int64_t", "i64"), ("uint32_t", "u32"), ("int32_t", "i32"),
+                         ("double", "f64"), ("int", "i32")):
+        if re.search(r"\b" + c_name + r"\b", p):
+            return kind
+    raise AssertionError(f"unmapped C parameter type: {param!r}")
+
+
+def test_python_binding_types_match_header():
+    """...and in every position the same kind of argument: pointer, int32, int64 (an int32 /
+    int64 swap would pass ctypes and corrupt the call)."""
+    import ctypes as C
+
+    from paper_2508_11553_b200._lib import SIGNATURES
+
+    kind = {C.c_void_p: "ptr", C.c_char_p: "ptr", C.c_int64: "i64", C.c_int32: "i32", C.c_int: "i32",
+            C.c_uint64: "u64", C.c_uint32: "u32", C.c_double: "f64"}
+    src = re.sub(r"/\*.*?\*/", " ", open(HEADER).read(), flags=re.S)
+    bad = []
+    for m in re.finditer(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tm_\w+)\s*\(([^;{]*?)\)\s*;", src, re.M):
+        params = [x for x in m.group(2).split(",") if x.strip() and x.strip() != "void"]
+        want = [_ctype_of(x) for x in params]
+        got = [kind.get(t, repr(t)) for t in SIGNATURES[m.group(1)][1]]
+        if want != got:
+            bad.append((m.group(1), want, got))
+    assert bad == []
