@@ -112,3 +112,18 @@ def test_python_binding_types_match_header():
         if want != got:
             bad.append((m.group(1), want, got))
     assert bad == []
+
+
+def test_python_constants_match_header_enums():
+    """Status codes, memory kinds, row orders and profiler kernel kinds: the Python side's
+    numbers are the header's."""
+    from paper_2508_11553_b200 import _lib
+    from paper_2508_11553_b200.store import DeviceStore
+
+    src = re.sub(r"/\*.*?\*/", " ", open(HEADER).read(), flags=re.S)
+    enums = {k: int(v) for k, v in re.findall(r"\b(TM_[A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    for name in ("TM_OK", "TM_EINVAL", "TM_ENOENT", "TM_ENOMEM", "TM_ECUDA", "TM_MEM_HOST", "TM_MEM_DEVICE",
+                 "TM_ORDER_INSERT", "TM_ORDER_LEX"):
+        assert getattr(_lib, name) == enums[name], name
+    kernels = {k[len("TM_KERNEL_"):].lower(): v for k, v in enums.items() if k.startswith("TM_KERNEL_")}
+    assert DeviceStore.KERNELS == kernels
