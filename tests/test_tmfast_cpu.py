@@ -63,3 +63,27 @@ def test_pack_i32_and_pack_lists():
         assert np.array_equal(tok, np.concatenate([np.asarray(r, np.int32) for r in rows]))
     with pytest.raises(ValueError):
         _tmfast.pack_lists([[1, 2], [2**40]], 2)
+
+
+def test_meta_runs_fast_path_equals_python_path(monkeypatch):
+    """trie.meta_runs with the extension and with its pure-Python path (lists, tuples,
+    numpy integer versions, this package's enum and bools) give the same runs."""
+    from paper_2508_11553_b200 import trie as T
+
+    rng = np.random.default_rng(13)
+    for trial in range(600):
+        n = int(rng.integers(1, 200))
+        o = rng.integers(0, 2, n)
+        if rng.random() < 0.6:
+            o = np.resize(np.repeat(o[: max(1, n // 10)], 10), n)
+        v = np.cumsum(rng.random(n) < 0.1).astype(np.int64)
+        origins = [OUT if x else IN for x in o] if trial % 2 else [bool(x) for x in o]
+        versions = [int(x) for x in v] if trial % 3 else [np.int64(x) for x in v]
+        if trial % 4 == 1:
+            origins, versions = tuple(origins), tuple(versions)
+        fast = T.meta_runs(origins, versions)
+        monkeypatch.setattr(T, "_tmfast", None)
+        slow = T.meta_runs(origins, versions)
+        monkeypatch.setattr(T, "_tmfast", _tmfast)
+        for f, s in zip(fast, slow):
+            assert np.array_equal(np.asarray(f, np.int64), np.asarray(s, np.int64)), trial
